@@ -1,0 +1,523 @@
+// abq/abq.hpp -- C++ drop-in mirror of the reference operator API for the
+// bit-plane quantized matmul hot path, backed by the sm_100a engine through
+// the C-ABI in abq_cuda.h (libabq_cuda.so).
+//
+// Same namespace, type names, signatures, value semantics and exception
+// classes as the reference headers (paths relative to /root/reference/proj):
+//   core.hpp:13-70, 113-145   Error hierarchy, Matrix<T>, Mat/CodeMat/IntMat, Rng
+//   quantizer.hpp:14-224      Scheme, Granularity, QuantSpec, CompensationPair,
+//                             QuantizedTensor, quantize, quantize_balanced
+//   bitplane.hpp:15-96        BitPlaneMatrix, bitpack, unpack, bmma
+//   gemm.hpp:19-307           TileConfig, default_tile, GemmStats, fits_int32,
+//                             engine_threads, gemm_arbitrary(_wide), gemm_naive,
+//                             zero_point_correct, code_rowsums, quantized_linear
+//   tune.hpp:17-23            padding_redundancy
+// Host containers in, host containers out (the reference's contract): each
+// call stages its operands in HBM, runs the kernels, and copies the result
+// back.  Nothing numeric is computed on the host.  The device-resident API
+// (abq::device::Weights / abq::device::Linear) keeps packed weights in HBM
+// across calls for the serving path.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <optional>
+#include <random>
+#include <sstream>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "abq_cuda.h"
+
+namespace abq {
+
+// ---- errors (core.hpp:13-36) ------------------------------------------------
+class Error : public std::runtime_error {
+ public:
+  explicit Error(const std::string& m) : std::runtime_error(m) {}
+};
+class ShapeError : public Error {
+ public:
+  explicit ShapeError(const std::string& m) : Error(m) {}
+};
+class ValueError : public Error {
+ public:
+  explicit ValueError(const std::string& m) : Error(m) {}
+};
+class OverflowError : public Error {
+ public:
+  explicit OverflowError(const std::string& m) : Error(m) {}
+};
+class IoError : public Error {
+ public:
+  explicit IoError(const std::string& m) : Error(m) {}
+};
+
+namespace detail {
+inline void check(int status) {
+  if (status == ABQ_OK) return;
+  const std::string msg = abq_last_error();
+  switch (status) {
+    case ABQ_ERR_SHAPE: throw ShapeError(msg);
+    case ABQ_ERR_VALUE: throw ValueError(msg);
+    case ABQ_ERR_OVERFLOW: throw OverflowError(msg);
+    case ABQ_ERR_IO: throw IoError(msg);
+    default: throw Error(msg);
+  }
+}
+inline void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw Error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// RAII device buffer used to stage host operands in HBM.
+template <typename T>
+class DeviceBuffer {
+ public:
+  DeviceBuffer() = default;
+  explicit DeviceBuffer(std::size_t n) : n_(n) {
+    if (n) cuda_check(cudaMalloc(&p_, n * sizeof(T)), "cudaMalloc");
+  }
+  DeviceBuffer(const T* host, std::size_t n) : DeviceBuffer(n) {
+    if (n) cuda_check(cudaMemcpy(p_, host, n * sizeof(T), cudaMemcpyHostToDevice), "cudaMemcpy H2D");
+  }
+  explicit DeviceBuffer(const std::vector<T>& v) : DeviceBuffer(v.data(), v.size()) {}
+  DeviceBuffer(const DeviceBuffer&) = delete;
+  DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+  DeviceBuffer(DeviceBuffer&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr; o.n_ = 0; }
+  DeviceBuffer& operator=(DeviceBuffer&& o) noexcept {
+    std::swap(p_, o.p_);
+    std::swap(n_, o.n_);
+    return *this;
+  }
+  ~DeviceBuffer() {
+    if (p_) cudaFree(p_);
+  }
+  T* get() const { return p_; }
+  std::size_t size() const { return n_; }
+  void to_host(T* host) const {
+    if (n_) cuda_check(cudaMemcpy(host, p_, n_ * sizeof(T), cudaMemcpyDeviceToHost), "cudaMemcpy D2H");
+  }
+
+ private:
+  T* p_ = nullptr;
+  std::size_t n_ = 0;
+};
+}  // namespace detail
+
+// ---- core containers (core.hpp:39-70) ---------------------------------------
+template <typename T>
+struct Matrix {
+  std::size_t rows = 0;
+  std::size_t cols = 0;
+  std::vector<T> data;
+
+  Matrix() = default;
+  Matrix(std::size_t r, std::size_t c, T fill = T{}) : rows(r), cols(c), data(r * c, fill) {}
+  T& operator()(std::size_t i, std::size_t j) { return data[i * cols + j]; }
+  const T& operator()(std::size_t i, std::size_t j) const { return data[i * cols + j]; }
+  std::size_t size() const { return rows * cols; }
+  bool same_shape(const Matrix& o) const { return rows == o.rows && cols == o.cols; }
+  bool operator==(const Matrix& o) const { return same_shape(o) && data == o.data; }
+};
+
+using Mat = Matrix<double>;
+using CodeMat = Matrix<std::uint8_t>;
+using IntMat = Matrix<std::int64_t>;
+
+/// Seeded generator with the reference's distributions (core.hpp:113-142), so
+/// seeded test cases replay the reference's inputs draw for draw.
+class Rng {
+ public:
+  explicit Rng(std::uint64_t seed) : gen_(seed) {}
+  double gauss(double mean = 0.0, double stddev = 1.0) {
+    return std::normal_distribution<double>(mean, stddev)(gen_);
+  }
+  double uniform(double lo, double hi) { return std::uniform_real_distribution<double>(lo, hi)(gen_); }
+  std::uint64_t integer(std::uint64_t lo, std::uint64_t hi) {
+    return std::uniform_int_distribution<std::uint64_t>(lo, hi)(gen_);
+  }
+  Mat gauss_matrix(std::size_t r, std::size_t c, double stddev = 1.0) {
+    Mat m(r, c);
+    for (auto& v : m.data) v = gauss(0.0, stddev);
+    return m;
+  }
+  CodeMat code_matrix(std::size_t r, std::size_t c, unsigned bits) {
+    CodeMat m(r, c);
+    for (auto& v : m.data) v = static_cast<std::uint8_t>(integer(0, (1u << bits) - 1));
+    return m;
+  }
+
+ private:
+  std::mt19937_64 gen_;
+};
+
+// ---- quantizer types (quantizer.hpp:14-107) ---------------------------------
+enum class Scheme : std::uint8_t { Asymmetric = 0, Symmetric = 1, Balanced = 2 };
+enum class Granularity : std::uint8_t { PerTensor = 0, PerChannel = 1, PerToken = 2 };
+
+struct QuantSpec {
+  unsigned bits = 8;
+  Scheme scheme = Scheme::Asymmetric;
+  Granularity granularity = Granularity::PerTensor;
+  double alpha = 1.0;
+  double beta = 1.0;
+  std::vector<double> balance_scale;
+
+  bool passthrough() const { return bits >= 16; }
+  abq_quant_spec c_spec() const {
+    return abq_quant_spec{bits, int(scheme), int(granularity), alpha, beta};
+  }
+  unsigned levels() const {
+    abq_quant_spec s = c_spec();
+    return abq_spec_levels(&s);
+  }
+  unsigned planes() const {
+    abq_quant_spec s = c_spec();
+    return abq_spec_planes(&s);
+  }
+  void validate() const {
+    if (bits < 1 || (bits > 8 && !passthrough()))
+      throw ValueError("QuantSpec: bits must be in [1,8] (or >=16 for passthrough)");
+    if (scheme == Scheme::Balanced && bits > 7 && !passthrough())
+      throw ValueError("QuantSpec: balanced codes reach 2^bits and must fit one byte, so bits <= 7");
+    if (!(alpha > 0.0 && alpha <= 1.0)) throw ValueError("QuantSpec: alpha must be in (0,1]");
+    if (!(beta > 0.0 && beta <= 1.0)) throw ValueError("QuantSpec: beta must be in (0,1]");
+    for (double s : balance_scale)
+      if (!(s > 0.0)) throw ValueError("QuantSpec: balance_scale entries must be positive");
+  }
+};
+
+struct CompensationPair {
+  std::vector<double> a;
+  std::vector<double> b;
+};
+
+struct QuantizedTensor {
+  CodeMat codes;
+  std::vector<double> scales;
+  std::vector<std::int32_t> zero_points;
+  QuantSpec spec;
+
+  std::size_t rows() const { return codes.rows; }
+  std::size_t cols() const { return codes.cols; }
+  std::size_t axis_count() const { return scales.size(); }
+  std::size_t axis_of(std::size_t i, std::size_t) const {
+    return spec.granularity == Granularity::PerTensor ? 0 : i;
+  }
+};
+
+// ---- bit planes (bitplane.hpp:15-44) ---------------------------------------
+struct BitPlaneMatrix {
+  unsigned planes = 0;
+  std::size_t rows = 0;
+  std::size_t cols = 0;
+  std::size_t words_per_row = 0;
+  std::vector<std::uint64_t> data;  // [plane][row][word]
+
+  BitPlaneMatrix() = default;
+  BitPlaneMatrix(unsigned p, std::size_t r, std::size_t c)
+      : planes(p), rows(r), cols(c), words_per_row((c + 63) / 64),
+        data(std::size_t(p) * r * ((c + 63) / 64), 0) {}
+  const std::uint64_t* row(unsigned plane, std::size_t r) const {
+    return data.data() + (std::size_t(plane) * rows + r) * words_per_row;
+  }
+  bool bit(unsigned plane, std::size_t r, std::size_t c) const {
+    return (row(plane, r)[c / 64] >> (c % 64)) & 1u;
+  }
+  bool operator==(const BitPlaneMatrix& o) const {
+    return planes == o.planes && rows == o.rows && cols == o.cols && data == o.data;
+  }
+};
+
+// ---- engine types (gemm.hpp:19-84) ------------------------------------------
+struct TileConfig {
+  std::size_t BM = 64, BN = 64, BK = 512;
+  std::size_t WM = 64, WN = 64, WK = 128;
+  static constexpr std::size_t mma_m = 8, mma_n = 8, mma_k = 128;
+
+  abq_tile_config c_tile() const { return abq_tile_config{BM, BN, BK, WM, WN, WK}; }
+  bool valid(unsigned p, unsigned q) const {
+    abq_tile_config t = c_tile();
+    return abq_tile_valid(&t, p, q) != 0;
+  }
+  std::string describe() const {
+    std::ostringstream os;
+    os << "BM" << BM << "_BN" << BN << "_BK" << BK << "_WM" << WM << "_WN" << WN;
+    return os.str();
+  }
+  void require_valid(unsigned p, unsigned q) const {
+    if (!valid(p, q)) {
+      std::ostringstream os;
+      os << "TileConfig invalid for p=" << p << " q=" << q << ": BM=" << BM << " BN=" << BN
+         << " BK=" << BK << " WM=" << WM << " WN=" << WN << " WK=" << WK;
+      throw ValueError(os.str());
+    }
+  }
+};
+
+inline TileConfig default_tile(unsigned p, unsigned q) {
+  abq_tile_config t = abq_default_tile(p, q);
+  return TileConfig{t.BM, t.BN, t.BK, t.WM, t.WN, t.WK};
+}
+
+struct GemmStats {
+  std::uint64_t block_tiles = 0;
+  std::uint64_t plane_pair_products = 0;
+};
+
+inline bool fits_int32(unsigned p, unsigned q, std::size_t k) { return abq_fits_int32(p, q, k) != 0; }
+
+/// Process-global knob kept for API parity (gemm.hpp:81-84); the GPU engine's
+/// results never depend on it.
+inline unsigned& engine_threads() {
+  static unsigned n = 0;
+  return n;
+}
+
+inline double padding_redundancy(std::size_t m, unsigned p, std::size_t mma_m) {
+  double out = 0.0;
+  detail::check(abq_padding_redundancy(m, p, mma_m, &out));
+  return out;
+}
+
+// ---- L2 entry points ---------------------------------------------------------
+inline BitPlaneMatrix bitpack(const CodeMat& codes, unsigned bits) {
+  if (bits < 1 || bits > 8) throw ValueError("bitpack: plane count must be in [1,8]");
+  BitPlaneMatrix out(bits, codes.rows, codes.cols);
+  detail::DeviceBuffer<std::uint8_t> dc(codes.data);
+  detail::DeviceBuffer<std::uint64_t> dp(out.data.size());
+  detail::check(abq_bitpack(dc.get(), codes.rows, codes.cols, bits, dp.get(), nullptr));
+  dp.to_host(out.data.data());
+  return out;
+}
+
+inline CodeMat unpack(const BitPlaneMatrix& m) {
+  CodeMat codes(m.rows, m.cols);
+  detail::DeviceBuffer<std::uint64_t> dp(m.data);
+  detail::DeviceBuffer<std::uint8_t> dc(codes.data.size());
+  detail::check(abq_unpack(dp.get(), m.planes, m.rows, m.cols, dc.get(), nullptr));
+  dc.to_host(codes.data.data());
+  return codes;
+}
+
+inline Matrix<std::int32_t> bmma(const BitPlaneMatrix& a, unsigned a_plane, const BitPlaneMatrix& bt,
+                                 unsigned b_plane) {
+  if (a.cols != bt.cols) throw ShapeError("bmma: shared K dimension differs");
+  Matrix<std::int32_t> out(a.rows, bt.rows, 0);
+  detail::DeviceBuffer<std::uint64_t> da(a.data), db(bt.data);
+  detail::DeviceBuffer<std::int32_t> dout(out.data.size());
+  detail::check(abq_bmma(da.get(), a.planes, a.rows, a_plane, db.get(), bt.planes, bt.rows, b_plane,
+                         a.cols, dout.get(), nullptr));
+  dout.to_host(out.data.data());
+  return out;
+}
+
+// ---- L3 entry points ---------------------------------------------------------
+inline Matrix<std::int32_t> gemm_arbitrary(const BitPlaneMatrix& a, const BitPlaneMatrix& bt,
+                                           const TileConfig& tile, GemmStats* stats = nullptr) {
+  Matrix<std::int32_t> out(a.rows, bt.rows, 0);
+  detail::DeviceBuffer<std::uint64_t> da(a.data), db(bt.data);
+  detail::DeviceBuffer<std::int32_t> dout(out.data.size());
+  abq_tile_config t = tile.c_tile();
+  abq_gemm_stats st{stats ? stats->block_tiles : 0, stats ? stats->plane_pair_products : 0};
+  detail::check(abq_gemm_arbitrary(da.get(), a.planes, a.rows, a.cols, db.get(), bt.planes, bt.rows,
+                                   bt.cols, &t, dout.get(), &st, nullptr));
+  dout.to_host(out.data.data());
+  if (stats) *stats = GemmStats{st.block_tiles, st.plane_pair_products};
+  return out;
+}
+
+inline Matrix<std::int64_t> gemm_arbitrary_wide(const BitPlaneMatrix& a, const BitPlaneMatrix& bt,
+                                                const TileConfig& tile, GemmStats* stats = nullptr) {
+  Matrix<std::int64_t> out(a.rows, bt.rows, 0);
+  detail::DeviceBuffer<std::uint64_t> da(a.data), db(bt.data);
+  detail::DeviceBuffer<std::int64_t> dout(out.data.size());
+  abq_tile_config t = tile.c_tile();
+  abq_gemm_stats st{stats ? stats->block_tiles : 0, stats ? stats->plane_pair_products : 0};
+  detail::check(abq_gemm_arbitrary_wide(da.get(), a.planes, a.rows, a.cols, db.get(), bt.planes,
+                                        bt.rows, bt.cols, &t, dout.get(), &st, nullptr));
+  dout.to_host(out.data.data());
+  if (stats) *stats = GemmStats{st.block_tiles, st.plane_pair_products};
+  return out;
+}
+
+inline Matrix<std::int32_t> gemm_naive(const BitPlaneMatrix& a, const BitPlaneMatrix& bt) {
+  Matrix<std::int32_t> out(a.rows, bt.rows, 0);
+  detail::DeviceBuffer<std::uint64_t> da(a.data), db(bt.data);
+  detail::DeviceBuffer<std::int32_t> dout(out.data.size());
+  detail::check(abq_gemm_naive(da.get(), a.planes, a.rows, a.cols, db.get(), bt.planes, bt.rows,
+                               bt.cols, dout.get(), nullptr));
+  dout.to_host(out.data.data());
+  return out;
+}
+
+template <typename Acc>
+inline Matrix<Acc> zero_point_correct(const Matrix<Acc>& acc, const std::vector<std::int64_t>& rowsum_a,
+                                      const std::vector<std::int64_t>& colsum_b,
+                                      const std::vector<std::int32_t>& z_a,
+                                      const std::vector<std::int32_t>& z_b, std::size_t k) {
+  static_assert(sizeof(Acc) == 4 || sizeof(Acc) == 8, "int32 or int64 accumulators");
+  if (rowsum_a.size() != acc.rows || z_a.size() != acc.rows)
+    throw ShapeError("zero_point_correct: row-side vectors do not match");
+  if (colsum_b.size() != acc.cols || z_b.size() != acc.cols)
+    throw ShapeError("zero_point_correct: col-side vectors do not match");
+  Matrix<Acc> out(acc.rows, acc.cols);
+  detail::DeviceBuffer<Acc> dacc(acc.data), dout(out.data.size());
+  detail::DeviceBuffer<std::int64_t> dra(rowsum_a), dcb(colsum_b);
+  detail::DeviceBuffer<std::int32_t> dza(z_a), dzb(z_b);
+  if constexpr (sizeof(Acc) == 4)
+    detail::check(abq_zero_point_correct_i32(reinterpret_cast<const std::int32_t*>(dacc.get()),
+                                             acc.rows, acc.cols, dra.get(), dcb.get(), dza.get(),
+                                             dzb.get(), k, reinterpret_cast<std::int32_t*>(dout.get()),
+                                             nullptr));
+  else
+    detail::check(abq_zero_point_correct_i64(reinterpret_cast<const std::int64_t*>(dacc.get()),
+                                             acc.rows, acc.cols, dra.get(), dcb.get(), dza.get(),
+                                             dzb.get(), k, reinterpret_cast<std::int64_t*>(dout.get()),
+                                             nullptr));
+  dout.to_host(out.data.data());
+  return out;
+}
+
+inline std::vector<std::int64_t> code_rowsums(const CodeMat& codes) {
+  std::vector<std::int64_t> sums(codes.rows, 0);
+  detail::DeviceBuffer<std::uint8_t> dc(codes.data);
+  detail::DeviceBuffer<std::int64_t> ds(sums.size());
+  detail::check(abq_code_rowsums(dc.get(), codes.rows, codes.cols, ds.get(), nullptr));
+  ds.to_host(sums.data());
+  return sums;
+}
+
+// ---- L1: quantize (quantizer.hpp:146-224) ------------------------------------
+inline QuantizedTensor quantize(const Mat& x, const QuantSpec& spec,
+                                const std::optional<CompensationPair>& comp = std::nullopt) {
+  spec.validate();
+  if (spec.passthrough()) throw ValueError("quantize: passthrough spec cannot be materialized");
+  QuantizedTensor q;
+  q.spec = spec;
+  q.codes = CodeMat(x.rows, x.cols);
+  const std::size_t groups = spec.granularity == Granularity::PerTensor ? 1 : x.rows;
+  q.scales.resize(groups);
+  q.zero_points.resize(groups);
+  detail::DeviceBuffer<double> dx(x.data);
+  detail::DeviceBuffer<double> da, db;
+  if (comp) {
+    if (comp->a.size() != x.rows || comp->b.size() != x.cols)
+      throw ShapeError("quantize: compensation pair does not match matrix shape");
+    da = detail::DeviceBuffer<double>(comp->a);
+    db = detail::DeviceBuffer<double>(comp->b);
+  }
+  detail::DeviceBuffer<std::uint8_t> dc(q.codes.data.size());
+  detail::DeviceBuffer<double> ds(groups);
+  detail::DeviceBuffer<std::int32_t> dz(groups);
+  abq_quant_spec cs = spec.c_spec();
+  detail::check(abq_quantize(dx.get(), ABQ_F64, x.rows, x.cols, &cs, comp ? da.get() : nullptr,
+                             comp ? db.get() : nullptr, dc.get(), ds.get(), dz.get(), nullptr));
+  dc.to_host(q.codes.data.data());
+  ds.to_host(q.scales.data());
+  dz.to_host(q.zero_points.data());
+  return q;
+}
+
+inline QuantizedTensor quantize_balanced(const Mat& x, unsigned bits,
+                                         Granularity granularity = Granularity::PerTensor) {
+  QuantSpec spec;
+  spec.bits = bits;
+  spec.scheme = Scheme::Balanced;
+  spec.granularity = granularity;
+  return quantize(x, spec);
+}
+
+// ---- engine path linear (gemm.hpp:266-307) ------------------------------------
+inline Mat quantized_linear(const QuantizedTensor& act, const QuantizedTensor& wt,
+                            GemmStats* stats = nullptr) {
+  if (act.cols() != wt.cols()) throw ShapeError("quantized_linear: inner dimensions differ");
+  const std::size_t k = act.cols();
+  const unsigned p = act.spec.planes(), q = wt.spec.planes();
+  const std::size_t m = act.rows(), n = wt.rows();
+  detail::DeviceBuffer<std::uint8_t> dac(act.codes.data), dwc(wt.codes.data);
+  detail::DeviceBuffer<std::uint64_t> dap(std::size_t(p) * m * ((k + 63) / 64));
+  detail::DeviceBuffer<std::uint64_t> dwp(std::size_t(q) * n * ((k + 63) / 64));
+  detail::check(abq_bitpack(dac.get(), m, k, p, dap.get(), nullptr));
+  detail::check(abq_bitpack(dwc.get(), n, k, q, dwp.get(), nullptr));
+  detail::DeviceBuffer<std::int64_t> dra(m), dcb(n);
+  detail::check(abq_code_rowsums(dac.get(), m, k, dra.get(), nullptr));
+  detail::check(abq_plane_rowsums(dwp.get(), q, n, k, dcb.get(), nullptr));
+  detail::DeviceBuffer<double> dsa(act.scales), dsb(wt.scales);
+  detail::DeviceBuffer<std::int32_t> dza(act.zero_points), dzb(wt.zero_points);
+  abq_act a{dap.get(), p, m, k, dsa.get(), dza.get(), dra.get(),
+            act.spec.granularity == Granularity::PerTensor};
+  abq_weights w{dwp.get(), q, n, k, dsb.get(), dzb.get(), dcb.get(),
+                wt.spec.granularity == Granularity::PerTensor};
+  Mat out(m, n);
+  detail::DeviceBuffer<double> dy(out.data.size());
+  detail::check(abq_linear_planes(&a, &w, dy.get(), ABQ_OUT_F64, nullptr));
+  dy.to_host(out.data.data());
+  if (stats) {
+    const TileConfig t = default_tile(p, q);
+    const std::uint64_t tiles = std::uint64_t((m + t.BM - 1) / t.BM) * ((n + t.BN - 1) / t.BN);
+    stats->block_tiles += tiles;
+    stats->plane_pair_products += tiles * p * q;
+  }
+  return out;
+}
+
+// ---- device-resident serving API (additions, SURVEY.md 8b "Ownership") -------
+namespace device {
+
+/// Weights packed once and kept in HBM: ABQP planes + per-channel metadata.
+class Weights {
+ public:
+  explicit Weights(const QuantizedTensor& wt)
+      : q_(wt.spec.planes()), n_(wt.rows()), k_(wt.cols()),
+        per_tensor_(wt.spec.granularity == Granularity::PerTensor),
+        planes_(std::size_t(q_) * n_ * ((k_ + 63) / 64)), scales_(wt.scales),
+        zps_(wt.zero_points), colsums_(n_) {
+    detail::DeviceBuffer<std::uint8_t> dc(wt.codes.data);
+    detail::check(abq_bitpack(dc.get(), n_, k_, q_, planes_.get(), nullptr));
+    detail::check(abq_plane_rowsums(planes_.get(), q_, n_, k_, colsums_.get(), nullptr));
+  }
+  abq_weights view() const {
+    return abq_weights{planes_.get(), q_, n_, k_, scales_.get(), zps_.get(), colsums_.get(),
+                       per_tensor_ ? 1 : 0};
+  }
+  std::size_t n() const { return n_; }
+  std::size_t k() const { return k_; }
+
+ private:
+  unsigned q_;
+  std::size_t n_, k_;
+  bool per_tensor_;
+  detail::DeviceBuffer<std::uint64_t> planes_;
+  detail::DeviceBuffer<double> scales_;
+  detail::DeviceBuffer<std::int32_t> zps_;
+  detail::DeviceBuffer<std::int64_t> colsums_;
+};
+
+/// ReQuant + BitPacking + plane GEMV/GEMM + fused epilogue on device pointers.
+class Linear {
+ public:
+  Linear(const Weights& w, const QuantSpec& act_spec, std::size_t max_m)
+      : w_(w.view()), spec_(act_spec.c_spec()), max_m_(max_m),
+        ws_bytes_(abq_linear_workspace_bytes(max_m, w.k(), act_spec.planes())), ws_(ws_bytes_) {
+    act_spec.validate();
+  }
+  /// x: device [m][k] (x_dtype ABQ_F16/F32/F64); y: device [m][n] of out_kind.
+  void operator()(const void* x, int x_dtype, std::size_t m, void* y, int out_kind,
+                  cudaStream_t stream = nullptr, std::int64_t* err_index = nullptr) const {
+    if (m > max_m_) throw ValueError("device::Linear: m exceeds max_m");
+    detail::check(abq_linear(x, x_dtype, m, w_.k, &spec_, &w_, y, out_kind, ws_.get(), ws_bytes_,
+                             err_index, stream));
+  }
+
+ private:
+  abq_weights w_;
+  abq_quant_spec spec_;
+  std::size_t max_m_, ws_bytes_;
+  detail::DeviceBuffer<std::uint8_t> ws_;
+};
+
+}  // namespace device
+}  // namespace abq

@@ -1,0 +1,502 @@
+"""Python mirror of the reference operator API for the hot path.
+
+Same names, argument meaning and error behaviour as the reference's C++
+functions in namespace ``abq`` (paths relative to /root/reference/proj):
+
+  core.hpp:13-36        Error / ShapeError / ValueError / OverflowError / IoError
+  quantizer.hpp:37-254  QuantSpec, QuantizedTensor, quantize, quantize_balanced, dequantize*
+  bitplane.hpp:15-96    BitPlaneMatrix, bitpack, unpack, bmma
+  gemm.hpp:19-307       TileConfig, default_tile, GemmStats, fits_int32, engine_threads,
+                        gemm_arbitrary(_wide), gemm_naive, zero_point_correct,
+                        code_rowsums, quantized_linear
+  tune.hpp:17-23        padding_redundancy
+
+Every numeric result is computed by the sm_100a kernels behind the C-ABI
+(include/abq_cuda.h); tensors live on the GPU (torch CUDA storage is used for
+device memory and streams only).  (*) dequantize is the reference's inverse
+map and runs as a plain elementwise torch op on the device.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib as L
+
+# ---------------------------------------------------------------------------
+# errors (core.hpp:13-36)
+# ---------------------------------------------------------------------------
+
+
+class Error(RuntimeError):
+    pass
+
+
+class ShapeError(Error):
+    pass
+
+
+class ValueError(Error, ValueError):  # noqa: A001 - mirrors abq::ValueError
+    pass
+
+
+class OverflowError(Error, OverflowError):  # noqa: A001 - mirrors abq::OverflowError
+    pass
+
+
+class IoError(Error):
+    pass
+
+
+class CudaError(Error):
+    pass
+
+
+_STATUS = {L.ABQ_ERR_SHAPE: ShapeError, L.ABQ_ERR_VALUE: ValueError,
+           L.ABQ_ERR_OVERFLOW: OverflowError, L.ABQ_ERR_IO: IoError, L.ABQ_ERR_CUDA: CudaError}
+
+
+def _check(status: int) -> None:
+    if status != L.ABQ_OK:
+        msg = L.lib().abq_last_error().decode()
+        raise _STATUS.get(status, Error)(msg)
+
+
+def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("engine tensors must live on the GPU")
+    return t.data_ptr()
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _dev() -> torch.device:
+    if not torch.cuda.is_available():
+        raise CudaError("abq: no CUDA device available; the engine has no CPU path")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _to_dev(x, dtype) -> torch.Tensor:
+    if isinstance(x, np.ndarray):
+        x = torch.from_numpy(np.ascontiguousarray(x))
+    return x.to(device=_dev(), dtype=dtype).contiguous()
+
+
+# ---------------------------------------------------------------------------
+# quantizer (quantizer.hpp)
+# ---------------------------------------------------------------------------
+ASYMMETRIC, SYMMETRIC, BALANCED = L.ABQ_ASYMMETRIC, L.ABQ_SYMMETRIC, L.ABQ_BALANCED
+PER_TENSOR, PER_CHANNEL, PER_TOKEN = L.ABQ_PER_TENSOR, L.ABQ_PER_CHANNEL, L.ABQ_PER_TOKEN
+
+
+@dataclasses.dataclass
+class QuantSpec:
+    """QuantSpec  quantizer.hpp:37-71."""
+    bits: int = 8
+    scheme: int = ASYMMETRIC
+    granularity: int = PER_TENSOR
+    alpha: float = 1.0
+    beta: float = 1.0
+
+    def passthrough(self) -> bool:
+        return self.bits >= 16
+
+    def levels(self) -> int:
+        return (1 << self.bits) + 1 if self.scheme == BALANCED else (1 << self.bits)
+
+    def planes(self) -> int:
+        lv, p = self.levels(), 0
+        while (1 << p) < lv:
+            p += 1
+        return p
+
+    def validate(self) -> None:
+        if self.bits < 1 or (self.bits > 8 and not self.passthrough()):
+            raise ValueError("QuantSpec: bits must be in [1,8] (or >=16 for passthrough)")
+        if self.scheme == BALANCED and self.bits > 7 and not self.passthrough():
+            raise ValueError("QuantSpec: balanced codes reach 2^bits and must fit one byte, so bits <= 7")
+        if not (0.0 < self.alpha <= 1.0):
+            raise ValueError("QuantSpec: alpha must be in (0,1]")
+        if not (0.0 < self.beta <= 1.0):
+            raise ValueError("QuantSpec: beta must be in (0,1]")
+
+    def c(self) -> L.QuantSpecC:
+        return L.QuantSpecC(self.bits, self.scheme, self.granularity, self.alpha, self.beta)
+
+
+@dataclasses.dataclass
+class QuantizedTensor:
+    """QuantizedTensor  quantizer.hpp:81-107 (device tensors)."""
+    codes: torch.Tensor          # uint8 rows x cols
+    scales: torch.Tensor         # float64, 1 or rows
+    zero_points: torch.Tensor    # int32, 1 or rows
+    spec: QuantSpec
+
+    def rows(self) -> int:
+        return self.codes.shape[0]
+
+    def cols(self) -> int:
+        return self.codes.shape[1]
+
+    def axis_of(self, i: int, j: int = 0) -> int:
+        return 0 if self.spec.granularity == PER_TENSOR else i
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.float16:
+        return L.ABQ_F16
+    if t.dtype == torch.float64:
+        return L.ABQ_F64
+    if t.dtype == torch.float32:
+        return L.ABQ_F32
+    raise ValueError(f"quantize: unsupported dtype {t.dtype}")
+
+
+def quantize(x, spec: QuantSpec, comp: Optional[tuple] = None) -> QuantizedTensor:
+    """quantize  quantizer.hpp:146-213 on the GPU (bit-exact FP64)."""
+    spec.validate()
+    if spec.passthrough():
+        raise ValueError("quantize: passthrough spec cannot be materialized")
+    if isinstance(x, np.ndarray):
+        x = torch.from_numpy(np.ascontiguousarray(x))
+    if x.dtype not in (torch.float16, torch.float32, torch.float64):
+        x = x.to(torch.float64)
+    x = x.to(_dev()).contiguous()
+    rows, cols = x.shape
+    ca = cb = None
+    if comp is not None:
+        a, b = comp
+        ca, cb = _to_dev(a, torch.float64), _to_dev(b, torch.float64)
+        if ca.numel() != rows or cb.numel() != cols:
+            raise ShapeError("quantize: compensation pair does not match matrix shape")
+    groups = 1 if spec.granularity == PER_TENSOR else rows
+    codes = torch.empty((rows, cols), dtype=torch.uint8, device=x.device)
+    scales = torch.empty(groups, dtype=torch.float64, device=x.device)
+    zps = torch.empty(groups, dtype=torch.int32, device=x.device)
+    cs = spec.c()
+    _check(L.lib().abq_quantize(_ptr(x), _dtype_code(x), rows, cols, C.byref(cs), _ptr(ca), _ptr(cb),
+                                _ptr(codes), _ptr(scales), _ptr(zps), _stream()))
+    return QuantizedTensor(codes, scales, zps, dataclasses.replace(spec))
+
+
+def quantize_balanced(x, bits: int, granularity: int = PER_TENSOR) -> QuantizedTensor:
+    """quantize_balanced  quantizer.hpp:217-224."""
+    return quantize(x, QuantSpec(bits=bits, scheme=BALANCED, granularity=granularity))
+
+
+def dequantize(q: QuantizedTensor) -> torch.Tensor:
+    """dequantize  quantizer.hpp:243-254: (code - z) * step in FP64."""
+    idx = 0 if q.spec.granularity == PER_TENSOR else slice(None)
+    s = q.scales[idx].reshape(-1, 1) if idx != 0 else q.scales[0]
+    z = q.zero_points[idx].reshape(-1, 1).double() if idx != 0 else q.zero_points[0].double()
+    return (q.codes.double() - z) * s
+
+
+# ---------------------------------------------------------------------------
+# bit planes (bitplane.hpp)
+# ---------------------------------------------------------------------------
+@dataclasses.dataclass
+class BitPlaneMatrix:
+    """BitPlaneMatrix  bitplane.hpp:15-44: data is [planes][rows][words_per_row]
+    u64 words (stored in an int64 CUDA tensor), LSB-first, tail bits zero."""
+    planes: int
+    rows: int
+    cols: int
+    data: torch.Tensor
+
+    @property
+    def words_per_row(self) -> int:
+        return (self.cols + 63) // 64
+
+    @staticmethod
+    def from_numpy(words: np.ndarray, cols: int) -> "BitPlaneMatrix":
+        p, r, _ = words.shape
+        return BitPlaneMatrix(p, r, cols, _to_dev(words.view(np.int64), torch.int64))
+
+    def numpy(self) -> np.ndarray:
+        return self.data.cpu().numpy().view(np.uint64)
+
+    def __eq__(self, o) -> bool:
+        return (self.planes, self.rows, self.cols) == (o.planes, o.rows, o.cols) and bool(
+            torch.equal(self.data, o.data))
+
+
+def _empty_planes(bits: int, rows: int, cols: int) -> torch.Tensor:
+    return torch.empty((bits, rows, (cols + 63) // 64), dtype=torch.int64, device=_dev())
+
+
+def bitpack(codes, bits: int) -> BitPlaneMatrix:
+    """bitpack  bitplane.hpp:47-64 ([M,K] codes -> [bits,M,K] planes)."""
+    codes = _to_dev(codes, torch.uint8)
+    rows, cols = codes.shape
+    out = _empty_planes(max(1, min(bits, 8)), rows, cols)
+    _check(L.lib().abq_bitpack(_ptr(codes), rows, cols, bits, _ptr(out), _stream()))
+    return BitPlaneMatrix(bits, rows, cols, out)
+
+
+def unpack(m: BitPlaneMatrix) -> torch.Tensor:
+    """unpack  bitplane.hpp:66-76."""
+    codes = torch.empty((m.rows, m.cols), dtype=torch.uint8, device=_dev())
+    _check(L.lib().abq_unpack(_ptr(m.data), m.planes, m.rows, m.cols, _ptr(codes), _stream()))
+    return codes
+
+
+def bmma(a: BitPlaneMatrix, a_plane: int, bt: BitPlaneMatrix, b_plane: int) -> torch.Tensor:
+    """bmma  bitplane.hpp:81-96 (single plane pair AND + popcount)."""
+    if a.cols != bt.cols:
+        raise ShapeError("bmma: shared K dimension differs")
+    out = torch.empty((a.rows, bt.rows), dtype=torch.int32, device=_dev())
+    _check(L.lib().abq_bmma(_ptr(a.data), a.planes, a.rows, a_plane, _ptr(bt.data), bt.planes,
+                            bt.rows, b_plane, a.cols, _ptr(out), _stream()))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# engine (gemm.hpp)
+# ---------------------------------------------------------------------------
+@dataclasses.dataclass
+class TileConfig:
+    """TileConfig  gemm.hpp:19-48."""
+    BM: int = 64
+    BN: int = 64
+    BK: int = 512
+    WM: int = 64
+    WN: int = 64
+    WK: int = 128
+    mma_m = 8
+    mma_n = 8
+    mma_k = 128
+
+    def c(self) -> L.TileConfigC:
+        return L.TileConfigC(self.BM, self.BN, self.BK, self.WM, self.WN, self.WK)
+
+    def valid(self, p: int, q: int) -> bool:
+        return bool(L.lib().abq_tile_valid(C.byref(self.c()), p, q))
+
+    def require_valid(self, p: int, q: int) -> None:
+        if not self.valid(p, q):
+            raise ValueError(
+                f"TileConfig invalid for p={p} q={q}: BM={self.BM} BN={self.BN} BK={self.BK} "
+                f"WM={self.WM} WN={self.WN} WK={self.WK}")
+
+    def describe(self) -> str:
+        return f"BM{self.BM}_BN{self.BN}_BK{self.BK}_WM{self.WM}_WN{self.WN}"
+
+
+def default_tile(p: int, q: int) -> TileConfig:
+    """default_tile  gemm.hpp:51-59."""
+    t = L.lib().abq_default_tile(p, q)
+    return TileConfig(t.BM, t.BN, t.BK, t.WM, t.WN, t.WK)
+
+
+@dataclasses.dataclass
+class GemmStats:
+    """GemmStats  gemm.hpp:61-64 (accumulated across calls)."""
+    block_tiles: int = 0
+    plane_pair_products: int = 0
+
+
+def fits_int32(p: int, q: int, k: int) -> bool:
+    """fits_int32  gemm.hpp:73-77."""
+    return bool(L.lib().abq_fits_int32(p, q, k))
+
+
+_engine_threads = [0]
+
+
+def engine_threads() -> list:
+    """engine_threads  gemm.hpp:81-84.  Kept for API parity: a process-global
+    knob whose value never changes results; the GPU engine ignores it."""
+    return _engine_threads
+
+
+def padding_redundancy(m: int, p: int, mma_m: int) -> float:
+    """padding_redundancy  tune.hpp:17-23."""
+    out = C.c_double()
+    _check(L.lib().abq_padding_redundancy(m, p, mma_m, C.byref(out)))
+    return out.value
+
+
+def _gemm(fn, name, a: BitPlaneMatrix, bt: BitPlaneMatrix, tile, stats, dtype):
+    out = torch.empty((a.rows, bt.rows), dtype=dtype, device=_dev())
+    st = L.GemmStatsC(stats.block_tiles, stats.plane_pair_products) if stats is not None else None
+    tc = tile.c() if tile is not None else None
+    _check(fn(_ptr(a.data), a.planes, a.rows, a.cols, _ptr(bt.data), bt.planes, bt.rows, bt.cols,
+              C.byref(tc) if tc is not None else None, _ptr(out),
+              C.byref(st) if st is not None else None, _stream()))
+    if stats is not None:
+        stats.block_tiles, stats.plane_pair_products = st.block_tiles, st.plane_pair_products
+    return out
+
+
+def gemm_arbitrary(a: BitPlaneMatrix, bt: BitPlaneMatrix, tile: TileConfig,
+                   stats: Optional[GemmStats] = None) -> torch.Tensor:
+    """gemm_arbitrary  gemm.hpp:185-198 -> int32 M x N."""
+    return _gemm(L.lib().abq_gemm_arbitrary, "gemm_arbitrary", a, bt, tile, stats, torch.int32)
+
+
+def gemm_arbitrary_wide(a: BitPlaneMatrix, bt: BitPlaneMatrix, tile: TileConfig,
+                        stats: Optional[GemmStats] = None) -> torch.Tensor:
+    """gemm_arbitrary_wide  gemm.hpp:201-209 -> int64 M x N."""
+    return _gemm(L.lib().abq_gemm_arbitrary_wide, "gemm_arbitrary_wide", a, bt, tile, stats,
+                 torch.int64)
+
+
+def gemm_naive(a: BitPlaneMatrix, bt: BitPlaneMatrix) -> torch.Tensor:
+    """gemm_naive  gemm.hpp:213-231."""
+    out = torch.empty((a.rows, bt.rows), dtype=torch.int32, device=_dev())
+    _check(L.lib().abq_gemm_naive(_ptr(a.data), a.planes, a.rows, a.cols, _ptr(bt.data), bt.planes,
+                                  bt.rows, bt.cols, _ptr(out), _stream()))
+    return out
+
+
+def zero_point_correct(acc: torch.Tensor, rowsum_a, colsum_b, z_a, z_b, k: int) -> torch.Tensor:
+    """zero_point_correct  gemm.hpp:235-254 (int64 arithmetic, result in acc's dtype)."""
+    m, n = acc.shape
+    ra, cb = _to_dev(rowsum_a, torch.int64), _to_dev(colsum_b, torch.int64)
+    za, zb = _to_dev(z_a, torch.int32), _to_dev(z_b, torch.int32)
+    if ra.numel() != m or za.numel() != m:
+        raise ShapeError("zero_point_correct: row-side vectors do not match")
+    if cb.numel() != n or zb.numel() != n:
+        raise ShapeError("zero_point_correct: col-side vectors do not match")
+    acc = acc.contiguous()
+    out = torch.empty_like(acc)
+    fn = L.lib().abq_zero_point_correct_i32 if acc.dtype == torch.int32 else L.lib().abq_zero_point_correct_i64
+    _check(fn(_ptr(acc), m, n, _ptr(ra), _ptr(cb), _ptr(za), _ptr(zb), k, _ptr(out), _stream()))
+    return out
+
+
+def code_rowsums(codes) -> torch.Tensor:
+    """code_rowsums  gemm.hpp:256-261."""
+    codes = _to_dev(codes, torch.uint8)
+    out = torch.empty(codes.shape[0], dtype=torch.int64, device=_dev())
+    _check(L.lib().abq_code_rowsums(_ptr(codes), codes.shape[0], codes.shape[1], _ptr(out), _stream()))
+    return out
+
+
+def plane_rowsums(m: BitPlaneMatrix) -> torch.Tensor:
+    """code row sums recovered from the planes (= code_rowsums(unpack(m)))."""
+    out = torch.empty(m.rows, dtype=torch.int64, device=_dev())
+    _check(L.lib().abq_plane_rowsums(_ptr(m.data), m.planes, m.rows, m.cols, _ptr(out), _stream()))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# device-resident weights + fused linear (the engine hot path)
+# ---------------------------------------------------------------------------
+@dataclasses.dataclass
+class PackedWeights:
+    """Offline-packed weights resident in HBM: ABQP planes + per-channel
+    scales / zero points + colsum_b.  The reference re-packs
+    these on every quantized_linear call (gemm.hpp:274-278)."""
+    planes: BitPlaneMatrix
+    scales: torch.Tensor
+    zero_points: torch.Tensor
+    colsums: torch.Tensor
+    per_tensor: bool
+
+    @staticmethod
+    def from_quantized(wt: QuantizedTensor) -> "PackedWeights":
+        pm = bitpack(wt.codes, wt.spec.planes())
+        return PackedWeights(pm, wt.scales.contiguous(), wt.zero_points.contiguous(),
+                             plane_rowsums(pm), wt.spec.granularity == PER_TENSOR)
+
+    @staticmethod
+    def from_planes(pm: BitPlaneMatrix, scales, zero_points, per_tensor=False) -> "PackedWeights":
+        return PackedWeights(pm, _to_dev(scales, torch.float64), _to_dev(zero_points, torch.int32),
+                             plane_rowsums(pm), per_tensor)
+
+    def c(self) -> L.WeightsC:
+        return L.WeightsC(_ptr(self.planes.data), self.planes.planes, self.planes.rows,
+                          self.planes.cols, _ptr(self.scales), _ptr(self.zero_points),
+                          _ptr(self.colsums), int(self.per_tensor))
+
+    def shard(self, rank: int, world: int) -> "PackedWeights":
+        """Column-parallel slice: output channels [rank*N/G, (rank+1)*N/G)
+        (SURVEY.md 8e).  Each plane contributes a contiguous row range."""
+        n = self.planes.rows
+        lo, hi = n * rank // world, n * (rank + 1) // world
+        pm = BitPlaneMatrix(self.planes.planes, hi - lo, self.planes.cols,
+                            self.planes.data[:, lo:hi, :].contiguous())
+        s = self.scales if self.per_tensor else self.scales[lo:hi].contiguous()
+        z = self.zero_points if self.per_tensor else self.zero_points[lo:hi].contiguous()
+        return PackedWeights(pm, s, z, self.colsums[lo:hi].contiguous(), self.per_tensor)
+
+
+_OUT = {torch.float16: L.ABQ_OUT_F16, torch.float64: L.ABQ_OUT_F64, torch.float32: L.ABQ_OUT_F32,
+        torch.int64: L.ABQ_OUT_CORR_I64}
+
+
+def linear_planes(a: BitPlaneMatrix, s_a, z_a, rowsum_a, w: PackedWeights, out_dtype=torch.float16,
+                  a_per_tensor: bool = False, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Fused K2/K3 + K4 on packed activation planes."""
+    if out is None:
+        out = torch.empty((a.rows, w.planes.rows), dtype=out_dtype, device=_dev())
+    act = L.ActC(_ptr(a.data), a.planes, a.rows, a.cols, _ptr(s_a), _ptr(z_a), _ptr(rowsum_a),
+                 int(a_per_tensor))
+    wc = w.c()
+    _check(L.lib().abq_linear_planes(C.byref(act), C.byref(wc), _ptr(out), _OUT[out.dtype], _stream()))
+    return out
+
+
+class Linear:
+    """One-call engine linear from fp16/fp32/fp64 activations: ReQuant +
+    BitPacking (K1), plane GEMV/GEMM (K2/K3) and the fused epilogue (K4).
+    Workspace is allocated once; call() is launch-only (no host sync) when
+    check=False."""
+
+    def __init__(self, weights: PackedWeights, act_spec: QuantSpec, max_m: int):
+        act_spec.validate()
+        self.w = weights
+        self.spec = act_spec
+        self.k = weights.planes.cols
+        self.ws_bytes = L.lib().abq_linear_workspace_bytes(max_m, self.k, act_spec.planes())
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=_dev())
+        self.err = torch.full((1,), -1, dtype=torch.int64, device=_dev())
+        self.max_m = max_m
+        self._wc = weights.c()
+        self._sc = act_spec.c()
+
+    def __call__(self, x: torch.Tensor, out: Optional[torch.Tensor] = None,
+                 out_dtype=torch.float16, check: bool = True) -> torch.Tensor:
+        m = x.shape[0]
+        if m > self.max_m:
+            raise ValueError(f"Linear: m={m} exceeds max_m={self.max_m}")
+        if out is None:
+            out = torch.empty((m, self.w.planes.rows), dtype=out_dtype, device=x.device)
+        _check(L.lib().abq_linear(_ptr(x), _dtype_code(x), m, self.k, C.byref(self._sc),
+                                  C.byref(self._wc), _ptr(out), _OUT[out.dtype], _ptr(self.ws),
+                                  self.ws_bytes, None if check else _ptr(self.err), _stream()))
+        return out
+
+
+def quantized_linear(act: QuantizedTensor, wt: QuantizedTensor,
+                     stats: Optional[GemmStats] = None) -> torch.Tensor:
+    """quantized_linear  gemm.hpp:266-307 -> float64 M x N, bit-identical to the
+    reference (FP64 epilogue, same operation order)."""
+    if act.cols() != wt.cols():
+        raise ShapeError("quantized_linear: inner dimensions differ")
+    p, q = act.spec.planes(), wt.spec.planes()
+    a = bitpack(act.codes, p)
+    w = PackedWeights.from_quantized(wt)
+    rows_a = code_rowsums(act.codes)
+    out = linear_planes(a, act.scales, act.zero_points, rows_a, w, torch.float64,
+                        a_per_tensor=act.spec.granularity == PER_TENSOR)
+    if stats is not None:
+        t = default_tile(p, q)
+        tiles = -(-act.rows() // t.BM) * -(-wt.rows() // t.BN)
+        stats.block_tiles += tiles
+        stats.plane_pair_products += tiles * p * q
+    return out
+
+
+def launch_count() -> int:
+    return int(L.lib().abq_launch_count())

@@ -1,0 +1,475 @@
+// abi.cu -- the C-ABI (include/abq_cuda.h): argument validation in the
+// reference's order and wording, error state, and dispatch to the sm_100a
+// kernels.  No CPU compute path exists here: every numeric result is produced
+// by a CUDA kernel; if the device is missing the call fails with ABQ_ERR_CUDA.
+#include <algorithm>
+#include <climits>
+#include <cstring>
+#include <mutex>
+
+#include "common.cuh"
+
+namespace abq_dev {
+
+// ---- state -----------------------------------------------------------------
+std::string& last_error() {
+  static thread_local std::string s;
+  return s;
+}
+
+int fail(int status, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  std::vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  last_error() = buf;
+  return status;
+}
+
+uint64_t& launch_counter() {
+  static thread_local uint64_t n = 0;
+  return n;
+}
+
+int num_sms() {
+  static int cache[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (cache[dev] == 0) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = v > 0 ? v : 148;
+  }
+  return cache[dev];
+}
+
+// per-thread, per-device scratch for synchronous status reporting
+static unsigned long long* scratch_words() {
+  static thread_local unsigned long long* ptr[64] = {nullptr};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!ptr[dev]) {
+    if (cudaMalloc(&ptr[dev], 8 * sizeof(unsigned long long)) != cudaSuccess) {
+      cudaGetLastError();
+      ptr[dev] = nullptr;
+    }
+  }
+  return ptr[dev];
+}
+
+static int g_gemv_variant = ABQ_GEMV_AUTO;
+
+// ---- kernels implemented in the other translation units --------------------
+int run_quantize(const void* x, int x_dtype, size_t rows, size_t cols, const QuantParams& qp,
+                 const double* ca, const double* cb, uint8_t* codes, uint64_t* planes,
+                 unsigned nplanes, double* scales, int32_t* zps, int64_t* rowsums,
+                 unsigned long long* bad, unsigned long long* range, cudaStream_t st);
+int run_bitpack(const uint8_t* codes, size_t rows, size_t cols, unsigned bits, uint64_t* planes,
+                unsigned long long* bad, cudaStream_t st);
+int run_unpack(const uint64_t* planes, unsigned bits, size_t rows, size_t cols, uint8_t* codes,
+               cudaStream_t st);
+int run_code_rowsums(const uint8_t* codes, size_t rows, size_t cols, int64_t* out, cudaStream_t st);
+int run_plane_rowsums(const uint64_t* planes, unsigned bits, size_t rows, size_t cols, int64_t* out,
+                      cudaStream_t st);
+template <typename Acc>
+int run_zero_point_correct(const Acc* acc, size_t m, size_t n, const int64_t* ra, const int64_t* cb,
+                           const int32_t* za, const int32_t* zb, size_t k, Acc* out, cudaStream_t st);
+int run_bmma(const uint64_t* a, size_t m, unsigned a_plane, const uint64_t* bt, size_t n,
+             unsigned b_plane, size_t k, int32_t* out, cudaStream_t st);
+int run_gemm_popc(const uint64_t* A, unsigned p, size_t m, const uint64_t* W, unsigned q, size_t n,
+                  size_t k, bool wide, const EpiParams& e, cudaStream_t st);
+
+// ---- shared validation -----------------------------------------------------
+static bool fits_int32_host(unsigned p, unsigned q, size_t k) {
+  unsigned log_k = 0;
+  while ((size_t{1} << log_k) < k + 1) ++log_k;
+  return p + q + log_k <= 31;
+}
+
+static bool tile_valid_host(const abq_tile_config& t, unsigned p, unsigned q) {
+  if (t.WK != 128) return false;
+  if (t.BK != 128 && t.BK != 256 && t.BK != 384 && t.BK != 512) return false;
+  if (t.BK % t.WK != 0) return false;
+  if (t.BM == 0 || t.BN == 0 || t.WM == 0 || t.WN == 0) return false;
+  if (t.WM % 8 != 0 || t.WN % 8 != 0) return false;
+  const double warps = (double(t.BM) * p / double(t.WM)) * (double(t.BN) * q / double(t.WN));
+  return warps >= 1.0 && warps <= 32.0;
+}
+
+static unsigned levels_of(const abq_quant_spec& s) {
+  return s.scheme == ABQ_BALANCED ? (1u << s.bits) + 1u : (1u << s.bits);
+}
+static unsigned planes_of(const abq_quant_spec& s) {
+  const unsigned L = levels_of(s);
+  unsigned p = 0;
+  while ((1u << p) < L) ++p;
+  return p;
+}
+
+// QuantSpec::validate (quantizer.hpp:61-70) + passthrough rejection (quantizer.hpp:150)
+static int validate_spec(const abq_quant_spec* s) {
+  if (!s) return fail(ABQ_ERR_VALUE, "quantize: null QuantSpec");
+  const bool passthrough = s->bits >= 16;
+  if (s->bits < 1 || (s->bits > 8 && !passthrough))
+    return fail(ABQ_ERR_VALUE, "QuantSpec: bits must be in [1,8] (or >=16 for passthrough)");
+  if (s->scheme == ABQ_BALANCED && s->bits > 7 && !passthrough)
+    return fail(ABQ_ERR_VALUE,
+                "QuantSpec: balanced codes reach 2^bits and must fit one byte, so bits <= 7");
+  if (!(s->alpha > 0.0 && s->alpha <= 1.0)) return fail(ABQ_ERR_VALUE, "QuantSpec: alpha must be in (0,1]");
+  if (!(s->beta > 0.0 && s->beta <= 1.0)) return fail(ABQ_ERR_VALUE, "QuantSpec: beta must be in (0,1]");
+  if (s->scheme < 0 || s->scheme > 2) return fail(ABQ_ERR_VALUE, "QuantSpec: unknown scheme");
+  if (s->granularity < 0 || s->granularity > 2) return fail(ABQ_ERR_VALUE, "QuantSpec: unknown granularity");
+  if (passthrough) return fail(ABQ_ERR_VALUE, "quantize: passthrough spec cannot be materialized");
+  return ABQ_OK;
+}
+
+static QuantParams params_of(const abq_quant_spec& s) {
+  QuantParams qp;
+  qp.bits = s.bits;
+  qp.scheme = s.scheme;
+  qp.per_tensor = s.granularity == ABQ_PER_TENSOR;
+  qp.alpha = s.alpha;
+  qp.beta = s.beta;
+  qp.levels = levels_of(s);
+  return qp;
+}
+
+static int check_device() {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    return fail(ABQ_ERR_CUDA, "abq: no CUDA device available (%s); the engine has no CPU path",
+                cudaGetErrorString(e));
+  }
+  return ABQ_OK;
+}
+
+static int sync_read(unsigned long long* dev_word, cudaStream_t st, unsigned long long* out) {
+  ABQ_CUDA_TRY(cudaMemcpyAsync(out, dev_word, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  ABQ_CUDA_TRY(cudaStreamSynchronize(st));
+  return ABQ_OK;
+}
+
+static void add_stats(abq_gemm_stats* stats, const abq_tile_config& t, size_t m, size_t n,
+                      unsigned p, unsigned q) {
+  if (!stats) return;
+  // gemm.hpp:108-115: one block tile per (BM rows, BN cols); p*q plane pairs per tile
+  const uint64_t tiles = uint64_t((m + t.BM - 1) / t.BM) * uint64_t((n + t.BN - 1) / t.BN);
+  stats->block_tiles += tiles;
+  stats->plane_pair_products += tiles * p * q;
+}
+
+static EpiParams raw_epi(void* out, size_t n, bool wide) {
+  EpiParams e{};
+  e.mode = wide ? EPI_ACC_I64 : EPI_ACC_I32;
+  e.out = out;
+  e.ldo = static_cast<long long>(n);
+  return e;
+}
+
+}  // namespace abq_dev
+
+using namespace abq_dev;
+
+extern "C" {
+
+const char* abq_last_error(void) { return last_error().c_str(); }
+int abq_version(void) { return 1; }
+uint64_t abq_launch_count(void) { return launch_counter(); }
+
+int abq_fits_int32(unsigned p, unsigned q, size_t k) { return fits_int32_host(p, q, k) ? 1 : 0; }
+
+int abq_tile_valid(const abq_tile_config* tile, unsigned p, unsigned q) {
+  return tile && tile_valid_host(*tile, p, q) ? 1 : 0;
+}
+
+abq_tile_config abq_default_tile(unsigned p, unsigned q) {
+  abq_tile_config t;
+  t.BM = 64;
+  t.BN = 64;
+  t.BK = 512;
+  t.WM = 32 * p;
+  t.WN = 32 * q;
+  t.WK = 128;
+  return t;
+}
+
+int abq_padding_redundancy(size_t m, unsigned p, size_t mma_m, double* out) {
+  if (m == 0 || p == 0 || mma_m == 0)
+    return fail(ABQ_ERR_VALUE, "padding_redundancy: arguments must be positive");
+  const size_t expanded = p * m;
+  const size_t padded = (expanded + mma_m - 1) / mma_m * mma_m;
+  *out = double(padded - expanded) / double(padded);
+  return ABQ_OK;
+}
+
+unsigned abq_spec_levels(const abq_quant_spec* spec) { return spec ? levels_of(*spec) : 0u; }
+unsigned abq_spec_planes(const abq_quant_spec* spec) { return spec ? planes_of(*spec) : 0u; }
+
+int abq_set_gemv_variant(int variant) {
+  if (variant < ABQ_GEMV_AUTO || variant > ABQ_GEMV_RECOMB)
+    return fail(ABQ_ERR_VALUE, "abq_set_gemv_variant: unknown variant %d", variant);
+  g_gemv_variant = variant;
+  return ABQ_OK;
+}
+int abq_get_gemv_variant(void) { return g_gemv_variant; }
+
+// ---- quantizer -------------------------------------------------------------
+int abq_quantize(const void* x, int x_dtype, size_t rows, size_t cols, const abq_quant_spec* spec,
+                 const double* comp_a, const double* comp_b, uint8_t* codes, double* scales,
+                 int32_t* zero_points, void* stream) {
+  int st = validate_spec(spec);
+  if (st) return st;
+  if ((comp_a == nullptr) != (comp_b == nullptr))
+    return fail(ABQ_ERR_SHAPE, "quantize: compensation pair does not match matrix shape");
+  if ((st = check_device())) return st;
+  unsigned long long* sc = scratch_words();
+  if (!sc) return fail(ABQ_ERR_CUDA, "quantize: cannot allocate device scratch");
+  cudaStream_t s = as_stream(stream);
+  st = run_quantize(x, x_dtype, rows, cols, params_of(*spec), comp_a, comp_b, codes, nullptr, 0,
+                    scales, zero_points, nullptr, sc, sc + 1, s);
+  if (st) return st;
+  unsigned long long bad = 0;
+  if ((st = sync_read(sc, s, &bad))) return st;
+  if (bad != ~0ull)
+    return fail(ABQ_ERR_VALUE, "quantize: non-finite element at (%llu,%llu)", bad / cols, bad % cols);
+  return ABQ_OK;
+}
+
+int abq_quant_pack_act(const void* x, int x_dtype, size_t m, size_t k, const abq_quant_spec* spec,
+                       uint64_t* planes, double* scales, int32_t* zero_points, int64_t* rowsums,
+                       uint8_t* codes, int64_t* err_index, void* stream) {
+  int st = validate_spec(spec);
+  if (st) return st;
+  if ((st = check_device())) return st;
+  unsigned long long* sc = scratch_words();
+  if (!sc) return fail(ABQ_ERR_CUDA, "quant_pack_act: cannot allocate device scratch");
+  cudaStream_t s = as_stream(stream);
+  unsigned long long* bad = err_index ? reinterpret_cast<unsigned long long*>(err_index) : sc;
+  st = run_quantize(x, x_dtype, m, k, params_of(*spec), nullptr, nullptr, codes, planes,
+                    planes_of(*spec), scales, zero_points, rowsums, bad, sc + 1, s);
+  if (st || err_index) return st;
+  unsigned long long b = 0;
+  if ((st = sync_read(sc, s, &b))) return st;
+  if (b != ~0ull)
+    return fail(ABQ_ERR_VALUE, "quantize: non-finite element at (%llu,%llu)", b / k, b % k);
+  return ABQ_OK;
+}
+
+// ---- bit planes ------------------------------------------------------------
+int abq_bitpack(const uint8_t* codes, size_t rows, size_t cols, unsigned bits, uint64_t* planes,
+                void* stream) {
+  if (bits < 1 || bits > 8) return fail(ABQ_ERR_VALUE, "bitpack: plane count must be in [1,8]");
+  int st = check_device();
+  if (st) return st;
+  unsigned long long* sc = scratch_words();
+  if (!sc) return fail(ABQ_ERR_CUDA, "bitpack: cannot allocate device scratch");
+  cudaStream_t s = as_stream(stream);
+  if ((st = run_bitpack(codes, rows, cols, bits, planes, sc, s))) return st;
+  unsigned long long bad = 0;
+  if ((st = sync_read(sc, s, &bad))) return st;
+  if (bad != ~0ull) {
+    uint8_t c = 0;
+    ABQ_CUDA_TRY(cudaMemcpy(&c, codes + bad, 1, cudaMemcpyDeviceToHost));
+    return fail(ABQ_ERR_VALUE, "bitpack: code %d at (%llu,%llu) needs more than %u planes", int(c),
+                bad / cols, bad % cols, bits);
+  }
+  return ABQ_OK;
+}
+
+int abq_unpack(const uint64_t* planes, unsigned bits, size_t rows, size_t cols, uint8_t* codes,
+               void* stream) {
+  int st = check_device();
+  if (st) return st;
+  return run_unpack(planes, bits, rows, cols, codes, as_stream(stream));
+}
+
+int abq_bmma(const uint64_t* a, unsigned a_planes, size_t m, unsigned a_plane, const uint64_t* bt,
+             unsigned b_planes, size_t n, unsigned b_plane, size_t k, int32_t* out, void* stream) {
+  if (a_plane >= a_planes || b_plane >= b_planes)
+    return fail(ABQ_ERR_VALUE, "bmma: plane index out of range");
+  int st = check_device();
+  if (st) return st;
+  return run_bmma(a, m, a_plane, bt, n, b_plane, k, out, as_stream(stream));
+}
+
+// ---- engine ----------------------------------------------------------------
+static int gemm_common(const char* name, const uint64_t* a, unsigned p, size_t m, size_t a_k,
+                       const uint64_t* bt, unsigned q, size_t n, size_t b_k,
+                       const abq_tile_config* tile, bool wide, bool check_overflow, void* out,
+                       abq_gemm_stats* stats, void* stream) {
+  if (a_k != b_k) return fail(ABQ_ERR_SHAPE, "%s: shared K dimension differs", name);
+  if (tile) {
+    if (!tile_valid_host(*tile, p, q))
+      return fail(ABQ_ERR_VALUE,
+                  "TileConfig invalid for p=%u q=%u: BM=%zu BN=%zu BK=%zu WM=%zu WN=%zu WK=%zu", p, q,
+                  tile->BM, tile->BN, tile->BK, tile->WM, tile->WN, tile->WK);
+  }
+  if (check_overflow && !fits_int32_host(p, q, a_k))
+    return fail(ABQ_ERR_OVERFLOW,
+                "%s: p+q+ceil(log2(K+1)) = %u+%u+log2(%zu+1) exceeds 31; use gemm_arbitrary_wide",
+                name, p, q, a_k);
+  if (p < 1 || p > 8 || q < 1 || q > 8) return fail(ABQ_ERR_VALUE, "%s: plane counts must be in [1,8]", name);
+  int st = check_device();
+  if (st) return st;
+  if (m * n > 0 && a_k == 0) {
+    // K == 0: every sum is empty
+    ABQ_CUDA_TRY(cudaMemsetAsync(out, 0, m * n * (wide ? 8 : 4), as_stream(stream)));
+  } else {
+    st = run_gemm_popc(a, p, m, bt, q, n, a_k, wide, raw_epi(out, n, wide), as_stream(stream));
+    if (st) return st;
+  }
+  if (tile) add_stats(stats, *tile, m, n, p, q);
+  return ABQ_OK;
+}
+
+int abq_gemm_arbitrary(const uint64_t* a, unsigned p, size_t m, size_t a_k, const uint64_t* bt,
+                       unsigned q, size_t n, size_t b_k, const abq_tile_config* tile, int32_t* out,
+                       abq_gemm_stats* stats, void* stream) {
+  abq_tile_config def = abq_default_tile(p, q);
+  return gemm_common("gemm_arbitrary", a, p, m, a_k, bt, q, n, b_k, tile ? tile : &def, false, true,
+                     out, stats, stream);
+}
+
+int abq_gemm_arbitrary_wide(const uint64_t* a, unsigned p, size_t m, size_t a_k,
+                            const uint64_t* bt, unsigned q, size_t n, size_t b_k,
+                            const abq_tile_config* tile, int64_t* out, abq_gemm_stats* stats,
+                            void* stream) {
+  abq_tile_config def = abq_default_tile(p, q);
+  return gemm_common("gemm_arbitrary_wide", a, p, m, a_k, bt, q, n, b_k, tile ? tile : &def, true,
+                     false, out, stats, stream);
+}
+
+int abq_gemm_naive(const uint64_t* a, unsigned p, size_t m, size_t a_k, const uint64_t* bt,
+                   unsigned q, size_t n, size_t b_k, int32_t* out, void* stream) {
+  // gemm.hpp:213-231: no tile and no overflow guard (int32 wraps like the reference would)
+  return gemm_common("gemm_naive", a, p, m, a_k, bt, q, n, b_k, nullptr, false, false, out, nullptr,
+                     stream);
+}
+
+int abq_zero_point_correct_i32(const int32_t* acc, size_t m, size_t n, const int64_t* rowsum_a,
+                               const int64_t* colsum_b, const int32_t* z_a, const int32_t* z_b,
+                               size_t k, int32_t* out, void* stream) {
+  int st = check_device();
+  if (st) return st;
+  return run_zero_point_correct<int32_t>(acc, m, n, rowsum_a, colsum_b, z_a, z_b, k, out,
+                                         as_stream(stream));
+}
+
+int abq_zero_point_correct_i64(const int64_t* acc, size_t m, size_t n, const int64_t* rowsum_a,
+                               const int64_t* colsum_b, const int32_t* z_a, const int32_t* z_b,
+                               size_t k, int64_t* out, void* stream) {
+  int st = check_device();
+  if (st) return st;
+  return run_zero_point_correct<int64_t>(acc, m, n, rowsum_a, colsum_b, z_a, z_b, k, out,
+                                         as_stream(stream));
+}
+
+int abq_code_rowsums(const uint8_t* codes, size_t rows, size_t cols, int64_t* out, void* stream) {
+  int st = check_device();
+  if (st) return st;
+  return run_code_rowsums(codes, rows, cols, out, as_stream(stream));
+}
+
+int abq_plane_rowsums(const uint64_t* planes, unsigned bits, size_t rows, size_t cols, int64_t* out,
+                      void* stream) {
+  int st = check_device();
+  if (st) return st;
+  return run_plane_rowsums(planes, bits, rows, cols, out, as_stream(stream));
+}
+
+// ---- fused linear ----------------------------------------------------------
+static int epi_mode_of(int out_kind, int* mode) {
+  switch (out_kind) {
+    case ABQ_OUT_F64: *mode = EPI_F64; return ABQ_OK;
+    case ABQ_OUT_F16: *mode = EPI_F16; return ABQ_OK;
+    case ABQ_OUT_F32: *mode = EPI_F32; return ABQ_OK;
+    case ABQ_OUT_CORR_I64: *mode = EPI_CORR_I64; return ABQ_OK;
+    default: return fail(ABQ_ERR_VALUE, "linear: unknown out_kind %d", out_kind);
+  }
+}
+
+int abq_linear_planes(const abq_act* act, const abq_weights* w, void* y, int out_kind,
+                      void* stream) {
+  if (!act || !w) return fail(ABQ_ERR_VALUE, "quantized_linear: null operand");
+  if (act->k != w->k) return fail(ABQ_ERR_SHAPE, "quantized_linear: inner dimensions differ");
+  if (act->p < 1 || act->p > 8 || w->q < 1 || w->q > 8)
+    return fail(ABQ_ERR_VALUE, "quantized_linear: plane counts must be in [1,8]");
+  int mode = 0;
+  int st = epi_mode_of(out_kind, &mode);
+  if (st) return st;
+  if ((st = check_device())) return st;
+  EpiParams e{};
+  e.mode = mode;
+  e.out = y;
+  e.ldo = static_cast<long long>(w->n);
+  e.s_a = act->scales;
+  e.sa_stride = act->per_tensor ? 0 : 1;
+  e.z_a = act->zero_points;
+  e.za_stride = act->per_tensor ? 0 : 1;
+  e.rowsum_a = act->rowsums;
+  e.s_b = w->scales;
+  e.sb_stride = w->per_tensor ? 0 : 1;
+  e.z_b = w->zero_points;
+  e.zb_stride = w->per_tensor ? 0 : 1;
+  e.colsum_b = w->colsums;
+  e.k = static_cast<long long>(act->k);
+  const bool wide = !fits_int32_host(act->p, w->q, act->k);
+  return run_gemm_popc(act->planes, act->p, act->m, w->planes, w->q, w->n, act->k, wide, e,
+                       as_stream(stream));
+}
+
+static size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
+
+size_t abq_linear_workspace_bytes(size_t m, size_t k, unsigned act_planes) {
+  return align256(size_t(act_planes) * m * wpr_of(k) * 8) + align256(m * 8) + align256(m * 4) +
+         align256(m * 8) + 256;
+}
+
+int abq_linear(const void* x, int x_dtype, size_t m, size_t k, const abq_quant_spec* act_spec,
+               const abq_weights* w, void* y, int out_kind, void* workspace, size_t workspace_bytes,
+               int64_t* err_index, void* stream) {
+  int st = validate_spec(act_spec);
+  if (st) return st;
+  if (!w) return fail(ABQ_ERR_VALUE, "quantized_linear: null weights");
+  if (k != w->k) return fail(ABQ_ERR_SHAPE, "quantized_linear: inner dimensions differ");
+  const unsigned p = planes_of(*act_spec);
+  if (workspace_bytes < abq_linear_workspace_bytes(m, k, p))
+    return fail(ABQ_ERR_VALUE, "linear: workspace too small (%zu < %zu)", workspace_bytes,
+                abq_linear_workspace_bytes(m, k, p));
+  if ((st = check_device())) return st;
+  char* ws = static_cast<char*>(workspace);
+  uint64_t* planes = reinterpret_cast<uint64_t*>(ws);
+  ws += align256(size_t(p) * m * wpr_of(k) * 8);
+  double* sa = reinterpret_cast<double*>(ws);
+  ws += align256(m * 8);
+  int32_t* za = reinterpret_cast<int32_t*>(ws);
+  ws += align256(m * 4);
+  int64_t* ra = reinterpret_cast<int64_t*>(ws);
+  ws += align256(m * 8);
+  unsigned long long* range = reinterpret_cast<unsigned long long*>(ws);
+  unsigned long long* sc = nullptr;
+  if (!err_index) {
+    sc = scratch_words();
+    if (!sc) return fail(ABQ_ERR_CUDA, "linear: cannot allocate device scratch");
+  }
+  unsigned long long* bad = err_index ? reinterpret_cast<unsigned long long*>(err_index) : sc;
+  cudaStream_t s = as_stream(stream);
+  st = run_quantize(x, x_dtype, m, k, params_of(*act_spec), nullptr, nullptr, nullptr, planes, p, sa,
+                    za, ra, bad, range, s);
+  if (st) return st;
+  abq_act act{planes, p, m, k, sa, za, ra, act_spec->granularity == ABQ_PER_TENSOR};
+  if ((st = abq_linear_planes(&act, w, y, out_kind, stream))) return st;
+  if (err_index) return ABQ_OK;
+  unsigned long long b = 0;
+  if ((st = sync_read(sc, s, &b))) return st;
+  if (b != ~0ull)
+    return fail(ABQ_ERR_VALUE, "quantize: non-finite element at (%llu,%llu)", b / k, b % k);
+  return ABQ_OK;
+}
+
+}  // extern "C"

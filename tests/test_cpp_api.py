@@ -1,0 +1,19 @@
+"""Runs tests/cpp/test_api (the reference's hot-path test cases restated
+against the C++ drop-in mirror include/abq/abq.hpp) on the GPU."""
+import os
+import subprocess
+
+import pytest
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+@pytest.mark.gpu
+def test_cpp_drop_in_api():
+    exe = os.path.join(HERE, "cpp", "test_api")
+    if not os.path.exists(exe):
+        subprocess.run(["make", "-s", "-C", os.path.join(HERE, "cpp")], check=True)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.count("PASS") == 8
