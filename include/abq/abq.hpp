@@ -449,8 +449,11 @@ inline Mat quantized_linear(const QuantizedTensor& act, const QuantizedTensor& w
   detail::DeviceBuffer<std::int32_t> dza(act.zero_points), dzb(wt.zero_points);
   abq_act a{dap.get(), p, m, k, dsa.get(), dza.get(), dra.get(),
             act.spec.granularity == Granularity::PerTensor};
+  // fragment-major copy for the tensor-pipe decode GEMV (used when m <= 8)
+  detail::DeviceBuffer<std::uint32_t> dfrag(m <= 8 ? abq_weights_frag_bytes(q, n, k) / 4 : 0);
+  if (m <= 8) detail::check(abq_weights_prepack(dwp.get(), q, n, k, dfrag.get(), nullptr));
   abq_weights w{dwp.get(), q, n, k, dsb.get(), dzb.get(), dcb.get(),
-                wt.spec.granularity == Granularity::PerTensor};
+                wt.spec.granularity == Granularity::PerTensor, m <= 8 ? dfrag.get() : nullptr};
   Mat out(m, n);
   detail::DeviceBuffer<double> dy(out.data.size());
   detail::check(abq_linear_planes(&a, &w, dy.get(), ABQ_OUT_F64, nullptr));
@@ -474,14 +477,15 @@ class Weights {
       : q_(wt.spec.planes()), n_(wt.rows()), k_(wt.cols()),
         per_tensor_(wt.spec.granularity == Granularity::PerTensor),
         planes_(std::size_t(q_) * n_ * ((k_ + 63) / 64)), scales_(wt.scales),
-        zps_(wt.zero_points), colsums_(n_) {
+        zps_(wt.zero_points), colsums_(n_), frag_(abq_weights_frag_bytes(q_, n_, k_) / 4) {
     detail::DeviceBuffer<std::uint8_t> dc(wt.codes.data);
     detail::check(abq_bitpack(dc.get(), n_, k_, q_, planes_.get(), nullptr));
     detail::check(abq_plane_rowsums(planes_.get(), q_, n_, k_, colsums_.get(), nullptr));
+    detail::check(abq_weights_prepack(planes_.get(), q_, n_, k_, frag_.get(), nullptr));
   }
   abq_weights view() const {
     return abq_weights{planes_.get(), q_, n_, k_, scales_.get(), zps_.get(), colsums_.get(),
-                       per_tensor_ ? 1 : 0};
+                       per_tensor_ ? 1 : 0, frag_.get()};
   }
   std::size_t n() const { return n_; }
   std::size_t k() const { return k_; }
@@ -494,6 +498,7 @@ class Weights {
   detail::DeviceBuffer<double> scales_;
   detail::DeviceBuffer<std::int32_t> zps_;
   detail::DeviceBuffer<std::int64_t> colsums_;
+  detail::DeviceBuffer<std::uint32_t> frag_;
 };
 
 /// ReQuant + BitPacking + plane GEMV/GEMM + fused epilogue on device pointers.
@@ -501,8 +506,10 @@ class Linear {
  public:
   Linear(const Weights& w, const QuantSpec& act_spec, std::size_t max_m)
       : w_(w.view()), spec_(act_spec.c_spec()), max_m_(max_m),
-        ws_bytes_(abq_linear_workspace_bytes(max_m, w.k(), act_spec.planes())), ws_(ws_bytes_) {
+        ws_bytes_(abq_linear_workspace_bytes(max_m, w.n(), w.k(), act_spec.planes())), ws_(ws_bytes_) {
     act_spec.validate();
+    // the engine expects a zero-filled workspace and leaves it zeroed
+    detail::cuda_check(cudaMemset(ws_.get(), 0, ws_bytes_), "cudaMemset workspace");
   }
   /// x: device [m][k] (x_dtype ABQ_F16/F32/F64); y: device [m][n] of out_kind.
   void operator()(const void* x, int x_dtype, std::size_t m, void* y, int out_kind,

@@ -88,6 +88,9 @@ typedef struct {
   const int32_t* zero_points;
   const int64_t* colsums;
   int per_tensor;
+  /* optional fragment-major copy of the planes for the tensor-pipe decode
+   * GEMV (abq_weights_prepack); NULL = AND+popcount kernels only */
+  const uint32_t* frag;
 } abq_weights;
 
 /* Activation-side metadata produced by abq_quant_pack_act (per-token or
@@ -181,6 +184,14 @@ int abq_code_rowsums(const uint8_t* codes, size_t rows, size_t cols, int64_t* ou
 int abq_plane_rowsums(const uint64_t* planes, unsigned bits, size_t rows, size_t cols,
                       int64_t* out, void* stream);
 
+/* K5: offline re-layout of ABQP weight planes into the fragment-major plane
+ * layout consumed by the decode GEMV on the int8 tensor pipe: [row-tile of 16]
+ * [k-block of 256][plane][lane][4 x u32] -- same bits, same byte count (rows
+ * padded to 16, K to 256 with zero bits). */
+size_t abq_weights_frag_bytes(unsigned q, size_t n, size_t k);
+int abq_weights_prepack(const uint64_t* planes, unsigned q, size_t n, size_t k, uint32_t* frag,
+                        void* stream);
+
 /* Fused engine linear on packed operands (K2/K3 + K4):
  *   y[i][j] = s_a[i] * s_b[j] * corrected[i][j]        gemm.hpp:266-307
  * out_kind selects what is written:
@@ -199,9 +210,12 @@ int abq_linear_planes(const abq_act* act, const abq_weights* w, void* y, int out
 
 /* One-call engine linear from float activations (K1 + K2/K3 + K4): the
  * device-resident equivalent of quantize(act) + quantized_linear
- * (toyblock.hpp:240-242).  workspace >= abq_linear_workspace_bytes(m,k,p).
- * err_index (device, may be NULL => synchronous check) as in abq_quant_pack_act. */
-size_t abq_linear_workspace_bytes(size_t m, size_t k, unsigned act_planes);
+ * (toyblock.hpp:240-242).  workspace >= abq_linear_workspace_bytes(m,n,k,p)
+ * and must be ZERO-FILLED before its first use (the engine leaves it zeroed).
+ * err_index (device, may be NULL => synchronous check) as in abq_quant_pack_act.
+ * With w->frag set and m <= 8 this is ONE kernel launch (ReQuant in the
+ * prologue, tensor-pipe plane GEMV, fused epilogue). */
+size_t abq_linear_workspace_bytes(size_t m, size_t n, size_t k, unsigned act_planes);
 int abq_linear(const void* x, int x_dtype, size_t m, size_t k, const abq_quant_spec* act_spec,
                const abq_weights* w, void* y, int out_kind, void* workspace,
                size_t workspace_bytes, int64_t* err_index, void* stream);

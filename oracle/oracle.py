@@ -205,6 +205,36 @@ class RefOracle:
         L.ref_padding_redundancy.restype = C.c_double
         L.ref_padding_redundancy.argtypes = [_S, _U, _S]
         L.ref_fits_int32.argtypes = [_U, _U, _S]
+        L.ref_linear_new.restype = C.c_void_p
+        L.ref_linear_new.argtypes = [_P, _S, _S, _U, _P, _P, _U]
+        L.ref_linear_run.argtypes = [_P, _P, _S, _U, _P]
+        L.ref_linear_free.argtypes = [_P]
+
+    def linear(self, wt_codes, w_bits, s_b, z_b, threads=1):
+        """Reference linear step with pre-packed weights (ref_shim.cpp
+        ref_linear_*); returns run(x_double[m,k], a_bits) -> y[m,n]."""
+        wt_codes = np.ascontiguousarray(wt_codes, np.uint8)
+        n, k = wt_codes.shape
+        s_b = np.ascontiguousarray(s_b, np.float64)
+        z_b = np.ascontiguousarray(z_b, np.int32)
+        h = self.lib.ref_linear_new(_p(wt_codes), n, k, w_bits, _p(s_b), _p(z_b), threads)
+        lib = self.lib
+
+        class _Run:
+            def __call__(self_, x, a_bits, out=None):
+                x = np.ascontiguousarray(x, np.float64)
+                m = x.shape[0]
+                if out is None:
+                    out = np.zeros((m, n), np.float64)
+                st = lib.ref_linear_run(h, _p(x), m, a_bits, _p(out))
+                if st:
+                    raise ValueError(f"reference linear status {st}")
+                return out
+
+            def __del__(self_):
+                lib.ref_linear_free(h)
+
+        return _Run()
 
     @staticmethod
     def available(path: str = REF_LIB_PATH) -> bool:

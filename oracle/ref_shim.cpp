@@ -9,6 +9,7 @@
 #include <cstdint>
 #include <cstring>
 #include <optional>
+#include <thread>
 #include <vector>
 
 #include "abq/bitplane.hpp"
@@ -170,6 +171,80 @@ int ref_quantized_linear(const std::uint8_t* act, std::size_t m, unsigned a_bits
     if (stats2) {
       stats2[0] = st.block_tiles;
       stats2[1] = st.plane_pair_products;
+    }
+    return 0;
+  } catch (const abq::Error& e) {
+    return status_of(e);
+  }
+}
+
+// ---- reference linear step for the CPU baseline -----------------------------
+// quantized_linear's body (gemm.hpp:266-307) with the per-call weight bitpack
+// (gemm.hpp:274, 278) hoisted out of the step -- weights are packed once, as the
+// engine does -- so the reference is timed on exactly the engine's per-step
+// work: quantize(act) -> bitpack(act) -> code_rowsums(act) -> gemm_arbitrary
+// (default_tile) -> zero_point_correct -> dequant.  threads > 1 is a
+// harness-parallel split of the output channels across std::threads, each
+// running the same reference calls on its slice (the reference itself only
+// parallelises over 64-row tiles of M, gemm.hpp:150-177).
+struct RefLinearSlice {
+  std::size_t n0, n1;
+  abq::BitPlaneMatrix w;
+  std::vector<std::int64_t> colsum;
+  std::vector<std::int32_t> z_b;
+  std::vector<double> s_b;
+};
+struct RefLinear {
+  std::size_t n, k;
+  unsigned w_bits;
+  std::vector<RefLinearSlice> slices;
+};
+
+void* ref_linear_new(const std::uint8_t* wt_codes, std::size_t n, std::size_t k, unsigned w_bits,
+                     const double* s_b, const std::int32_t* z_b, unsigned threads) {
+  auto* h = new RefLinear{n, k, w_bits, {}};
+  if (threads < 1) threads = 1;
+  for (unsigned t = 0; t < threads; ++t) {
+    std::size_t n0 = n * t / threads, n1 = n * (t + 1) / threads;
+    if (n0 == n1) continue;
+    abq::CodeMat c(n1 - n0, k);
+    std::memcpy(c.data.data(), wt_codes + n0 * k, (n1 - n0) * k);
+    RefLinearSlice s{n0, n1, abq::bitpack(c, w_bits), abq::code_rowsums(c),
+                     std::vector<std::int32_t>(z_b + n0, z_b + n1),
+                     std::vector<double>(s_b + n0, s_b + n1)};
+    h->slices.push_back(std::move(s));
+  }
+  return h;
+}
+
+void ref_linear_free(void* h) { delete static_cast<RefLinear*>(h); }
+
+int ref_linear_run(void* hv, const double* x, std::size_t m, unsigned a_bits, double* out) {
+  try {
+    auto* h = static_cast<RefLinear*>(hv);
+    abq::Mat xm(m, h->k);
+    std::memcpy(xm.data.data(), x, m * h->k * sizeof(double));
+    abq::QuantSpec spec;
+    spec.bits = a_bits;
+    spec.granularity = abq::Granularity::PerToken;
+    abq::QuantizedTensor qa = abq::quantize(xm, spec);  // ReQuant
+    abq::BitPlaneMatrix a = abq::bitpack(qa.codes, spec.planes());
+    auto rows_a = abq::code_rowsums(qa.codes);
+    abq::engine_threads() = 1;
+    auto work = [&](const RefLinearSlice& s) {
+      const std::size_t ns = s.n1 - s.n0;
+      auto acc = abq::gemm_arbitrary(a, s.w, abq::default_tile(a.planes, s.w.planes));
+      auto corrected = abq::zero_point_correct(acc, rows_a, s.colsum, qa.zero_points, s.z_b, h->k);
+      for (std::size_t i = 0; i < m; ++i)
+        for (std::size_t j = 0; j < ns; ++j)
+          out[i * h->n + s.n0 + j] = qa.scales[i] * s.s_b[j] * corrected(i, j);
+    };
+    if (h->slices.size() == 1) {
+      work(h->slices[0]);
+    } else {
+      std::vector<std::thread> pool;
+      for (const auto& s : h->slices) pool.emplace_back(work, std::cref(s));
+      for (auto& t : pool) t.join();
     }
     return 0;
   } catch (const abq::Error& e) {

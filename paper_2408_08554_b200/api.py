@@ -402,22 +402,33 @@ class PackedWeights:
     zero_points: torch.Tensor
     colsums: torch.Tensor
     per_tensor: bool
+    frag: Optional[torch.Tensor] = None  # fragment-major copy for the tensor-pipe GEMV
 
     @staticmethod
-    def from_quantized(wt: QuantizedTensor) -> "PackedWeights":
+    def from_quantized(wt: QuantizedTensor, frag: bool = True) -> "PackedWeights":
         pm = bitpack(wt.codes, wt.spec.planes())
         return PackedWeights(pm, wt.scales.contiguous(), wt.zero_points.contiguous(),
-                             plane_rowsums(pm), wt.spec.granularity == PER_TENSOR)
+                             plane_rowsums(pm), wt.spec.granularity == PER_TENSOR,
+                             prepack_frag(pm) if frag else None)
 
     @staticmethod
-    def from_planes(pm: BitPlaneMatrix, scales, zero_points, per_tensor=False) -> "PackedWeights":
+    def from_planes(pm: BitPlaneMatrix, scales, zero_points, per_tensor=False,
+                    frag: bool = True) -> "PackedWeights":
         return PackedWeights(pm, _to_dev(scales, torch.float64), _to_dev(zero_points, torch.int32),
-                             plane_rowsums(pm), per_tensor)
+                             plane_rowsums(pm), per_tensor, prepack_frag(pm) if frag else None)
 
     def c(self) -> L.WeightsC:
         return L.WeightsC(_ptr(self.planes.data), self.planes.planes, self.planes.rows,
                           self.planes.cols, _ptr(self.scales), _ptr(self.zero_points),
-                          _ptr(self.colsums), int(self.per_tensor))
+                          _ptr(self.colsums), int(self.per_tensor),
+                          _ptr(self.frag) if self.frag is not None else None)
+
+    def copy(self) -> "PackedWeights":
+        """Distinct HBM copy of the packed weights (same values)."""
+        pm = BitPlaneMatrix(self.planes.planes, self.planes.rows, self.planes.cols,
+                            self.planes.data.clone())
+        return PackedWeights(pm, self.scales, self.zero_points, self.colsums, self.per_tensor,
+                             self.frag.clone() if self.frag is not None else None)
 
     def shard(self, rank: int, world: int) -> "PackedWeights":
         """Column-parallel slice: output channels [rank*N/G, (rank+1)*N/G)
@@ -428,7 +439,21 @@ class PackedWeights:
                             self.planes.data[:, lo:hi, :].contiguous())
         s = self.scales if self.per_tensor else self.scales[lo:hi].contiguous()
         z = self.zero_points if self.per_tensor else self.zero_points[lo:hi].contiguous()
-        return PackedWeights(pm, s, z, self.colsums[lo:hi].contiguous(), self.per_tensor)
+        return PackedWeights(pm, s, z, self.colsums[lo:hi].contiguous(), self.per_tensor,
+                             prepack_frag(pm) if self.frag is not None else None)
+
+
+def prepack_frag(pm: BitPlaneMatrix) -> torch.Tensor:
+    """K5: ABQP planes -> fragment-major planes for the tensor-pipe decode GEMV."""
+    nbytes = L.lib().abq_weights_frag_bytes(pm.planes, pm.rows, pm.cols)
+    frag = torch.empty(max(1, nbytes // 4), dtype=torch.int32, device=_dev())
+    _check(L.lib().abq_weights_prepack(_ptr(pm.data), pm.planes, pm.rows, pm.cols, _ptr(frag), _stream()))
+    return frag
+
+
+def set_gemv_variant(variant: str) -> None:
+    """'auto' | 'popc' (AND+popcount on CUDA cores) | 'recomb' (planes on the int8 tensor pipe)."""
+    _check(L.lib().abq_set_gemv_variant({"auto": 0, "popc": 1, "recomb": 2}[variant]))
 
 
 _OUT = {torch.float16: L.ABQ_OUT_F16, torch.float64: L.ABQ_OUT_F64, torch.float32: L.ABQ_OUT_F32,
@@ -447,6 +472,25 @@ def linear_planes(a: BitPlaneMatrix, s_a, z_a, rowsum_a, w: PackedWeights, out_d
     return out
 
 
+def quant_pack_act(x: torch.Tensor, spec: QuantSpec):
+    """K1: fused ReQuant + BitPacking of device activations (quantizer.hpp:146-213
+    -> bitplane.hpp:47-64 -> gemm.hpp:256-261).  Returns (planes, scales,
+    zero_points, rowsums)."""
+    spec.validate()
+    x = x.contiguous()
+    m, k = x.shape
+    p = spec.planes()
+    groups = 1 if spec.granularity == PER_TENSOR else m
+    planes = _empty_planes(p, m, k)
+    sa = torch.empty(groups, dtype=torch.float64, device=x.device)
+    za = torch.empty(groups, dtype=torch.int32, device=x.device)
+    ra = torch.empty(m, dtype=torch.int64, device=x.device)
+    cs = spec.c()
+    _check(L.lib().abq_quant_pack_act(_ptr(x), _dtype_code(x), m, k, C.byref(cs), _ptr(planes),
+                                      _ptr(sa), _ptr(za), _ptr(ra), None, None, _stream()))
+    return BitPlaneMatrix(p, m, k, planes), sa, za, ra
+
+
 class Linear:
     """One-call engine linear from fp16/fp32/fp64 activations: ReQuant +
     BitPacking (K1), plane GEMV/GEMM (K2/K3) and the fused epilogue (K4).
@@ -458,8 +502,10 @@ class Linear:
         self.w = weights
         self.spec = act_spec
         self.k = weights.planes.cols
-        self.ws_bytes = L.lib().abq_linear_workspace_bytes(max_m, self.k, act_spec.planes())
-        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=_dev())
+        self.ws_bytes = L.lib().abq_linear_workspace_bytes(max_m, weights.planes.rows, self.k,
+                                                           act_spec.planes())
+        # zero-filled once; the engine leaves its cross-CTA accumulators zeroed
+        self.ws = torch.zeros(self.ws_bytes, dtype=torch.uint8, device=_dev())
         self.err = torch.full((1,), -1, dtype=torch.int64, device=_dev())
         self.max_m = max_m
         self._wc = weights.c()
@@ -476,6 +522,41 @@ class Linear:
                                   C.byref(self._wc), _ptr(out), _OUT[out.dtype], _ptr(self.ws),
                                   self.ws_bytes, None if check else _ptr(self.err), _stream()))
         return out
+
+
+class GraphedLinear:
+    """Serving entry point: one decode/prefill step of a Linear captured as a
+    CUDA graph together with its host I/O -- H2D of the activations from a
+    pinned host buffer, the engine kernels, D2H of the fp16 result into a
+    pinned host buffer.  step() replays it; the caller synchronises when it
+    needs the result (e.g. via torch.cuda.current_stream().synchronize())."""
+
+    def __init__(self, lin: Linear, m: int, x_dtype=torch.float16, out_dtype=torch.float16):
+        self.lin = lin
+        k, n = lin.k, lin.w.planes.rows
+        self.x_host = torch.empty((m, k), dtype=x_dtype, pin_memory=True)
+        self.y_host = torch.empty((m, n), dtype=out_dtype, pin_memory=True)
+        self.x_dev = torch.empty((m, k), dtype=x_dtype, device=_dev())
+        self.y_dev = torch.empty((m, n), dtype=out_dtype, device=_dev())
+        self.h2d_bytes = self.x_host.numel() * self.x_host.element_size()
+        self.d2h_bytes = self.y_host.numel() * self.y_host.element_size()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):  # warm up outside capture
+            self._body()
+        torch.cuda.current_stream().wait_stream(s)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self._body()
+
+    def _body(self):
+        self.x_dev.copy_(self.x_host, non_blocking=True)
+        self.lin(self.x_dev, out=self.y_dev, check=False)
+        self.y_host.copy_(self.y_dev, non_blocking=True)
+
+    def step(self) -> torch.Tensor:
+        self.graph.replay()
+        return self.y_host
 
 
 def quantized_linear(act: QuantizedTensor, wt: QuantizedTensor,

@@ -81,6 +81,21 @@ int run_bmma(const uint64_t* a, size_t m, unsigned a_plane, const uint64_t* bt, 
              unsigned b_plane, size_t k, int32_t* out, cudaStream_t st);
 int run_gemm_popc(const uint64_t* A, unsigned p, size_t m, const uint64_t* W, unsigned q, size_t n,
                   size_t k, bool wide, const EpiParams& e, cudaStream_t st);
+size_t frag_words(unsigned q, size_t n, size_t k);
+size_t imma_gacc_bytes(size_t m, size_t n);
+bool imma_supported(size_t m, size_t k);
+int run_prepack_frag(const uint64_t* planes, unsigned q, size_t n, size_t k, uint32_t* frag,
+                     cudaStream_t st);
+int run_gemv_imma(const uint32_t* frag, unsigned q, size_t n, size_t k, size_t m, const void* x,
+                  int x_dtype, const QuantParams* qp, const uint64_t* a_planes, unsigned p,
+                  const EpiParams& e, long long* gacc, unsigned* gcnt, unsigned long long* bad,
+                  cudaStream_t st);
+
+// decode GEMV on the tensor pipe: weights prepacked, M <= 8 tokens
+static bool use_imma(const abq_weights* w, size_t m, size_t k) {
+  return w->frag != nullptr && m >= 1 && m <= 8 && imma_supported(m, k) &&
+         g_gemv_variant != ABQ_GEMV_POPC;
+}
 
 // ---- shared validation -----------------------------------------------------
 static bool fits_int32_host(unsigned p, unsigned q, size_t k) {
@@ -382,6 +397,16 @@ int abq_plane_rowsums(const uint64_t* planes, unsigned bits, size_t rows, size_t
   return run_plane_rowsums(planes, bits, rows, cols, out, as_stream(stream));
 }
 
+size_t abq_weights_frag_bytes(unsigned q, size_t n, size_t k) { return frag_words(q, n, k) * 4; }
+
+int abq_weights_prepack(const uint64_t* planes, unsigned q, size_t n, size_t k, uint32_t* frag,
+                        void* stream) {
+  if (q < 1 || q > 8) return fail(ABQ_ERR_VALUE, "weights_prepack: plane count must be in [1,8]");
+  int st = check_device();
+  if (st) return st;
+  return run_prepack_frag(planes, q, n, k, frag, as_stream(stream));
+}
+
 // ---- fused linear ----------------------------------------------------------
 static int epi_mode_of(int out_kind, int* mode) {
   switch (out_kind) {
@@ -419,15 +444,19 @@ int abq_linear_planes(const abq_act* act, const abq_weights* w, void* y, int out
   e.colsum_b = w->colsums;
   e.k = static_cast<long long>(act->k);
   const bool wide = !fits_int32_host(act->p, w->q, act->k);
+  if (use_imma(w, act->m, act->k))
+    return run_gemv_imma(w->frag, w->q, w->n, act->k, act->m, nullptr, -1, nullptr, act->planes,
+                         act->p, e, nullptr, nullptr, nullptr, as_stream(stream));
   return run_gemm_popc(act->planes, act->p, act->m, w->planes, w->q, w->n, act->k, wide, e,
                        as_stream(stream));
 }
 
 static size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 
-size_t abq_linear_workspace_bytes(size_t m, size_t k, unsigned act_planes) {
-  return align256(size_t(act_planes) * m * wpr_of(k) * 8) + align256(m * 8) + align256(m * 4) +
-         align256(m * 8) + 256;
+size_t abq_linear_workspace_bytes(size_t m, size_t n, size_t k, unsigned act_planes) {
+  // [gacc + gcnt for the stream-K decode GEMV][act planes][s_a][z_a][rowsum_a][range]
+  return align256(imma_gacc_bytes(m <= 8 ? m : 8, n)) + align256(size_t(act_planes) * m * wpr_of(k) * 8) +
+         align256(m * 8) + align256(m * 4) + align256(m * 8) + 256;
 }
 
 int abq_linear(const void* x, int x_dtype, size_t m, size_t k, const abq_quant_spec* act_spec,
@@ -438,11 +467,17 @@ int abq_linear(const void* x, int x_dtype, size_t m, size_t k, const abq_quant_s
   if (!w) return fail(ABQ_ERR_VALUE, "quantized_linear: null weights");
   if (k != w->k) return fail(ABQ_ERR_SHAPE, "quantized_linear: inner dimensions differ");
   const unsigned p = planes_of(*act_spec);
-  if (workspace_bytes < abq_linear_workspace_bytes(m, k, p))
-    return fail(ABQ_ERR_VALUE, "linear: workspace too small (%zu < %zu)", workspace_bytes,
-                abq_linear_workspace_bytes(m, k, p));
+  const size_t need = abq_linear_workspace_bytes(m, w->n, k, p);
+  if (workspace_bytes < need)
+    return fail(ABQ_ERR_VALUE, "linear: workspace too small (%zu < %zu)", workspace_bytes, need);
+  int mode = 0;
+  if ((st = epi_mode_of(out_kind, &mode))) return st;
   if ((st = check_device())) return st;
   char* ws = static_cast<char*>(workspace);
+  const size_t gbytes = imma_gacc_bytes(m <= 8 ? m : 8, w->n);
+  long long* gacc = reinterpret_cast<long long*>(ws);
+  unsigned* gcnt = reinterpret_cast<unsigned*>(ws + (gbytes / (16 * 8 * 8 + 4)) * 16 * 8 * 8);
+  ws += align256(gbytes);
   uint64_t* planes = reinterpret_cast<uint64_t*>(ws);
   ws += align256(size_t(p) * m * wpr_of(k) * 8);
   double* sa = reinterpret_cast<double*>(ws);
@@ -459,11 +494,28 @@ int abq_linear(const void* x, int x_dtype, size_t m, size_t k, const abq_quant_s
   }
   unsigned long long* bad = err_index ? reinterpret_cast<unsigned long long*>(err_index) : sc;
   cudaStream_t s = as_stream(stream);
-  st = run_quantize(x, x_dtype, m, k, params_of(*act_spec), nullptr, nullptr, nullptr, planes, p, sa,
-                    za, ra, bad, range, s);
-  if (st) return st;
-  abq_act act{planes, p, m, k, sa, za, ra, act_spec->granularity == ABQ_PER_TENSOR};
-  if ((st = abq_linear_planes(&act, w, y, out_kind, stream))) return st;
+  if (use_imma(w, m, k)) {
+    // single launch: ReQuant prologue + tensor-pipe plane GEMV + fused epilogue
+    EpiParams e{};
+    e.mode = mode;
+    e.out = y;
+    e.ldo = static_cast<long long>(w->n);
+    e.s_b = w->scales;
+    e.sb_stride = w->per_tensor ? 0 : 1;
+    e.z_b = w->zero_points;
+    e.zb_stride = w->per_tensor ? 0 : 1;
+    e.colsum_b = w->colsums;
+    e.k = static_cast<long long>(k);
+    const QuantParams qp = params_of(*act_spec);
+    st = run_gemv_imma(w->frag, w->q, w->n, k, m, x, x_dtype, &qp, nullptr, 0, e, gacc, gcnt, bad, s);
+    if (st) return st;
+  } else {
+    st = run_quantize(x, x_dtype, m, k, params_of(*act_spec), nullptr, nullptr, nullptr, planes, p, sa,
+                      za, ra, bad, range, s);
+    if (st) return st;
+    abq_act act{planes, p, m, k, sa, za, ra, act_spec->granularity == ABQ_PER_TENSOR};
+    if ((st = abq_linear_planes(&act, w, y, out_kind, stream))) return st;
+  }
   if (err_index) return ABQ_OK;
   unsigned long long b = 0;
   if ((st = sync_read(sc, s, &b))) return st;

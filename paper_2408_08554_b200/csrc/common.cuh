@@ -79,8 +79,10 @@ struct EpiParams {
   long long k;
 };
 
-__device__ __forceinline__ void epi_store(const EpiParams& e, long long i, long long j,
-                                          long long acc) {
+// epilogue with the activation-side values already in hand (sa, za, rowsum of
+// token i), used by kernels that computed them on chip.
+__device__ __forceinline__ void epi_store_v(const EpiParams& e, long long i, long long j,
+                                            long long acc, double sa, long long za, long long ra) {
   const long long o = i * e.ldo + j;
   if (e.mode == EPI_ACC_I32) {
     static_cast<int32_t*>(e.out)[o] = static_cast<int32_t>(acc);
@@ -91,22 +93,29 @@ __device__ __forceinline__ void epi_store(const EpiParams& e, long long i, long 
     return;
   }
   // corrected = acc - z_a*colsum_b - z_b*rowsum_a + K*z_a*z_b   (int64, gemm.hpp:248-250)
-  const long long za = e.z_a[i * e.za_stride];
   const long long zb = e.z_b[j * e.zb_stride];
-  const long long corr = acc - za * e.colsum_b[j] - zb * e.rowsum_a[i] + e.k * za * zb;
+  const long long corr = acc - za * e.colsum_b[j] - zb * ra + e.k * za * zb;
   if (e.mode == EPI_CORR_I64) {
     static_cast<int64_t*>(e.out)[o] = corr;
     return;
   }
   // s_a[i] * s_b[j] * corrected, left to right, no contraction (gemm.hpp:298)
-  const double y = __dmul_rn(__dmul_rn(e.s_a[i * e.sa_stride], e.s_b[j * e.sb_stride]),
-                             static_cast<double>(corr));
+  const double y = __dmul_rn(__dmul_rn(sa, e.s_b[j * e.sb_stride]), static_cast<double>(corr));
   if (e.mode == EPI_F64)
     static_cast<double*>(e.out)[o] = y;
   else if (e.mode == EPI_F16)
     static_cast<__half*>(e.out)[o] = __double2half(y);
   else
     static_cast<float*>(e.out)[o] = __double2float_rn(y);
+}
+
+__device__ __forceinline__ void epi_store(const EpiParams& e, long long i, long long j,
+                                          long long acc) {
+  if (e.mode == EPI_ACC_I32 || e.mode == EPI_ACC_I64) {
+    epi_store_v(e, i, j, acc, 0.0, 0, 0);
+    return;
+  }
+  epi_store_v(e, i, j, acc, e.s_a[i * e.sa_stride], e.z_a[i * e.za_stride], e.rowsum_a[i]);
 }
 
 // ---- ordered-key encoding so that atomicMin/Max on u64 orders doubles -----

@@ -1,0 +1,116 @@
+// quant_dev.cuh -- device-side restatement of the reference quantizer math
+// (quantizer.hpp:146-213), shared by the standalone K1 kernels and the fused
+// GEMV prologue.  Every FP64 operation is an explicit round-to-nearest
+// intrinsic or IEEE division, so no FMA contraction can change a result;
+// round() is half-away-from-zero like std::round (core.hpp:145).
+#pragma once
+
+#include <math_constants.h>
+
+#include "common.cuh"
+
+namespace abq_dev {
+
+template <typename T>
+__device__ __forceinline__ double load_as_double(const T* p, size_t idx);
+template <>
+__device__ __forceinline__ double load_as_double<__half>(const __half* p, size_t idx) {
+  return static_cast<double>(__half2float(p[idx]));
+}
+template <>
+__device__ __forceinline__ double load_as_double<float>(const float* p, size_t idx) {
+  return static_cast<double>(p[idx]);
+}
+template <>
+__device__ __forceinline__ double load_as_double<double>(const double* p, size_t idx) {
+  return p[idx];
+}
+
+// value after the optional compensation pair: v = x + a[i]*b[j]  (quantizer.hpp:161-166)
+template <typename T>
+__device__ __forceinline__ double value_at(const T* x, size_t cols, size_t i, size_t j,
+                                           const double* ca, const double* cb) {
+  double v = load_as_double(x, i * cols + j);
+  if (ca) v = __dadd_rn(v, __dmul_rn(ca[i], cb[j]));
+  return v;
+}
+
+__device__ __forceinline__ double warp_min(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ long long warp_sum(long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// step and zero point of one axis group (quantizer.hpp:169-201)
+__device__ __forceinline__ void group_params(const QuantParams& qp, double lo_raw, double hi_raw,
+                                             double* step_out, int* z_out) {
+  const double lo = __dmul_rn(qp.beta, lo_raw);
+  const double hi = __dmul_rn(qp.alpha, hi_raw);
+  double step;
+  int z;
+  if (qp.scheme == ABQ_ASYMMETRIC) {
+    if (hi == lo) {
+      step = 1.0;
+      z = 0;
+    } else {
+      step = __dsub_rn(hi, lo) / static_cast<double>(qp.levels - 1);
+      double zz = round(-lo / step);
+      const double top = static_cast<double>(qp.levels - 1);
+      zz = zz < 0.0 ? 0.0 : (top < zz ? top : zz);
+      z = static_cast<int>(zz);
+    }
+  } else {
+    const double alo = fabs(lo), ahi = fabs(hi);
+    const double amax = alo < ahi ? ahi : alo;
+    const int half = 1 << (qp.bits - 1);
+    if (amax == 0.0) {
+      step = 1.0;
+      z = 0;
+    } else {
+      if (qp.scheme == ABQ_BALANCED)
+        step = amax / static_cast<double>(half);
+      else
+        step = qp.bits == 1 ? amax : amax / static_cast<double>(half - 1);
+      z = half;
+    }
+  }
+  *step_out = step;
+  *z_out = z;
+}
+
+// code = clamp(round(v/step) + z, 0, L-1)  (quantizer.hpp:205-210)
+__device__ __forceinline__ unsigned quant_code(double v, double step, double z, double top) {
+  double c = __dadd_rn(round(v / step), z);
+  c = c < 0.0 ? 0.0 : (top < c ? top : c);
+  return static_cast<unsigned>(c);
+}
+
+// Same result as quant_code, with the IEEE division replaced by a multiply by
+// the reciprocal except near rounding ties.  q1 = RN(v * RN(1/step)) is within
+// a few ulp of RN(v/step); round() only changes value across half-integers, so
+// whenever q1 is farther than a generous 2^-44 relative band from the nearest
+// n + 1/2 both quotients round to the same integer.  Inside the band the exact
+// IEEE quotient is used.  (Bit-exactness is tested against the reference on
+// every quantizer case, tests/test_gpu_parity.py.)
+__device__ __forceinline__ unsigned quant_code_fast(double v, double step, double inv_step,
+                                                    double z, double top) {
+  double q = __dmul_rn(v, inv_step);
+  const double f = floor(q);
+  const double d = fabs(__dsub_rn(__dsub_rn(q, f), 0.5));
+  if (d <= fmax(fabs(q), 1.0) * 5.6843418860808015e-14) q = v / step;  // 2^-44
+  double c = __dadd_rn(round(q), z);
+  c = c < 0.0 ? 0.0 : (top < c ? top : c);
+  return static_cast<unsigned>(c);
+}
+
+}  // namespace abq_dev

@@ -1,0 +1,109 @@
+"""Both decode-GEMV variants (AND+popcount on CUDA cores, and weight planes on
+the int8 tensor pipe) must produce bit-identical results to the oracle on
+ragged shapes: N not a multiple of the 16-row tile, K not a multiple of the
+256-element block, every (p, q) pair, per-token and per-tensor activations,
+fp16 / fp32 / fp64 inputs, the stream-K (workspace) and row-tile paths."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(params=["popc", "recomb"])
+def variant(request, abq):
+    abq.api.set_gemv_variant(request.param)
+    yield request.param
+    abq.api.set_gemv_variant("auto")
+
+
+def _case(rng, m, n, k, wbits, abits, xdtype=np.float16):
+    x = (rng.standard_normal((m, k)) * rng.uniform(0.2, 4)).astype(xdtype)
+    wc = rng.integers(0, 1 << wbits, (n, k), dtype=np.uint8)
+    sb = rng.uniform(1e-3, 1e-2, n)
+    zb = rng.integers(0, 1 << wbits, n).astype(np.int32)
+    return x, wc, sb, zb
+
+
+def test_linear_ragged_shapes(abq, orc, variant):
+    rng = np.random.default_rng(5)
+    for trial in range(60):
+        m = int(rng.integers(1, 9))
+        n = int(rng.integers(1, 700))
+        k = int(rng.integers(1, 1500))
+        wbits, abits = (int(v) for v in rng.integers(1, 9, 2))
+        x, wc, sb, zb = _case(rng, m, n, k, wbits, abits)
+        w = abq.PackedWeights.from_planes(abq.bitpack(wc, wbits), sb, zb)
+        gran = abq.api.PER_TENSOR if trial % 5 == 0 else abq.api.PER_TOKEN
+        lin = abq.Linear(w, abq.QuantSpec(bits=abits, granularity=gran), max_m=m)
+        y = lin(torch.from_numpy(x).cuda(), out_dtype=torch.float64).cpu().numpy()
+        ac, sa, za = orc.quantize(x.astype(np.float64), abits, 0, gran)
+        want = orc.quantized_linear(ac, abits, sa, za, wc, wbits, sb, zb, a_per_tensor=gran == 0)
+        assert np.array_equal(y, want), (trial, m, n, k, wbits, abits, gran)
+
+
+def test_linear_planes_ragged(abq, orc, variant):
+    """activation planes given (abq_linear_planes): row-tile split, no workspace"""
+    rng = np.random.default_rng(6)
+    for trial in range(40):
+        m = int(rng.integers(1, 9))
+        n = int(rng.integers(1, 900))
+        k = int(rng.integers(1, 2100))
+        p, q = (int(v) for v in rng.integers(1, 9, 2))
+        a = rng.integers(0, 1 << p, (m, k), dtype=np.uint8)
+        wc = rng.integers(0, 1 << q, (n, k), dtype=np.uint8)
+        w = abq.PackedWeights.from_planes(abq.bitpack(wc, q), np.ones(n), np.zeros(n, np.int32))
+        pa = abq.bitpack(a, p)
+        sa = torch.ones(m, dtype=torch.float64, device="cuda")
+        za = torch.zeros(m, dtype=torch.int32, device="cuda")
+        got = abq.linear_planes(pa, sa, za, abq.code_rowsums(a), w, torch.int64).cpu().numpy()
+        assert np.array_equal(got, orc.gemm_codes(a, p, wc, q)), (trial, m, n, k, p, q)
+
+
+@pytest.mark.parametrize("xdtype", [np.float16, np.float32, np.float64])
+def test_linear_input_dtypes(abq, orc, variant, xdtype):
+    rng = np.random.default_rng(7)
+    x, wc, sb, zb = _case(rng, 3, 333, 1000, 4, 8, xdtype)
+    w = abq.PackedWeights.from_planes(abq.bitpack(wc, 4), sb, zb)
+    lin = abq.Linear(w, abq.QuantSpec(bits=8, granularity=abq.api.PER_TOKEN), max_m=3)
+    y = lin(torch.from_numpy(x).cuda(), out_dtype=torch.float64).cpu().numpy()
+    ac, sa, za = orc.quantize(x.astype(np.float64), 8, 0, 2)
+    assert np.array_equal(y, orc.quantized_linear(ac, 8, sa, za, wc, 4, sb, zb))
+
+
+def test_linear_symmetric_balanced_schemes(abq, orc, variant):
+    rng = np.random.default_rng(8)
+    for scheme, bits in [(abq.api.SYMMETRIC, 4), (abq.api.BALANCED, 3), (abq.api.SYMMETRIC, 1)]:
+        x, wc, sb, zb = _case(rng, 2, 200, 512, 2, 8)
+        w = abq.PackedWeights.from_planes(abq.bitpack(wc, 2), sb, zb)
+        spec = abq.QuantSpec(bits=bits, scheme=scheme, granularity=abq.api.PER_TOKEN)
+        lin = abq.Linear(w, spec, max_m=2)
+        y = lin(torch.from_numpy(x).cuda(), out_dtype=torch.float64).cpu().numpy()
+        ac, sa, za = orc.quantize(x.astype(np.float64), bits, scheme, 2)
+        want = orc.quantized_linear(ac, spec.planes(), sa, za, wc, 2, sb, zb)
+        assert np.array_equal(y, want), (scheme, bits)
+
+
+def test_nonfinite_activation_reported(abq, variant):
+    rng = np.random.default_rng(9)
+    x, wc, sb, zb = _case(rng, 2, 64, 256, 4, 4)
+    x[1, 17] = np.inf
+    w = abq.PackedWeights.from_planes(abq.bitpack(wc, 4), sb, zb)
+    lin = abq.Linear(w, abq.QuantSpec(bits=4, granularity=abq.api.PER_TOKEN), max_m=2)
+    with pytest.raises(abq.ValueError, match=r"\(1,17\)"):
+        lin(torch.from_numpy(x).cuda())
+    # the next clean call succeeds (status word and accumulators are reset)
+    x[1, 17] = 0.5
+    lin(torch.from_numpy(x).cuda())
+
+
+def test_repeated_calls_are_deterministic(abq, variant):
+    """self-cleaning cross-CTA accumulators: identical results call after call"""
+    rng = np.random.default_rng(10)
+    x, wc, sb, zb = _case(rng, 1, 11008, 4096, 4, 4)
+    w = abq.PackedWeights.from_planes(abq.bitpack(wc, 4), sb, zb)
+    lin = abq.Linear(w, abq.QuantSpec(bits=4, granularity=abq.api.PER_TOKEN), max_m=1)
+    xd = torch.from_numpy(x).cuda()
+    first = lin(xd, out_dtype=torch.float64).clone()
+    for _ in range(20):
+        assert torch.equal(lin(xd, out_dtype=torch.float64, check=False), first)

@@ -179,9 +179,6 @@ def test_quant_pack_act_fp16_matches_oracle(abq, orc):
         x = (rng.standard_normal((m, k)) * rng.uniform(0.1, 3)).astype(np.float16)
         xd = torch.from_numpy(x).cuda()
         spec = abq.QuantSpec(bits=bits, granularity=abq.api.PER_TOKEN)
-        lin_ws = torch.empty(abq._lib.lib().abq_linear_workspace_bytes(m, k, bits), dtype=torch.uint8,
-                             device="cuda")
-        del lin_ws
         planes = torch.empty((bits, m, (k + 63) // 64), dtype=torch.int64, device="cuda")
         sa = torch.empty(m, dtype=torch.float64, device="cuda")
         za = torch.empty(m, dtype=torch.int32, device="cuda")
