@@ -300,6 +300,7 @@ def run_ours(args, world, rank, local):
     if args.variant == "popc":  # keep only the ABQP planes resident
         for w in weights:
             w.frag = None
+            w.tc = None
     spec = abq.QuantSpec(bits=ab, granularity=abq.api.PER_TOKEN)
     lins = [abq.Linear(w, spec, max_m=m) for w in weights]
     x = torch.from_numpy(x_np).cuda()

@@ -449,11 +449,18 @@ inline Mat quantized_linear(const QuantizedTensor& act, const QuantizedTensor& w
   detail::DeviceBuffer<std::int32_t> dza(act.zero_points), dzb(wt.zero_points);
   abq_act a{dap.get(), p, m, k, dsa.get(), dza.get(), dra.get(),
             act.spec.granularity == Granularity::PerTensor};
-  // fragment-major copy for the tensor-pipe decode GEMV (used when m <= 8)
-  detail::DeviceBuffer<std::uint32_t> dfrag(m <= 8 ? abq_weights_frag_bytes(q, n, k) / 4 : 0);
-  if (m <= 8) detail::check(abq_weights_prepack(dwp.get(), q, n, k, dfrag.get(), nullptr));
+  // engine re-layout of the planes: fragment-major for the tensor-pipe decode
+  // GEMV (m <= 8), tc planes for the tcgen05 prefill GEMM (m >= 9)
+  const bool decode = m <= 8;
+  detail::DeviceBuffer<std::uint32_t> dlay(decode ? abq_weights_frag_bytes(q, n, k) / 4
+                                                  : abq_weights_tc_bytes(q, n, k) / 4);
+  if (decode)
+    detail::check(abq_weights_prepack(dwp.get(), q, n, k, dlay.get(), nullptr));
+  else
+    detail::check(abq_weights_prepack_tc(dwp.get(), q, n, k, dlay.get(), nullptr));
   abq_weights w{dwp.get(), q, n, k, dsb.get(), dzb.get(), dcb.get(),
-                wt.spec.granularity == Granularity::PerTensor, m <= 8 ? dfrag.get() : nullptr};
+                wt.spec.granularity == Granularity::PerTensor, decode ? dlay.get() : nullptr,
+                decode ? nullptr : dlay.get()};
   Mat out(m, n);
   detail::DeviceBuffer<double> dy(out.data.size());
   detail::check(abq_linear_planes(&a, &w, dy.get(), ABQ_OUT_F64, nullptr));
@@ -477,15 +484,17 @@ class Weights {
       : q_(wt.spec.planes()), n_(wt.rows()), k_(wt.cols()),
         per_tensor_(wt.spec.granularity == Granularity::PerTensor),
         planes_(std::size_t(q_) * n_ * ((k_ + 63) / 64)), scales_(wt.scales),
-        zps_(wt.zero_points), colsums_(n_), frag_(abq_weights_frag_bytes(q_, n_, k_) / 4) {
+        zps_(wt.zero_points), colsums_(n_), frag_(abq_weights_frag_bytes(q_, n_, k_) / 4),
+        tc_(abq_weights_tc_bytes(q_, n_, k_) / 4) {
     detail::DeviceBuffer<std::uint8_t> dc(wt.codes.data);
     detail::check(abq_bitpack(dc.get(), n_, k_, q_, planes_.get(), nullptr));
     detail::check(abq_plane_rowsums(planes_.get(), q_, n_, k_, colsums_.get(), nullptr));
     detail::check(abq_weights_prepack(planes_.get(), q_, n_, k_, frag_.get(), nullptr));
+    detail::check(abq_weights_prepack_tc(planes_.get(), q_, n_, k_, tc_.get(), nullptr));
   }
   abq_weights view() const {
     return abq_weights{planes_.get(), q_, n_, k_, scales_.get(), zps_.get(), colsums_.get(),
-                       per_tensor_ ? 1 : 0, frag_.get()};
+                       per_tensor_ ? 1 : 0, frag_.get(), tc_.get()};
   }
   std::size_t n() const { return n_; }
   std::size_t k() const { return k_; }
@@ -499,6 +508,7 @@ class Weights {
   detail::DeviceBuffer<std::int32_t> zps_;
   detail::DeviceBuffer<std::int64_t> colsums_;
   detail::DeviceBuffer<std::uint32_t> frag_;
+  detail::DeviceBuffer<std::uint32_t> tc_;
 };
 
 /// ReQuant + BitPacking + plane GEMV/GEMM + fused epilogue on device pointers.

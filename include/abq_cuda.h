@@ -91,6 +91,9 @@ typedef struct {
   /* optional fragment-major copy of the planes for the tensor-pipe decode
    * GEMV (abq_weights_prepack); NULL = AND+popcount kernels only */
   const uint32_t* frag;
+  /* optional tcgen05-GEMM copy of the planes (abq_weights_prepack_tc) used
+   * for M >= 9 tokens; NULL = no prefill tensor-core path */
+  const uint32_t* tc;
 } abq_weights;
 
 /* Activation-side metadata produced by abq_quant_pack_act (per-token or
@@ -191,6 +194,12 @@ int abq_plane_rowsums(const uint64_t* planes, unsigned bits, size_t rows, size_t
 size_t abq_weights_frag_bytes(unsigned q, size_t n, size_t k);
 int abq_weights_prepack(const uint64_t* planes, unsigned q, size_t n, size_t k, uint32_t* frag,
                         void* stream);
+/* K5 for the prefill GEMM: ABQP planes -> [row-tile 128][k-block 128][plane]
+ * [row][4 x u32] (bit 8b+c of word j <-> k = 32j + 4c + b), the layout the
+ * tcgen05 kernel rebuilds u8 codes from. */
+size_t abq_weights_tc_bytes(unsigned q, size_t n, size_t k);
+int abq_weights_prepack_tc(const uint64_t* planes, unsigned q, size_t n, size_t k, uint32_t* tc,
+                           void* stream);
 
 /* Fused engine linear on packed operands (K2/K3 + K4):
  *   y[i][j] = s_a[i] * s_b[j] * corrected[i][j]        gemm.hpp:266-307
@@ -228,6 +237,11 @@ typedef enum {
 } abq_gemv_variant;
 int abq_set_gemv_variant(int variant);
 int abq_get_gemv_variant(void);
+
+/* Profiling hook: when set (device buffer of >= 4 u64 per CTA, NULL = off),
+ * the decode GEMV records %globaltimer at kernel start, after the ReQuant
+ * prologue, after the main loop and before the split-tile epilogue. */
+int abq_set_trace_buffer(void* dev_words);
 
 #ifdef __cplusplus
 }

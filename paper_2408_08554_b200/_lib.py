@@ -39,7 +39,7 @@ class GemmStatsC(C.Structure):
 class WeightsC(C.Structure):
     _fields_ = [("planes", C.c_void_p), ("q", C.c_uint), ("n", C.c_size_t), ("k", C.c_size_t),
                 ("scales", C.c_void_p), ("zero_points", C.c_void_p), ("colsums", C.c_void_p),
-                ("per_tensor", C.c_int), ("frag", C.c_void_p)]
+                ("per_tensor", C.c_int), ("frag", C.c_void_p), ("tc", C.c_void_p)]
 
 
 class ActC(C.Structure):
@@ -79,12 +79,15 @@ _SIGNATURES = {
     "abq_plane_rowsums": (_I, [_P, _U, _S, _S, _P, _P]),
     "abq_weights_frag_bytes": (_S, [_U, _S, _S]),
     "abq_weights_prepack": (_I, [_P, _U, _S, _S, _P, _P]),
+    "abq_weights_tc_bytes": (_S, [_U, _S, _S]),
+    "abq_weights_prepack_tc": (_I, [_P, _U, _S, _S, _P, _P]),
     "abq_linear_planes": (_I, [C.POINTER(ActC), C.POINTER(WeightsC), _P, _I, _P]),
     "abq_linear_workspace_bytes": (_S, [_S, _S, _S, _U]),
     "abq_linear": (_I, [_P, _I, _S, _S, C.POINTER(QuantSpecC), C.POINTER(WeightsC), _P, _I, _P, _S,
                         _P, _P]),
     "abq_set_gemv_variant": (_I, [_I]),
     "abq_get_gemv_variant": (_I, []),
+    "abq_set_trace_buffer": (_I, [_P]),
 }
 
 

@@ -402,33 +402,37 @@ class PackedWeights:
     zero_points: torch.Tensor
     colsums: torch.Tensor
     per_tensor: bool
-    frag: Optional[torch.Tensor] = None  # fragment-major copy for the tensor-pipe GEMV
+    frag: Optional[torch.Tensor] = None  # fragment-major copy for the tensor-pipe GEMV (M <= 8)
+    tc: Optional[torch.Tensor] = None    # tcgen05-GEMM copy (M >= 9)
 
     @staticmethod
-    def from_quantized(wt: QuantizedTensor, frag: bool = True) -> "PackedWeights":
+    def from_quantized(wt: QuantizedTensor, frag: bool = True, tc: bool = True) -> "PackedWeights":
         pm = bitpack(wt.codes, wt.spec.planes())
         return PackedWeights(pm, wt.scales.contiguous(), wt.zero_points.contiguous(),
                              plane_rowsums(pm), wt.spec.granularity == PER_TENSOR,
-                             prepack_frag(pm) if frag else None)
+                             prepack_frag(pm) if frag else None, prepack_tc(pm) if tc else None)
 
     @staticmethod
     def from_planes(pm: BitPlaneMatrix, scales, zero_points, per_tensor=False,
-                    frag: bool = True) -> "PackedWeights":
+                    frag: bool = True, tc: bool = True) -> "PackedWeights":
         return PackedWeights(pm, _to_dev(scales, torch.float64), _to_dev(zero_points, torch.int32),
-                             plane_rowsums(pm), per_tensor, prepack_frag(pm) if frag else None)
+                             plane_rowsums(pm), per_tensor, prepack_frag(pm) if frag else None,
+                             prepack_tc(pm) if tc else None)
 
     def c(self) -> L.WeightsC:
         return L.WeightsC(_ptr(self.planes.data), self.planes.planes, self.planes.rows,
                           self.planes.cols, _ptr(self.scales), _ptr(self.zero_points),
                           _ptr(self.colsums), int(self.per_tensor),
-                          _ptr(self.frag) if self.frag is not None else None)
+                          _ptr(self.frag) if self.frag is not None else None,
+                          _ptr(self.tc) if self.tc is not None else None)
 
     def copy(self) -> "PackedWeights":
         """Distinct HBM copy of the packed weights (same values)."""
         pm = BitPlaneMatrix(self.planes.planes, self.planes.rows, self.planes.cols,
                             self.planes.data.clone())
         return PackedWeights(pm, self.scales, self.zero_points, self.colsums, self.per_tensor,
-                             self.frag.clone() if self.frag is not None else None)
+                             self.frag.clone() if self.frag is not None else None,
+                             self.tc.clone() if self.tc is not None else None)
 
     def shard(self, rank: int, world: int) -> "PackedWeights":
         """Column-parallel slice: output channels [rank*N/G, (rank+1)*N/G)
@@ -440,7 +444,8 @@ class PackedWeights:
         s = self.scales if self.per_tensor else self.scales[lo:hi].contiguous()
         z = self.zero_points if self.per_tensor else self.zero_points[lo:hi].contiguous()
         return PackedWeights(pm, s, z, self.colsums[lo:hi].contiguous(), self.per_tensor,
-                             prepack_frag(pm) if self.frag is not None else None)
+                             prepack_frag(pm) if self.frag is not None else None,
+                             prepack_tc(pm) if self.tc is not None else None)
 
 
 def prepack_frag(pm: BitPlaneMatrix) -> torch.Tensor:
@@ -449,6 +454,14 @@ def prepack_frag(pm: BitPlaneMatrix) -> torch.Tensor:
     frag = torch.empty(max(1, nbytes // 4), dtype=torch.int32, device=_dev())
     _check(L.lib().abq_weights_prepack(_ptr(pm.data), pm.planes, pm.rows, pm.cols, _ptr(frag), _stream()))
     return frag
+
+
+def prepack_tc(pm: BitPlaneMatrix) -> torch.Tensor:
+    """K5: ABQP planes -> tc planes for the tcgen05 prefill GEMM."""
+    nbytes = L.lib().abq_weights_tc_bytes(pm.planes, pm.rows, pm.cols)
+    tc = torch.empty(max(1, nbytes // 4), dtype=torch.int32, device=_dev())
+    _check(L.lib().abq_weights_prepack_tc(_ptr(pm.data), pm.planes, pm.rows, pm.cols, _ptr(tc), _stream()))
+    return tc
 
 
 def set_gemv_variant(variant: str) -> None:

@@ -82,18 +82,32 @@ int run_bmma(const uint64_t* a, size_t m, unsigned a_plane, const uint64_t* bt, 
 int run_gemm_popc(const uint64_t* A, unsigned p, size_t m, const uint64_t* W, unsigned q, size_t n,
                   size_t k, bool wide, const EpiParams& e, cudaStream_t st);
 size_t frag_words(unsigned q, size_t n, size_t k);
-size_t imma_gacc_bytes(size_t m, size_t n);
+size_t imma_ws_bytes(size_t n, size_t k);
 bool imma_supported(size_t m, size_t k);
+unsigned long long*& trace_buffer();
 int run_prepack_frag(const uint64_t* planes, unsigned q, size_t n, size_t k, uint32_t* frag,
                      cudaStream_t st);
-int run_gemv_imma(const uint32_t* frag, unsigned q, size_t n, size_t k, size_t m, const void* x,
-                  int x_dtype, const QuantParams* qp, const uint64_t* a_planes, unsigned p,
-                  const EpiParams& e, long long* gacc, unsigned* gcnt, unsigned long long* bad,
-                  cudaStream_t st);
+int run_gemv_imma_planes(const uint32_t* frag, unsigned q, size_t n, size_t k, size_t m,
+                         const uint64_t* a_planes, unsigned p, const EpiParams& e, cudaStream_t st);
+int run_gemv_imma_fused(const uint32_t* frag, unsigned q, size_t n, size_t k, size_t m, const void* x,
+                        int x_dtype, const QuantParams& qp, const EpiParams& e, void* ws,
+                        unsigned long long* bad_out, cudaStream_t st);
+
+size_t tc_words(unsigned q, size_t n, size_t k);
+int run_prepack_tc(const uint64_t* planes, unsigned q, size_t n, size_t k, uint32_t* out,
+                   cudaStream_t st);
+bool gemm_tc_supported(size_t k, size_t ldk);
+int run_gemm_tc(const uint32_t* wtc, unsigned q, size_t n, size_t k, const uint8_t* act, size_t ldk,
+                size_t m, const EpiParams& e, cudaStream_t st);
 
 // decode GEMV on the tensor pipe: weights prepacked, M <= 8 tokens
 static bool use_imma(const abq_weights* w, size_t m, size_t k) {
   return w->frag != nullptr && m >= 1 && m <= 8 && imma_supported(m, k) &&
+         g_gemv_variant != ABQ_GEMV_POPC;
+}
+// prefill GEMM on tcgen05: weights prepacked (tc planes), M >= 9 tokens
+static bool use_tc(const abq_weights* w, size_t m, size_t k, bool wide) {
+  return w->tc != nullptr && m >= 9 && !wide && gemm_tc_supported(k, k) &&
          g_gemv_variant != ABQ_GEMV_POPC;
 }
 
@@ -178,6 +192,28 @@ static void add_stats(abq_gemm_stats* stats, const abq_tile_config& t, size_t m,
   stats->plane_pair_products += tiles * p * q;
 }
 
+// tcgen05 GEMM from packed activation planes: recombine the activation planes
+// to u8 codes (unpack kernel) and, when no tc-layout weights are resident,
+// re-lay the ABQP weight planes out for the GEMM, in stream-ordered scratch.
+static int gemm_tc_from_planes(const uint64_t* a, unsigned p, size_t m, const uint64_t* w_planes,
+                               const uint32_t* wtc, unsigned q, size_t n, size_t k,
+                               const EpiParams& e, cudaStream_t s) {
+  uint8_t* codes = nullptr;
+  ABQ_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&codes), m * k, s));
+  int st = run_unpack(a, p, m, k, codes, s);
+  uint32_t* tmp = nullptr;
+  if (!st && !wtc) {
+    cudaError_t err = cudaMallocAsync(reinterpret_cast<void**>(&tmp), tc_words(q, n, k) * 4, s);
+    if (err != cudaSuccess) st = fail(ABQ_ERR_CUDA, "gemm_tc: scratch: %s", cudaGetErrorString(err));
+    if (!st) st = run_prepack_tc(w_planes, q, n, k, tmp, s);
+    wtc = tmp;
+  }
+  if (!st) st = run_gemm_tc(wtc, q, n, k, codes, k, m, e, s);
+  cudaFreeAsync(codes, s);
+  if (tmp) cudaFreeAsync(tmp, s);
+  return st;
+}
+
 static EpiParams raw_epi(void* out, size_t n, bool wide) {
   EpiParams e{};
   e.mode = wide ? EPI_ACC_I64 : EPI_ACC_I32;
@@ -232,6 +268,11 @@ int abq_set_gemv_variant(int variant) {
   return ABQ_OK;
 }
 int abq_get_gemv_variant(void) { return g_gemv_variant; }
+
+int abq_set_trace_buffer(void* dev_words) {
+  trace_buffer() = static_cast<unsigned long long*>(dev_words);
+  return ABQ_OK;
+}
 
 // ---- quantizer -------------------------------------------------------------
 int abq_quantize(const void* x, int x_dtype, size_t rows, size_t cols, const abq_quant_spec* spec,
@@ -334,6 +375,10 @@ static int gemm_common(const char* name, const uint64_t* a, unsigned p, size_t m
   if (m * n > 0 && a_k == 0) {
     // K == 0: every sum is empty
     ABQ_CUDA_TRY(cudaMemsetAsync(out, 0, m * n * (wide ? 8 : 4), as_stream(stream)));
+  } else if (m >= 16 && !wide && gemm_tc_supported(a_k, a_k) && g_gemv_variant != ABQ_GEMV_POPC) {
+    // prefill-shaped: recombined planes on tcgen05 (weights re-laid out per call)
+    st = gemm_tc_from_planes(a, p, m, bt, nullptr, q, n, a_k, raw_epi(out, n, wide), as_stream(stream));
+    if (st) return st;
   } else {
     st = run_gemm_popc(a, p, m, bt, q, n, a_k, wide, raw_epi(out, n, wide), as_stream(stream));
     if (st) return st;
@@ -407,6 +452,16 @@ int abq_weights_prepack(const uint64_t* planes, unsigned q, size_t n, size_t k, 
   return run_prepack_frag(planes, q, n, k, frag, as_stream(stream));
 }
 
+size_t abq_weights_tc_bytes(unsigned q, size_t n, size_t k) { return tc_words(q, n, k) * 4; }
+
+int abq_weights_prepack_tc(const uint64_t* planes, unsigned q, size_t n, size_t k, uint32_t* tc,
+                           void* stream) {
+  if (q < 1 || q > 8) return fail(ABQ_ERR_VALUE, "weights_prepack_tc: plane count must be in [1,8]");
+  int st = check_device();
+  if (st) return st;
+  return run_prepack_tc(planes, q, n, k, tc, as_stream(stream));
+}
+
 // ---- fused linear ----------------------------------------------------------
 static int epi_mode_of(int out_kind, int* mode) {
   switch (out_kind) {
@@ -445,8 +500,11 @@ int abq_linear_planes(const abq_act* act, const abq_weights* w, void* y, int out
   e.k = static_cast<long long>(act->k);
   const bool wide = !fits_int32_host(act->p, w->q, act->k);
   if (use_imma(w, act->m, act->k))
-    return run_gemv_imma(w->frag, w->q, w->n, act->k, act->m, nullptr, -1, nullptr, act->planes,
-                         act->p, e, nullptr, nullptr, nullptr, as_stream(stream));
+    return run_gemv_imma_planes(w->frag, w->q, w->n, act->k, act->m, act->planes, act->p, e,
+                                as_stream(stream));
+  if (use_tc(w, act->m, act->k, wide))
+    return gemm_tc_from_planes(act->planes, act->p, act->m, w->planes, w->tc, w->q, w->n, act->k, e,
+                               as_stream(stream));
   return run_gemm_popc(act->planes, act->p, act->m, w->planes, w->q, w->n, act->k, wide, e,
                        as_stream(stream));
 }
@@ -454,9 +512,10 @@ int abq_linear_planes(const abq_act* act, const abq_weights* w, void* y, int out
 static size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 
 size_t abq_linear_workspace_bytes(size_t m, size_t n, size_t k, unsigned act_planes) {
-  // [gacc + gcnt for the stream-K decode GEMV][act planes][s_a][z_a][rowsum_a][range]
-  return align256(imma_gacc_bytes(m <= 8 ? m : 8, n)) + align256(size_t(act_planes) * m * wpr_of(k) * 8) +
-         align256(m * 8) + align256(m * 4) + align256(m * 8) + 256;
+  // [gacc + gcnt for the stream-K decode GEMV][act planes][s_a][z_a][rowsum_a][range 256 B]
+  // [u8 act codes m x k for the tcgen05 GEMM]
+  return align256(imma_ws_bytes(n, k)) + align256(size_t(act_planes) * m * wpr_of(k) * 8) +
+         align256(m * 8) + align256(m * 4) + align256(m * 8) + 256 + align256(m * k);
 }
 
 int abq_linear(const void* x, int x_dtype, size_t m, size_t k, const abq_quant_spec* act_spec,
@@ -474,10 +533,8 @@ int abq_linear(const void* x, int x_dtype, size_t m, size_t k, const abq_quant_s
   if ((st = epi_mode_of(out_kind, &mode))) return st;
   if ((st = check_device())) return st;
   char* ws = static_cast<char*>(workspace);
-  const size_t gbytes = imma_gacc_bytes(m <= 8 ? m : 8, w->n);
-  long long* gacc = reinterpret_cast<long long*>(ws);
-  unsigned* gcnt = reinterpret_cast<unsigned*>(ws + (gbytes / (16 * 8 * 8 + 4)) * 16 * 8 * 8);
-  ws += align256(gbytes);
+  void* ws_imma = ws;
+  ws += align256(imma_ws_bytes(w->n, k));
   uint64_t* planes = reinterpret_cast<uint64_t*>(ws);
   ws += align256(size_t(p) * m * wpr_of(k) * 8);
   double* sa = reinterpret_cast<double*>(ws);
@@ -507,7 +564,30 @@ int abq_linear(const void* x, int x_dtype, size_t m, size_t k, const abq_quant_s
     e.colsum_b = w->colsums;
     e.k = static_cast<long long>(k);
     const QuantParams qp = params_of(*act_spec);
-    st = run_gemv_imma(w->frag, w->q, w->n, k, m, x, x_dtype, &qp, nullptr, 0, e, gacc, gcnt, bad, s);
+    st = run_gemv_imma_fused(w->frag, w->q, w->n, k, m, x, x_dtype, qp, e, ws_imma, bad, s);
+    if (st) return st;
+  } else if (use_tc(w, m, k, !fits_int32_host(p, w->q, k))) {
+    // ReQuant straight to u8 codes (K1), then the tcgen05 GEMM with the fused epilogue
+    uint8_t* codes = reinterpret_cast<uint8_t*>(range + 32);
+    st = run_quantize(x, x_dtype, m, k, params_of(*act_spec), nullptr, nullptr, codes, nullptr, p, sa,
+                      za, ra, bad, range, s);
+    if (st) return st;
+    EpiParams e{};
+    e.mode = mode;
+    e.out = y;
+    e.ldo = static_cast<long long>(w->n);
+    e.s_a = sa;
+    e.sa_stride = act_spec->granularity == ABQ_PER_TENSOR ? 0 : 1;
+    e.z_a = za;
+    e.za_stride = e.sa_stride;
+    e.rowsum_a = ra;
+    e.s_b = w->scales;
+    e.sb_stride = w->per_tensor ? 0 : 1;
+    e.z_b = w->zero_points;
+    e.zb_stride = w->per_tensor ? 0 : 1;
+    e.colsum_b = w->colsums;
+    e.k = static_cast<long long>(k);
+    st = run_gemm_tc(w->tc, w->q, w->n, k, codes, k, m, e, s);
     if (st) return st;
   } else {
     st = run_quantize(x, x_dtype, m, k, params_of(*act_spec), nullptr, nullptr, nullptr, planes, p, sa,

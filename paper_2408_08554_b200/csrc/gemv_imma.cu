@@ -24,14 +24,22 @@
 // need for the 8 k32 chunks of the block; bit (8b + c) of word u is element
 // (row g + 8*(u&1), k = 32c + 16*(u>>1) + 4*tig + b), so chunk c's register
 // is (w << (7 - c)) & 0x80808080.  Same byte count as ABQP; each (tile, block)
-// is q x 512 contiguous bytes: one coalesced 16-byte load per lane per plane.
+// "unit" is q x 512 contiguous bytes.
 //
-// Work split (persistent, stream-K): the (row-tile, k-block) units are split
-// evenly over all CTAs and warps; partial row-tile sums meet in shared memory
-// (64-bit atomics) and, for row-tiles cut between CTAs, in a self-cleaning
-// global accumulator where the last contributing CTA runs the epilogue.
-// The prologue ReQuantizes the fp16 activations (or recombines given planes)
-// into shared memory while the first weight loads are in flight.
+// Pipeline (one persistent CTA of 16 warps per SM):
+//   * work split, stream-K: the (row-tile, k-block) units are divided evenly
+//     over CTAs and warps; a warp's units are one contiguous global range;
+//   * each warp streams its units through a private ring of shared-memory
+//     slots with 1-D TMA bulk copies (cp.async.bulk + mbarrier complete_tx),
+//     issued at kernel start -- before the activations exist;
+//   * the activations are ReQuantized by the small act_quant_kernel launched
+//     just before this kernel with programmatic dependent launch: this kernel
+//     starts immediately, fills its weight ring, prefetches its per-channel
+//     epilogue parameters, and only then waits (griddepcontrol.wait) for the
+//     u8 codes (written by act_quant_kernel already in the B-fragment order);
+//   * partial row-tile sums meet in shared memory (64-bit atomics) and, for the
+//     row-tiles cut between CTAs, in a self-cleaning global accumulator where
+//     the last contributing CTA runs the fused zero-point/dequant epilogue.
 #include "common.cuh"
 #include "quant_dev.cuh"
 
@@ -39,7 +47,7 @@ namespace abq_dev {
 
 constexpr int kRowTile = 16;
 constexpr int kKBlock = 256;
-constexpr int kImmaThreads = 512;
+constexpr int kWeightSmem = 176 * 1024;  // per-CTA TMA ring budget
 
 // ---------------------------------------------------------------------------
 // prepack: ABQP [q][n][wpr] -> fragment-major [rt][kb][q][lane][4]
@@ -75,23 +83,42 @@ __global__ void prepack_frag_kernel(const uint64_t* __restrict__ planes, int q, 
 }
 
 // ---------------------------------------------------------------------------
-// main kernel
+// PTX helpers
 // ---------------------------------------------------------------------------
-struct ImmaParams {
-  const uint32_t* frag;
-  int q, n, k, rowtiles, kblocks;
-  int m;  // total tokens
-  // activations: either float x (+ quant params) or packed planes
-  const void* x;
-  QuantParams qp;
-  const uint64_t* a_planes;
-  int p;
-  int wpr_a;
-  EpiParams e;
-  long long* gacc;  // [tokblocks][rowtiles][16][8] int64, zero on entry and exit
-  unsigned* gcnt;   // [tokblocks][rowtiles], zero on entry and exit
-  unsigned long long* bad;
-};
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init1(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAITG_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAITG_%=;\n\t}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 1-D TMA bulk copy global -> shared, completion counted on an mbarrier
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;"); }
 
 __device__ __forceinline__ void imma_16832(int (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
                                            uint32_t a3, uint32_t b0, uint32_t b1) {
@@ -102,31 +129,226 @@ __device__ __forceinline__ void imma_16832(int (&d)[4], uint32_t a0, uint32_t a1
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-__device__ __forceinline__ uint4 ld_frag(const uint32_t* p) {
-  uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
-  return r;
-}
-
 // CTA that owns unit u under the even split (c*U)/G
 __device__ __forceinline__ int cta_of_unit(long long u, long long U, int G) {
   return static_cast<int>(((u + 1) * G - 1) / U);
 }
 
-// SRC: 0 = activation planes, 1 = fp16 x, 2 = fp32 x, 3 = fp64 x
-template <int QT, int MT, int SRC, int PF>
-__global__ void __launch_bounds__(kImmaThreads, 1) gemv_imma_kernel(ImmaParams P) {
+// u32 index of activation codes (k-group v of 4, token i) in B-fragment order:
+// [kb][c][token i][tig][h]   (kb = v/64, c = (v%64)/8, h = (v%8)/4, tig = v%4)
+__device__ __forceinline__ int act_frag_index(int v, int i, int mt) {
+  const int kb = v >> 6, rem = v & 63;
+  return ((((kb * 8 + (rem >> 3)) * mt + i) * 4 + (rem & 3)) * 2) + ((rem >> 2) & 1);
+}
+
+// ---------------------------------------------------------------------------
+// K1 for the fused decode path: per-token ReQuant of the float activations
+// into u8 codes already in the GEMV's B-fragment order (one CTA per token)
+// plus scale / zero point / code row sum.  Non-finite inputs are reported as
+// atomicMax(~flat_index) into a zero-initialised word (0 = none).
+// ---------------------------------------------------------------------------
+constexpr int kActThreads = 256;
+
+template <typename T>
+__global__ void __launch_bounds__(kActThreads) act_quant_kernel(const T* __restrict__ x, int m, int k, int mt,
+                                                                QuantParams qp, uint32_t* __restrict__ act_frag,
+                                                                double* __restrict__ s_a, long long* __restrict__ z_a,
+                                                                long long* __restrict__ rowsum,
+                                                                unsigned long long* __restrict__ bad_word) {
+  griddep_launch();  // let the dependent GEMV start streaming its weights now
+  __shared__ double s_lo[kActThreads / 32], s_hi[kActThreads / 32];
+  __shared__ long long s_sum[kActThreads / 32];
+  __shared__ double s_step;
+  __shared__ int s_z;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tok = blockIdx.x;
+  const int tb = tok / mt, i = tok % mt;
+  const int kpad = ((k + kKBlock - 1) / kKBlock) * kKBlock;
+  uint32_t* dst = act_frag + static_cast<size_t>(tb) * mt * kpad / 4;
+  const T* row = x + static_cast<size_t>(tok) * k;
+  if constexpr (sizeof(T) == 2) {
+    // fp16 rows, per token, K % 8 == 0, K <= 8 * 4 * kActThreads: the row is read
+    // once with 16-byte loads and kept in registers (min/max in fp32 is exact
+    // for fp16 inputs); codes and sums as in the generic path below.
+    if (!qp.per_tensor && (k & 7) == 0 && k <= 8 * 4 * kActThreads) {
+      const int nvec = k >> 3;
+      uint4 v[4];
+      float flo = CUDART_INF_F, fhi = -CUDART_INF_F;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int idx = tid + r * kActThreads;
+        v[r] = make_uint4(0u, 0u, 0u, 0u);
+        if (idx < nvec) {
+          v[r] = __ldg(reinterpret_cast<const uint4*>(row) + idx);
+          const __half2* h2 = reinterpret_cast<const __half2*>(&v[r]);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 f = __half22float2(h2[e]);
+            if (!isfinite(f.x)) atomicMax(bad_word, ~(static_cast<unsigned long long>(tok) * k + idx * 8 + 2 * e));
+            if (!isfinite(f.y)) atomicMax(bad_word, ~(static_cast<unsigned long long>(tok) * k + idx * 8 + 2 * e + 1));
+            flo = fminf(flo, fminf(f.x, f.y));
+            fhi = fmaxf(fhi, fmaxf(f.x, f.y));
+          }
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        flo = fminf(flo, __shfl_xor_sync(0xffffffffu, flo, o));
+        fhi = fmaxf(fhi, __shfl_xor_sync(0xffffffffu, fhi, o));
+      }
+      if (lane == 0) {
+        s_lo[warp] = flo;
+        s_hi[warp] = fhi;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        double l = s_lo[0], h = s_hi[0];
+        for (int w = 1; w < kActThreads / 32; ++w) {
+          l = fmin(l, s_lo[w]);
+          h = fmax(h, s_hi[w]);
+        }
+        double step;
+        int z;
+        group_params(qp, l, h, &step, &z);
+        s_step = step;
+        s_z = z;
+        s_a[tok] = step;
+        z_a[tok] = z;
+      }
+      __syncthreads();
+      const double step = s_step, zd = static_cast<double>(s_z), inv = 1.0 / step;
+      const double top = static_cast<double>(qp.levels - 1);
+      long long rsum = 0;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int idx = tid + r * kActThreads;
+        if (idx < nvec) {
+          const __half* hv = reinterpret_cast<const __half*>(&v[r]);
+          uint32_t w0 = 0, w1 = 0;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const unsigned c = quant_code_fast(static_cast<double>(__half2float(hv[e])), step, inv, zd, top);
+            rsum += c;
+            if (e < 4) w0 |= c << (8 * e);
+            else w1 |= c << (8 * (e - 4));
+          }
+          dst[act_frag_index(2 * idx, i, mt)] = w0;
+          dst[act_frag_index(2 * idx + 1, i, mt)] = w1;
+        }
+      }
+      // zero codes in the k padding of the last 256-block
+      for (int v4 = k / 4 + tid; v4 < kpad / 4; v4 += kActThreads) dst[act_frag_index(v4, i, mt)] = 0u;
+      rsum = warp_sum(rsum);
+      if (lane == 0) s_sum[warp] = rsum;
+      __syncthreads();
+      if (tid == 0) {
+        long long rr = 0;
+        for (int w = 0; w < kActThreads / 32; ++w) rr += s_sum[w];
+        rowsum[tok] = rr;
+      }
+      return;
+    }
+  }
+  double lo = CUDART_INF, hi = -CUDART_INF;
+  if (qp.per_tensor) {
+    for (int t = 0; t < m; ++t)
+      for (int j = tid; j < k; j += kActThreads) {
+        const double v = load_as_double(x, static_cast<size_t>(t) * k + j);
+        if (!isfinite(v)) atomicMax(bad_word, ~(static_cast<unsigned long long>(t) * k + j));
+        lo = fmin(lo, v);
+        hi = fmax(hi, v);
+      }
+  } else {
+    for (int j = tid; j < k; j += kActThreads) {
+      const double v = load_as_double(row, j);
+      if (!isfinite(v)) atomicMax(bad_word, ~(static_cast<unsigned long long>(tok) * k + j));
+      lo = fmin(lo, v);
+      hi = fmax(hi, v);
+    }
+  }
+  lo = warp_min(lo);
+  hi = warp_max(hi);
+  if (lane == 0) {
+    s_lo[warp] = lo;
+    s_hi[warp] = hi;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int w = 1; w < kActThreads / 32; ++w) {
+      lo = fmin(lo, s_lo[w]);
+      hi = fmax(hi, s_hi[w]);
+    }
+    double step;
+    int z;
+    group_params(qp, lo, hi, &step, &z);
+    s_step = step;
+    s_z = z;
+    s_a[tok] = step;
+    z_a[tok] = z;
+  }
+  __syncthreads();
+  const double step = s_step, zd = static_cast<double>(s_z), inv = 1.0 / step;
+  const double top = static_cast<double>(qp.levels - 1);
+  long long rsum = 0;
+  const int ngroups = kpad / 4;  // zero codes past k
+  for (int v = tid; v < ngroups; v += kActThreads) {
+    uint32_t word = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int j = 4 * v + b;
+      if (j < k) {
+        const unsigned c = quant_code_fast(load_as_double(row, j), step, inv, zd, top);
+        rsum += c;
+        word |= c << (8 * b);
+      }
+    }
+    dst[act_frag_index(v, i, mt)] = word;
+  }
+  rsum = warp_sum(rsum);
+  if (lane == 0) s_sum[warp] = rsum;
+  __syncthreads();
+  if (tid == 0) {
+    long long r = 0;
+    for (int w = 0; w < kActThreads / 32; ++w) r += s_sum[w];
+    rowsum[tok] = r;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// main kernel
+// ---------------------------------------------------------------------------
+struct ImmaParams {
+  const uint32_t* frag;
+  int q, n, k, rowtiles, kblocks;
+  int m;  // total tokens
+  // activations: codes from act_quant_kernel (act_frag + stats) or packed planes
+  const uint32_t* act_frag;
+  const double* s_a;
+  const long long* z_a;
+  const long long* rowsum;
+  const uint64_t* a_planes;
+  int p;
+  int wpr_a;
+  EpiParams e;
+  long long* gacc;  // [rowtiles][16][8] int64, zero on entry and exit (stream-K)
+  unsigned* gcnt;   // [rowtiles], zero on entry and exit
+  unsigned long long* bad_word;  // written by act_quant_kernel (~index, 0 = none)
+  unsigned long long* bad_out;   // published here: first bad index or ~0
+  unsigned long long* trace;     // optional [grid][4] globaltimer stamps (profiling)
+  int slots;                     // TMA ring slots per warp
+};
+
+// FROM_PLANES: activations are given as ABQP planes (API path) instead of
+// codes from act_quant_kernel.
+template <int QT, int MT, bool FROM_PLANES, int NWARP>
+__global__ void __launch_bounds__(NWARP * 32, 1) gemv_imma_kernel(ImmaParams P) {
   constexpr int QMAX = QT > 0 ? QT : 8;
   const int q = QT > 0 ? QT : P.q;
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];
   const int kpad = P.kblocks * kKBlock;
-  uint32_t* act = reinterpret_cast<uint32_t*>(smem);  // MT * kpad bytes
   const int G = gridDim.x;
   const long long U = static_cast<long long>(P.rowtiles) * P.kblocks;
   const bool stream_k = P.gacc != nullptr;
-  // CTA unit range
   long long U0, U1;
   if (stream_k) {
     U0 = blockIdx.x * U / G;
@@ -138,43 +360,61 @@ __global__ void __launch_bounds__(kImmaThreads, 1) gemv_imma_kernel(ImmaParams P
   const int rt_first = static_cast<int>(U0 / P.kblocks);
   const int rt_last = U1 > U0 ? static_cast<int>((U1 - 1) / P.kblocks) : rt_first - 1;
   const int nlrt = rt_last - rt_first + 1;
-  long long* accs = reinterpret_cast<long long*>(smem + static_cast<size_t>(MT) * kpad);  // [nlrt][16][MT]
-  double* s_sa = reinterpret_cast<double*>(accs + static_cast<size_t>(max(nlrt, 0)) * 16 * MT);
+  const int unit_bytes = q * 512;
+
+  // shared memory carve-up
+  unsigned char* wring = smem;                                                        // [16][slots][unit]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(wring + NWARP * P.slots * unit_bytes);  // [16][slots]
+  uint32_t* act = reinterpret_cast<uint32_t*>(bars + NWARP * P.slots);           // MT * kpad bytes
+  long long* accs = reinterpret_cast<long long*>(reinterpret_cast<unsigned char*>(act) + MT * kpad);
+  double* c_sb = reinterpret_cast<double*>(accs + nlrt * 16 * MT);  // per-channel epilogue params
+  long long* c_zb = reinterpret_cast<long long*>(c_sb + nlrt * 16);
+  long long* c_cs = c_zb + nlrt * 16;
+  double* s_sa = reinterpret_cast<double*>(c_cs + nlrt * 16);
   long long* s_za = reinterpret_cast<long long*>(s_sa + MT);
   long long* s_ra = s_za + MT;
-  double* s_lo = reinterpret_cast<double*>(s_ra + MT);  // [16 warps][MT]
-  double* s_hi = s_lo + 16 * MT;
-  long long* s_sum = reinterpret_cast<long long*>(s_hi + 16 * MT);  // [16][MT]
   __shared__ int s_last;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, tig = lane & 3;
   const int tok0 = blockIdx.y * MT;
   const int mb = min(MT, P.m - tok0);
+  unsigned long long* trace = P.trace ? P.trace + 8 * (blockIdx.y * gridDim.x + blockIdx.x) : nullptr;
+  if (trace && tid == 0) trace[0] = clock64();
 
-  // ---- warp unit range and the first weight loads (in flight during the prologue)
-  const long long wu0 = U0 + (U1 - U0) * warp / 16;
-  const long long wu1 = U0 + (U1 - U0) * (warp + 1) / 16;
-  const size_t unit_words = static_cast<size_t>(q) * 128;
-  uint4 ring[PF + 1][QMAX];
-#pragma unroll
-  for (int s = 0; s < PF; ++s) {
-    const long long uu = wu0 + s;
-#pragma unroll
-    for (int t = 0; t < QMAX; ++t)
-      if (t < q && uu < wu1) ring[s][t] = ld_frag(P.frag + uu * unit_words + t * 128 + lane * 4);
+  // ---- 1. this warp's units; start its TMA weight ring immediately
+  const long long wu0 = U0 + (U1 - U0) * warp / NWARP;
+  const long long wu1 = U0 + (U1 - U0) * (warp + 1) / NWARP;
+  unsigned char* my_ring = wring + warp * P.slots * unit_bytes;
+  uint64_t* my_bars = bars + warp * P.slots;
+  const unsigned char* wsrc = reinterpret_cast<const unsigned char*>(P.frag);
+  if (lane == 0) {
+    for (int s = 0; s < P.slots; ++s) mbar_init1(&my_bars[s]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int s = 0; s < P.slots && wu0 + s < wu1; ++s) {
+      mbar_expect_tx(&my_bars[s], unit_bytes);
+      tma_bulk_g2s(my_ring + s * unit_bytes, wsrc + (wu0 + s) * unit_bytes, unit_bytes, &my_bars[s]);
+    }
   }
 
-  // ---- prologue: activations -> u8 codes in smem, fragment layout
-  // u32 index of (kb, c, h, tok i, tig): (((kb*8 + c)*MT + i)*4 + tig)*2 + h
-  for (int idx = tid; idx < MT * kpad / 4; idx += kImmaThreads) act[idx] = 0u;
-  for (int idx = tid; idx < nlrt * 16 * MT; idx += kImmaThreads) accs[idx] = 0;
-  // only CTA (0, y=0) reports non-finite inputs; it owns the status word
-  if (SRC != 0 && P.bad && blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) *P.bad = ~0ull;
-  __syncthreads();
-  const int ngroups = (P.k + 3) / 4;
-  if (SRC == 0) {
-    for (int idx = tid; idx < mb * ngroups; idx += kImmaThreads) {
+  // ---- 2. per-channel epilogue parameters of this CTA's row-tiles, zero accumulators
+  const bool dequant = P.e.mode != EPI_ACC_I32 && P.e.mode != EPI_ACC_I64;
+  for (int idx = tid; dequant && idx < nlrt * 16; idx += NWARP * 32) {
+    const int j = rt_first * kRowTile + idx;
+    if (j < P.n) {
+      c_sb[idx] = P.e.s_b[j * P.e.sb_stride];
+      c_zb[idx] = P.e.z_b[j * P.e.zb_stride];
+      c_cs[idx] = P.e.colsum_b[j];
+    }
+  }
+  for (int idx = tid; idx < nlrt * 16 * MT; idx += NWARP * 32) accs[idx] = 0;
+
+  // ---- 3. activations (u8 codes, B-fragment order) into shared memory
+  if (FROM_PLANES) {
+    for (int idx = tid; idx < MT * kpad / 4; idx += NWARP * 32) act[idx] = 0u;
+    __syncthreads();
+    const int ngroups = (P.k + 3) / 4;
+    for (int idx = tid; idx < mb * ngroups; idx += NWARP * 32) {
       const int i = idx / ngroups, v = idx % ngroups;
       const int tok = tok0 + i;
       uint32_t word = 0;
@@ -183,104 +423,28 @@ __global__ void __launch_bounds__(kImmaThreads, 1) gemv_imma_kernel(ImmaParams P
         const uint32_t nib = static_cast<uint32_t>(pw >> ((v & 15) * 4)) & 0xFu;
         word |= ((nib * 0x00204081u) & 0x01010101u) << s;
       }
-      const int kb = v >> 6, rem = v & 63;
-      act[((((kb * 8 + (rem >> 3)) * MT + i) * 4 + (rem & 3)) * 2) + ((rem >> 2) & 1)] = word;
+      act[act_frag_index(v, i, MT)] = word;
     }
   } else {
-    // ReQuant (quantizer.hpp:146-213), per-token (or per-tensor) asymmetric/symmetric/balanced
-    double lo[MT], hi[MT];
-#pragma unroll
-    for (int i = 0; i < MT; ++i) {
-      lo[i] = CUDART_INF;
-      hi[i] = -CUDART_INF;
+    griddep_wait();  // act_quant_kernel done and its writes visible
+    const uint4* src = reinterpret_cast<const uint4*>(P.act_frag + static_cast<size_t>(blockIdx.y) * MT * kpad / 4);
+    uint4* dst = reinterpret_cast<uint4*>(act);
+    for (int idx = tid; idx < MT * kpad / 16; idx += NWARP * 32) dst[idx] = __ldcg(src + idx);
+    if (tid < mb) {
+      s_sa[tid] = P.s_a[tok0 + tid];
+      s_za[tid] = P.z_a[tok0 + tid];
+      s_ra[tid] = P.rowsum[tok0 + tid];
     }
-    auto scan = [&](int tok, double& l, double& h) {
-      for (int j = tid; j < P.k; j += kImmaThreads) {
-        double v;
-        if (SRC == 1) v = load_as_double(static_cast<const __half*>(P.x), static_cast<size_t>(tok) * P.k + j);
-        else if (SRC == 2) v = load_as_double(static_cast<const float*>(P.x), static_cast<size_t>(tok) * P.k + j);
-        else v = load_as_double(static_cast<const double*>(P.x), static_cast<size_t>(tok) * P.k + j);
-        if (!isfinite(v) && blockIdx.x == 0 && blockIdx.y == 0 && P.bad)
-          atomicMin(P.bad, static_cast<unsigned long long>(tok) * P.k + j);
-        l = fmin(l, v);
-        h = fmax(h, v);
-      }
-    };
-    if (P.qp.per_tensor) {  // one range over every token (quantizer.hpp:116-129)
-      for (int tok = 0; tok < P.m; ++tok) scan(tok, lo[0], hi[0]);
-    } else {
-#pragma unroll
-      for (int i = 0; i < MT; ++i)
-        if (i < mb) scan(tok0 + i, lo[i], hi[i]);
-    }
-#pragma unroll
-    for (int i = 0; i < MT; ++i) {
-      const double l = warp_min(lo[i]), h = warp_max(hi[i]);
-      if (lane == 0) {
-        s_lo[warp * MT + i] = l;
-        s_hi[warp * MT + i] = h;
-      }
-    }
-    __syncthreads();
-    if (tid < MT) {
-      const int i = P.qp.per_tensor ? 0 : tid;
-      double l = CUDART_INF, h = -CUDART_INF;
-      for (int w = 0; w < 16; ++w) {
-        l = fmin(l, s_lo[w * MT + i]);
-        h = fmax(h, s_hi[w * MT + i]);
-      }
-      double step;
-      int z;
-      group_params(P.qp, l, h, &step, &z);
-      s_sa[tid] = step;
-      s_za[tid] = z;
-    }
-    __syncthreads();
-    long long rsum[MT];
-#pragma unroll
-    for (int i = 0; i < MT; ++i) rsum[i] = 0;
-    const double top = static_cast<double>(P.qp.levels - 1);
-    for (int idx = tid; idx < mb * ngroups; idx += kImmaThreads) {
-      const int i = idx / ngroups, v = idx % ngroups;
-      const int tok = tok0 + i;
-      const double step = s_sa[i], zd = static_cast<double>(s_za[i]);
-      const double inv = 1.0 / step;
-      uint32_t word = 0;
-      unsigned sum = 0;
-#pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const int j = 4 * v + b;
-        if (j < P.k) {
-          double x;
-          if (SRC == 1) x = load_as_double(static_cast<const __half*>(P.x), static_cast<size_t>(tok) * P.k + j);
-          else if (SRC == 2) x = load_as_double(static_cast<const float*>(P.x), static_cast<size_t>(tok) * P.k + j);
-          else x = load_as_double(static_cast<const double*>(P.x), static_cast<size_t>(tok) * P.k + j);
-          const unsigned c = quant_code_fast(x, step, inv, zd, top);
-          sum += c;
-          word |= c << (8 * b);
-        }
-      }
-#pragma unroll
-      for (int ii = 0; ii < MT; ++ii)
-        if (ii == i) rsum[ii] += sum;
-      const int kb = v >> 6, rem = v & 63;
-      act[((((kb * 8 + (rem >> 3)) * MT + i) * 4 + (rem & 3)) * 2) + ((rem >> 2) & 1)] = word;
-    }
-#pragma unroll
-    for (int i = 0; i < MT; ++i) {
-      const long long r = warp_sum(rsum[i]);
-      if (lane == 0) s_sum[warp * MT + i] = r;
-    }
-    __syncthreads();
-    if (tid < MT) {
-      long long r = 0;
-      for (int w = 0; w < 16; ++w) r += s_sum[w * MT + tid];
-      s_ra[tid] = r;
+    if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0 && P.bad_out) {
+      const unsigned long long w = *P.bad_word;
+      *P.bad_out = w ? ~w : ~0ull;
+      *P.bad_word = 0ull;
     }
   }
   __syncthreads();
+  if (trace && tid == 0) trace[1] = clock64();
 
-  // ---- main loop over this warp's (row-tile, k-block) units
+  // ---- 4. main loop over this warp's units (one body, TMA ring slots)
   int acc[QMAX][4];
 #pragma unroll
   for (int t = 0; t < QMAX; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0;
@@ -306,97 +470,148 @@ __global__ void __launch_bounds__(kImmaThreads, 1) gemv_imma_kernel(ImmaParams P
     for (int t = 0; t < QMAX; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0;
   };
 
-  for (long long u = wu0; u < wu1; u += PF + 1) {
+  int slot = 0;
+  uint32_t phase = 0;
+  for (long long uu = wu0; uu < wu1; ++uu) {
+    const int rt = static_cast<int>(uu / P.kblocks);
+    const int kb = static_cast<int>(uu - static_cast<long long>(rt) * P.kblocks);
+    if (rt != cur_rt) {
+      flush(cur_rt);
+      cur_rt = rt;
+    }
+    mbar_wait_parity(&my_bars[slot], phase);
+    const uint4* wv = reinterpret_cast<const uint4*>(my_ring + slot * unit_bytes) + lane;
+    uint4 w[QMAX];
 #pragma unroll
-    for (int s = 0; s <= PF; ++s) {
-      const long long uu = u + s;
-      if (uu < wu1) {
-        // issue the load PF units ahead into the slot freed last iteration
-        const long long un = uu + PF;
-        const int slot_n = (s + PF) % (PF + 1);
-        if (un < wu1) {
+    for (int t = 0; t < QMAX; ++t)
+      if (t < q) w[t] = wv[t * 32];
+    const uint2* ab = act2 + static_cast<size_t>(kb) * 8 * MT * 4;
 #pragma unroll
-          for (int t = 0; t < QMAX; ++t)
-            if (t < q) ring[slot_n][t] = ld_frag(P.frag + un * unit_words + t * 128 + lane * 4);
-        }
-        const int rt = static_cast<int>(uu / P.kblocks);
-        const int kb = static_cast<int>(uu % P.kblocks);
-        if (rt != cur_rt) {
-          flush(cur_rt);
-          cur_rt = rt;
-        }
-        const uint2* ab = act2 + static_cast<size_t>(kb) * 8 * MT * 4;
+    for (int c = 0; c < 8; ++c) {
+      uint2 b = make_uint2(0u, 0u);
+      if (g < MT) b = ab[(c * MT + g) * 4 + tig];
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          uint2 b = make_uint2(0u, 0u);
-          if (g < MT) b = ab[(c * MT + g) * 4 + tig];
-#pragma unroll
-          for (int t = 0; t < QMAX; ++t) {
-            if (t < q) {
-              const uint4 w = ring[s][t];
-              const uint32_t a0 = (w.x << (7 - c)) & 0x80808080u;
-              const uint32_t a1 = (w.y << (7 - c)) & 0x80808080u;
-              const uint32_t a2 = (w.z << (7 - c)) & 0x80808080u;
-              const uint32_t a3 = (w.w << (7 - c)) & 0x80808080u;
-              imma_16832(acc[t], a0, a1, a2, a3, b.x, b.y);
-            }
-          }
+      for (int t = 0; t < QMAX; ++t) {
+        if (t < q) {
+          const uint32_t a0 = (w[t].x << (7 - c)) & 0x80808080u;
+          const uint32_t a1 = (w[t].y << (7 - c)) & 0x80808080u;
+          const uint32_t a2 = (w[t].z << (7 - c)) & 0x80808080u;
+          const uint32_t a3 = (w[t].w << (7 - c)) & 0x80808080u;
+          imma_16832(acc[t], a0, a1, a2, a3, b.x, b.y);
         }
       }
+    }
+    // refill this slot with the unit `slots` ahead (the whole warp has read it)
+    __syncwarp();
+    const long long un = uu + P.slots;
+    if (lane == 0 && un < wu1) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(&my_bars[slot], unit_bytes);
+      tma_bulk_g2s(my_ring + slot * unit_bytes, wsrc + un * unit_bytes, unit_bytes, &my_bars[slot]);
+    }
+    if (++slot == P.slots) {
+      slot = 0;
+      phase ^= 1u;
     }
   }
   if (cur_rt >= 0) flush(cur_rt);
   __syncthreads();
+  if (trace && tid == 0) trace[2] = clock64();
 
-  // ---- epilogue per local row-tile
-  const int base_blk = blockIdx.y * P.rowtiles;
-  for (int lrt = 0; lrt < nlrt; ++lrt) {
-    const int rt = rt_first + lrt;
+  // ---- 5. epilogue.  Row-tiles owned by this CTA alone are stored straight
+  // from shared memory; only the first / last row-tile can be cut between CTAs
+  // (stream-K): their partial sums meet in the global accumulator and the last
+  // arriving CTA (counter) stores them and re-zeroes the slot.
+  // a row-tile is owned by this CTA alone iff all its units lie in [U0, U1)
+  auto owned = [&](int rt) {
     const long long ufirst = static_cast<long long>(rt) * P.kblocks;
-    const long long ulast = ufirst + P.kblocks - 1;
-    const int contributors = stream_k ? cta_of_unit(ulast, U, G) - cta_of_unit(ufirst, U, G) + 1 : 1;
-    if (contributors == 1) {
-      for (int idx = tid; idx < 16 * mb; idx += kImmaThreads) {
-        const int row = idx / mb, i = idx % mb;
-        const int j = rt * kRowTile + row;
-        if (j < P.n) {
-          const long long a = accs[(lrt * 16 + row) * MT + i];
-          if (SRC == 0) epi_store(P.e, tok0 + i, j, a);
-          else epi_store_v(P.e, tok0 + i, j, a, s_sa[P.qp.per_tensor ? 0 : i],
-                           s_za[P.qp.per_tensor ? 0 : i], s_ra[i]);
-        }
-      }
-    } else {
-      long long* gslot = P.gacc + (static_cast<size_t>(base_blk) + rt) * 16 * 8;
-      for (int idx = tid; idx < 16 * mb; idx += kImmaThreads) {
-        const int row = idx / mb, i = idx % mb;
-        atomicAdd(reinterpret_cast<unsigned long long*>(&gslot[row * 8 + i]),
-                  static_cast<unsigned long long>(accs[(lrt * 16 + row) * MT + i]));
-      }
-      __threadfence();
-      __syncthreads();
-      if (tid == 0) {
-        const unsigned old = atomicAdd(&P.gcnt[base_blk + rt], 1u);
-        s_last = old == static_cast<unsigned>(contributors - 1);
-      }
-      __syncthreads();
-      if (s_last) {
-        __threadfence();
-        for (int idx = tid; idx < 16 * mb; idx += kImmaThreads) {
-          const int row = idx / mb, i = idx % mb;
-          const long long a = static_cast<long long>(
-              atomicExch(reinterpret_cast<unsigned long long*>(&gslot[row * 8 + i]), 0ull));
-          const int j = rt * kRowTile + row;
-          if (j < P.n) {
-            if (SRC == 0) epi_store(P.e, tok0 + i, j, a);
-            else epi_store_v(P.e, tok0 + i, j, a, s_sa[P.qp.per_tensor ? 0 : i],
-                             s_za[P.qp.per_tensor ? 0 : i], s_ra[i]);
-          }
-        }
-        if (tid == 0) P.gcnt[base_blk + rt] = 0u;
-      }
-      __syncthreads();
+    return ufirst >= U0 && ufirst + P.kblocks <= U1;
+  };
+  auto contributors_of = [&](int rt) {  // thread 0 only: 64-bit divisions
+    if (!stream_k) return 1;
+    const long long ufirst = static_cast<long long>(rt) * P.kblocks;
+    return cta_of_unit(ufirst + P.kblocks - 1, U, G) - cta_of_unit(ufirst, U, G) + 1;
+  };
+  auto store = [&](int lrt, int row, int i, long long a) {
+    const int j = (rt_first + lrt) * kRowTile + row;
+    if (j >= P.n) return;
+    const int c = lrt * 16 + row;
+    if (P.e.mode == EPI_ACC_I32 || P.e.mode == EPI_ACC_I64) {
+      epi_store_v(P.e, tok0 + i, j, a, 0.0, 0, 0);
+      return;
     }
+    // fused zero-point correction + dequant from the prefetched parameters
+    double sa;
+    long long za, ra;
+    if (FROM_PLANES) {
+      sa = P.e.s_a[(tok0 + i) * P.e.sa_stride];
+      za = P.e.z_a[(tok0 + i) * P.e.za_stride];
+      ra = P.e.rowsum_a[tok0 + i];
+    } else {
+      sa = s_sa[i];
+      za = s_za[i];
+      ra = s_ra[i];
+    }
+    const long long zb = c_zb[c];
+    const long long corr = a - za * c_cs[c] - zb * ra + P.e.k * za * zb;
+    const long long o = static_cast<long long>(tok0 + i) * P.e.ldo + j;
+    if (P.e.mode == EPI_CORR_I64) {
+      static_cast<int64_t*>(P.e.out)[o] = corr;
+      return;
+    }
+    const double y = __dmul_rn(__dmul_rn(sa, c_sb[c]), static_cast<double>(corr));
+    if (P.e.mode == EPI_F64)
+      static_cast<double*>(P.e.out)[o] = y;
+    else if (P.e.mode == EPI_F16)
+      static_cast<__half*>(P.e.out)[o] = __double2half(y);
+    else
+      static_cast<float*>(P.e.out)[o] = __double2float_rn(y);
+  };
+  int nsplit = 0;
+  if (trace && tid == 0) trace[4] = nlrt;
+  for (int idx = tid; idx < nlrt * 16 * mb; idx += NWARP * 32) {
+    const int lrt = idx / (16 * mb), rem = idx % (16 * mb), row = rem / mb, i = rem % mb;
+    if (!stream_k || owned(rt_first + lrt)) store(lrt, row, i, accs[(lrt * 16 + row) * MT + i]);
+  }
+  if (trace && tid == 0) trace[5] = clock64();
+  for (int lrt = 0; lrt < nlrt; ++lrt) {
+    if (!stream_k || owned(rt_first + lrt)) continue;
+    ++nsplit;
+    long long* gslot = P.gacc + static_cast<size_t>(rt_first + lrt) * 16 * 8;
+    for (int idx = tid; idx < 16 * mb; idx += NWARP * 32)
+      atomicAdd(reinterpret_cast<unsigned long long*>(&gslot[(idx / mb) * 8 + idx % mb]),
+                static_cast<unsigned long long>(accs[(lrt * 16 + idx / mb) * MT + idx % mb]));
+  }
+  if (trace && tid == 0) trace[3] = clock64();
+  if (nsplit == 0) return;  // uniform across the CTA
+  __syncthreads();
+  // release: one gpu-scope fence by thread 0 after the CTA barrier orders every
+  // thread's partial-sum atomics before the arrival counter (fence cumulativity)
+  if (tid == 0) {
+    __threadfence();
+    int mask = 0;
+    for (int e = 0; e < 2; ++e) {  // only the first / last local row-tile can be shared
+      const int lrt = e == 0 ? 0 : nlrt - 1;
+      if (e == 1 && lrt == 0) break;
+      const int rt = rt_first + lrt;
+      const int c = contributors_of(rt);
+      if (c > 1 && atomicAdd(&P.gcnt[rt], 1u) == static_cast<unsigned>(c - 1)) mask |= 1 << e;
+    }
+    if (mask) __threadfence();  // acquire side for the slot reads below
+    s_last = mask;
+  }
+  __syncthreads();
+  const int mask = s_last;
+  for (int e = 0; e < 2; ++e) {
+    if (!(mask & (1 << e))) continue;
+    const int lrt = e == 0 ? 0 : nlrt - 1;
+    long long* gslot = P.gacc + static_cast<size_t>(rt_first + lrt) * 16 * 8;
+    for (int idx = tid; idx < 16 * mb; idx += NWARP * 32) {
+      const long long a = static_cast<long long>(
+          atomicExch(reinterpret_cast<unsigned long long*>(&gslot[(idx / mb) * 8 + idx % mb]), 0ull));
+      store(lrt, idx / mb, idx % mb, a);
+    }
+    if (tid == 0) P.gcnt[rt_first + lrt] = 0u;
   }
 }
 
@@ -408,9 +623,11 @@ size_t frag_words(unsigned q, size_t n, size_t k) {
   return rowtiles * kblocks * q * 128;
 }
 
-size_t imma_gacc_bytes(size_t m, size_t n) {
-  const size_t rowtiles = (n + kRowTile - 1) / kRowTile, tokblocks = (m + 7) / 8;
-  return tokblocks * rowtiles * (16 * 8 * sizeof(long long) + sizeof(unsigned));
+// stream-K accumulators + counters + act codes (8 tokens) + stats + status word
+size_t imma_ws_bytes(size_t n, size_t k) {
+  const size_t rowtiles = (n + kRowTile - 1) / kRowTile;
+  const size_t kpad = ((k + kKBlock - 1) / kKBlock) * kKBlock;
+  return rowtiles * 16 * 8 * 8 + ((rowtiles * 4 + 255) & ~size_t(255)) + 8 * kpad + 8 * 24 + 256;
 }
 
 int run_prepack_frag(const uint64_t* planes, unsigned q, size_t n, size_t k, uint32_t* frag,
@@ -428,66 +645,104 @@ int run_prepack_frag(const uint64_t* planes, unsigned q, size_t n, size_t k, uin
   return ABQ_OK;
 }
 
-template <int QT, int MT, int SRC>
-static int launch_imma(ImmaParams P, int grid_x, int grid_y, cudaStream_t st) {
-  constexpr int QQ = QT > 0 ? QT : 8;
-  constexpr int PF = QQ <= 2 ? 3 : (QQ <= 4 ? 2 : 1);
-  auto kern = gemv_imma_kernel<QT, MT, SRC, PF>;
+unsigned long long*& trace_buffer() {
+  static unsigned long long* buf = nullptr;
+  return buf;
+}
+
+static size_t imma_smem_bytes(const ImmaParams& P, int mt, int grid_x, int nwarp) {
   const long long U = static_cast<long long>(P.rowtiles) * P.kblocks;
   const long long per_cta_units = (U + grid_x - 1) / grid_x + P.kblocks;
   const int nlrt_max = static_cast<int>(per_cta_units / P.kblocks + 2);
-  const size_t smem = static_cast<size_t>(MT) * P.kblocks * kKBlock +
-                      static_cast<size_t>(nlrt_max) * 16 * MT * 8 + MT * (8 + 8 + 8) +
-                      2 * 16 * MT * 8 + 16 * MT * 8;
+  return static_cast<size_t>(nwarp) * P.slots * P.q * 512 + nwarp * P.slots * 8 +
+         static_cast<size_t>(mt) * P.kblocks * kKBlock + static_cast<size_t>(nlrt_max) * 16 * mt * 8 +
+         static_cast<size_t>(nlrt_max) * 16 * 24 + mt * 24 + 128;
+}
+
+// warps per CTA: 32 (1024 threads, <= 64 registers) for q <= 4 where the
+// unit body is ALU / issue bound and needs the extra latency hiding; 16 for
+// wider planes (more weight registers per unit)
+static int imma_warps(int q) { return q >= 1 && q <= 4 ? 32 : 16; }
+
+template <int QT, int MT, bool FROM_PLANES, int NWARP>
+static int launch_imma_w(ImmaParams P, int grid_x, int grid_y, bool pdl, cudaStream_t st) {
+  auto kern = gemv_imma_kernel<QT, MT, FROM_PLANES, NWARP>;
+  const size_t smem = imma_smem_bytes(P, MT, grid_x, NWARP);
   if (smem > 227 * 1024) return fail(ABQ_ERR_VALUE, "gemv_imma: shared memory plan too large (%zu B)", smem);
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
   if (err != cudaSuccess) return fail(ABQ_ERR_CUDA, "gemv_imma: smem attribute: %s", cudaGetErrorString(err));
-  kern<<<dim3(grid_x, grid_y), kImmaThreads, smem, st>>>(P);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid_x, grid_y);
+  cfg.blockDim = dim3(NWARP * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  err = cudaLaunchKernelEx(&cfg, kern, P);
+  if (err != cudaSuccess) return fail(ABQ_ERR_CUDA, "gemv_imma: launch: %s", cudaGetErrorString(err));
   ABQ_LAUNCHED();
   return ABQ_OK;
 }
 
-template <int MT, int SRC>
-static int launch_q(ImmaParams P, int gx, int gy, cudaStream_t st) {
+template <int QT, int MT, bool FROM_PLANES>
+static int launch_imma(ImmaParams P, int grid_x, int grid_y, bool pdl, cudaStream_t st) {
+  if (QT >= 1 && QT <= 4) return launch_imma_w<QT, MT, FROM_PLANES, 32>(P, grid_x, grid_y, pdl, st);
+  return launch_imma_w<QT, MT, FROM_PLANES, 16>(P, grid_x, grid_y, pdl, st);
+}
+
+template <int MT, bool FP>
+static int launch_q(ImmaParams P, int gx, int gy, bool pdl, cudaStream_t st) {
   switch (P.q) {
-    case 1: return launch_imma<1, MT, SRC>(P, gx, gy, st);
-    case 2: return launch_imma<2, MT, SRC>(P, gx, gy, st);
-    case 3: return launch_imma<3, MT, SRC>(P, gx, gy, st);
-    case 4: return launch_imma<4, MT, SRC>(P, gx, gy, st);
-    case 8: return launch_imma<8, MT, SRC>(P, gx, gy, st);
-    default: return launch_imma<0, MT, SRC>(P, gx, gy, st);
+    case 1: return launch_imma<1, MT, FP>(P, gx, gy, pdl, st);
+    case 2: return launch_imma<2, MT, FP>(P, gx, gy, pdl, st);
+    case 3: return launch_imma<3, MT, FP>(P, gx, gy, pdl, st);
+    case 4: return launch_imma<4, MT, FP>(P, gx, gy, pdl, st);
+    case 8: return launch_imma<8, MT, FP>(P, gx, gy, pdl, st);
+    default: return launch_imma<0, MT, FP>(P, gx, gy, pdl, st);
   }
 }
 
-template <int SRC>
-static int launch_mt(ImmaParams P, int mt, int gx, int gy, cudaStream_t st) {
+template <bool FP>
+static int launch_mt(ImmaParams P, int mt, int gx, int gy, bool pdl, cudaStream_t st) {
   switch (mt) {
-    case 1: return launch_q<1, SRC>(P, gx, gy, st);
-    case 2: return launch_q<2, SRC>(P, gx, gy, st);
-    case 4: return launch_q<4, SRC>(P, gx, gy, st);
-    default: return launch_q<8, SRC>(P, gx, gy, st);
+    case 1: return launch_q<1, FP>(P, gx, gy, pdl, st);
+    case 2: return launch_q<2, FP>(P, gx, gy, pdl, st);
+    case 4: return launch_q<4, FP>(P, gx, gy, pdl, st);
+    default: return launch_q<8, FP>(P, gx, gy, pdl, st);
   }
 }
 
-static int pick_imma_mt(int m, int kblocks) {
-  int mt = m >= 5 ? 8 : (m >= 3 ? 4 : m);
-  while (mt > 1 && static_cast<size_t>(mt) * kblocks * kKBlock > 160 * 1024) mt >>= 1;
-  return mt;
-}
+static int pick_imma_mt(int m) { return m >= 5 ? 8 : (m >= 3 ? 4 : m); }
 
-// K supported by the activation smem plan (mt=1): up to 160 KB of codes
+// activations + stats for 8 tokens must fit next to a minimal weight ring
 bool imma_supported(size_t m, size_t k) {
   (void)m;
-  return k > 0 && ((k + kKBlock - 1) / kKBlock) * kKBlock <= 160 * 1024;
+  const size_t kpad = ((k + kKBlock - 1) / kKBlock) * kKBlock;
+  return k > 0 && k <= 65536 && 8 * kpad <= 64 * 1024;
 }
 
-// x_dtype < 0: activations come from planes (a_planes/p), else from float x.
-int run_gemv_imma(const uint32_t* frag, unsigned q, size_t n, size_t k, size_t m, const void* x,
-                  int x_dtype, const QuantParams* qp, const uint64_t* a_planes, unsigned p,
-                  const EpiParams& e, long long* gacc, unsigned* gcnt, unsigned long long* bad,
-                  cudaStream_t st) {
-  if (m == 0 || n == 0) return ABQ_OK;
+static void plan_grid(ImmaParams& P, int mt, bool stream_k, int* gx) {
+  const int nwarp = imma_warps(P.q);
+  const long long U = static_cast<long long>(P.rowtiles) * P.kblocks;
+  if (stream_k)  // stream-K over units; keep >= one unit per warp per CTA
+    *gx = static_cast<int>(std::min<long long>(num_sms(), std::max<long long>(1, U / nwarp)));
+  else
+    *gx = std::min(num_sms(), P.rowtiles);
+  // TMA ring depth: as many unit slots per warp as the smem budget allows (<= 8)
+  const int unit = P.q * 512;
+  const size_t other = static_cast<size_t>(mt) * P.kblocks * kKBlock + 48 * 1024;
+  int slots = static_cast<int>((kWeightSmem + 48 * 1024 - other) / (nwarp * unit));
+  if (slots > 8) slots = 8;
+  if (slots < 2) slots = 2;
+  P.slots = slots;
+}
+
+static ImmaParams base_params(const uint32_t* frag, unsigned q, size_t n, size_t k, size_t m,
+                              const EpiParams& e) {
   ImmaParams P{};
   P.frag = frag;
   P.q = static_cast<int>(q);
@@ -496,30 +751,78 @@ int run_gemv_imma(const uint32_t* frag, unsigned q, size_t n, size_t k, size_t m
   P.rowtiles = static_cast<int>((n + kRowTile - 1) / kRowTile);
   P.kblocks = static_cast<int>((k + kKBlock - 1) / kKBlock);
   P.m = static_cast<int>(m);
-  P.x = x;
-  if (qp) P.qp = *qp;
+  P.e = e;
+  P.trace = trace_buffer();
+  return P;
+}
+
+// API path: activations given as planes (+ s_a/z_a/rowsum in e); row-tile split.
+int run_gemv_imma_planes(const uint32_t* frag, unsigned q, size_t n, size_t k, size_t m,
+                         const uint64_t* a_planes, unsigned p, const EpiParams& e, cudaStream_t st) {
+  if (m == 0 || n == 0) return ABQ_OK;
+  ImmaParams P = base_params(frag, q, n, k, m, e);
   P.a_planes = a_planes;
   P.p = static_cast<int>(p);
   P.wpr_a = static_cast<int>(wpr_of(k));
-  P.e = e;
-  P.gacc = reinterpret_cast<long long*>(gacc);
-  P.gcnt = gcnt;
-  P.bad = bad;
-  const int mt = pick_imma_mt(static_cast<int>(m), P.kblocks);
-  const int gy = static_cast<int>((m + mt - 1) / mt);
-  const long long U = static_cast<long long>(P.rowtiles) * P.kblocks;
+  const int mt = pick_imma_mt(static_cast<int>(m));
   int gx;
-  if (gacc) {
-    // stream-K over units; keep >= 16 units (one per warp) per CTA
-    gx = static_cast<int>(std::min<long long>(num_sms(), std::max<long long>(1, U / 16)));
-  } else {
-    gx = std::min(num_sms(), P.rowtiles);
+  plan_grid(P, mt, false, &gx);
+  const int gy = static_cast<int>((m + mt - 1) / mt);
+  return launch_mt<true>(P, mt, gx, gy, false, st);
+}
+
+// Serving path: act_quant_kernel (ReQuant into B-fragment codes) followed by the
+// stream-K GEMV with programmatic dependent launch.  `ws` must be
+// imma_ws_bytes(n, k) of zero-filled device memory (left zeroed).
+int run_gemv_imma_fused(const uint32_t* frag, unsigned q, size_t n, size_t k, size_t m, const void* x,
+                        int x_dtype, const QuantParams& qp, const EpiParams& e, void* ws,
+                        unsigned long long* bad_out, cudaStream_t st) {
+  if (m == 0 || n == 0) return ABQ_OK;
+  ImmaParams P = base_params(frag, q, n, k, m, e);
+  const int mt = pick_imma_mt(static_cast<int>(m));
+  const size_t rowtiles = P.rowtiles;
+  const size_t kpad = static_cast<size_t>(P.kblocks) * kKBlock;
+  char* w = static_cast<char*>(ws);
+  P.gacc = reinterpret_cast<long long*>(w);
+  w += rowtiles * 16 * 8 * 8;
+  P.gcnt = reinterpret_cast<unsigned*>(w);
+  w += (rowtiles * 4 + 255) & ~size_t(255);
+  uint32_t* act_frag = reinterpret_cast<uint32_t*>(w);
+  w += 8 * kpad;
+  double* s_a = reinterpret_cast<double*>(w);
+  long long* z_a = reinterpret_cast<long long*>(w + 64);
+  long long* rowsum = reinterpret_cast<long long*>(w + 128);
+  unsigned long long* bad_word = reinterpret_cast<unsigned long long*>(w + 192);
+  P.act_frag = act_frag;
+  P.s_a = s_a;
+  P.z_a = z_a;
+  P.rowsum = rowsum;
+  P.bad_word = bad_word;
+  P.bad_out = bad_out;
+  // K1: one CTA per token
+  switch (x_dtype) {
+    case ABQ_F16:
+      act_quant_kernel<__half><<<static_cast<unsigned>(m), kActThreads, 0, st>>>(
+          static_cast<const __half*>(x), static_cast<int>(m), static_cast<int>(k), mt, qp, act_frag, s_a, z_a,
+          rowsum, bad_word);
+      break;
+    case ABQ_F32:
+      act_quant_kernel<float><<<static_cast<unsigned>(m), kActThreads, 0, st>>>(
+          static_cast<const float*>(x), static_cast<int>(m), static_cast<int>(k), mt, qp, act_frag, s_a, z_a,
+          rowsum, bad_word);
+      break;
+    default:
+      act_quant_kernel<double><<<static_cast<unsigned>(m), kActThreads, 0, st>>>(
+          static_cast<const double*>(x), static_cast<int>(m), static_cast<int>(k), mt, qp, act_frag, s_a, z_a,
+          rowsum, bad_word);
+      break;
   }
-  if (gacc && mt != 8 && gy > 1) return fail(ABQ_ERR_VALUE, "gemv_imma: token blocking needs mt=8");
-  if (x_dtype < 0) return launch_mt<0>(P, mt, gx, gy, st);
-  if (x_dtype == ABQ_F16) return launch_mt<1>(P, mt, gx, gy, st);
-  if (x_dtype == ABQ_F32) return launch_mt<2>(P, mt, gx, gy, st);
-  return launch_mt<3>(P, mt, gx, gy, st);
+  ABQ_LAUNCHED();
+  int gx;
+  plan_grid(P, mt, true, &gx);
+  const int gy = static_cast<int>((m + mt - 1) / mt);
+  if (gy != 1) return fail(ABQ_ERR_VALUE, "gemv_imma: fused path supports m <= 8");
+  return launch_mt<false>(P, mt, gx, gy, true, st);
 }
 
 }  // namespace abq_dev

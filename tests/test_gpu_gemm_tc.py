@@ -1,0 +1,69 @@
+"""Prefill GEMM on tcgen05 (M >= 9 tokens): plane recombination into u8 codes
+in shared memory + UMMA kind::i8 into TMEM.  Bit-exact against the oracle on
+ragged shapes (N not a multiple of the 128-channel tile, K multiple of 16 but
+not of the 128-wide stage, M not a multiple of the token tile), every weight
+plane count, through the fused linear and the raw gemm_arbitrary API."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def test_tc_linear_ragged(abq, orc):
+    rng = np.random.default_rng(21)
+    for trial in range(30):
+        m = int(rng.integers(9, 300))
+        n = int(rng.integers(1, 700))
+        k = 16 * int(rng.integers(1, 100))
+        wbits, abits = (int(v) for v in rng.integers(1, 9, 2))
+        x = (rng.standard_normal((m, k)) * rng.uniform(0.2, 4)).astype(np.float16)
+        wc = rng.integers(0, 1 << wbits, (n, k), dtype=np.uint8)
+        sb = rng.uniform(1e-3, 1e-2, n)
+        zb = rng.integers(0, 1 << wbits, n).astype(np.int32)
+        w = abq.PackedWeights.from_planes(abq.bitpack(wc, wbits), sb, zb)
+        lin = abq.Linear(w, abq.QuantSpec(bits=abits, granularity=abq.api.PER_TOKEN), max_m=m)
+        y = lin(torch.from_numpy(x).cuda(), out_dtype=torch.float64).cpu().numpy()
+        ac, sa, za = orc.quantize(x.astype(np.float64), abits, 0, 2)
+        want = orc.quantized_linear(ac, abits, sa, za, wc, wbits, sb, zb)
+        assert np.array_equal(y, want), (trial, m, n, k, wbits, abits)
+
+
+@pytest.mark.parametrize("m,n,k,p,q", [(16, 11008, 4096, 4, 4), (128, 11008, 4096, 4, 4),
+                                       (128, 4096, 4096, 8, 2), (128, 11008, 4096, 8, 8),
+                                       (200, 1024, 11008, 6, 6), (2048, 512, 1024, 4, 4)])
+def test_tc_gemm_llama_shapes(abq, orc, m, n, k, p, q):
+    rng = np.random.default_rng(m * 7 + n)
+    a = rng.integers(0, 1 << p, (m, k), dtype=np.uint8)
+    b = rng.integers(0, 1 << q, (n, k), dtype=np.uint8)
+    got = abq.gemm_arbitrary(abq.bitpack(a, p), abq.bitpack(b, q), abq.default_tile(p, q)).cpu().numpy()
+    want = a.astype(np.int64) @ b.astype(np.int64).T  # exact integer product
+    assert np.array_equal(got, want)
+
+
+def test_tc_gemm_random_raw(abq, orc):
+    rng = np.random.default_rng(22)
+    for trial in range(40):
+        m = int(rng.integers(16, 260))
+        n = int(rng.integers(1, 400))
+        k = 16 * int(rng.integers(1, 60))
+        p, q = (int(v) for v in rng.integers(1, 9, 2))
+        a = rng.integers(0, 1 << p, (m, k), dtype=np.uint8)
+        b = rng.integers(0, 1 << q, (n, k), dtype=np.uint8)
+        got = abq.gemm_arbitrary(abq.bitpack(a, p), abq.bitpack(b, q), abq.default_tile(p, q)).cpu().numpy()
+        assert np.array_equal(got, orc.gemm_codes(a, p, b, q)), (trial, m, n, k, p, q)
+
+
+def test_tc_variant_matches_popc(abq):
+    """same call under the forced AND+popcount variant gives the same bits"""
+    rng = np.random.default_rng(23)
+    a = rng.integers(0, 16, (64, 1024), dtype=np.uint8)
+    b = rng.integers(0, 16, (300, 1024), dtype=np.uint8)
+    pa, pb = abq.bitpack(a, 4), abq.bitpack(b, 4)
+    tc = abq.gemm_arbitrary(pa, pb, abq.default_tile(4, 4))
+    abq.api.set_gemv_variant("popc")
+    try:
+        popc = abq.gemm_arbitrary(pa, pb, abq.default_tile(4, 4))
+    finally:
+        abq.api.set_gemv_variant("auto")
+    assert torch.equal(tc, popc)
