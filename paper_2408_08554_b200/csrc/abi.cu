@@ -98,7 +98,11 @@ int run_prepack_tc(const uint64_t* planes, unsigned q, size_t n, size_t k, uint3
                    cudaStream_t st);
 bool gemm_tc_supported(size_t k, size_t ldk);
 int run_gemm_tc(const uint32_t* wtc, unsigned q, size_t n, size_t k, const uint8_t* act, size_t ldk,
-                size_t m, const EpiParams& e, cudaStream_t st);
+                size_t m, const EpiParams& e, cudaStream_t st, unsigned long long* bad_word = nullptr,
+                unsigned long long* bad_out = nullptr, bool pdl = false);
+int run_act_quant(const void* x, int x_dtype, size_t m, size_t k, int mt, const QuantParams& qp,
+                  uint32_t* out, int row_ld, double* s_a, int32_t* z_a, long long* rowsum,
+                  unsigned long long* bad_word, cudaStream_t st);
 
 // decode GEMV on the tensor pipe: weights prepacked, M <= 8 tokens
 static bool use_imma(const abq_weights* w, size_t m, size_t k) {
@@ -569,15 +573,23 @@ int abq_linear(const void* x, int x_dtype, size_t m, size_t k, const abq_quant_s
   } else if (use_tc(w, m, k, !fits_int32_host(p, w->q, k))) {
     // ReQuant straight to u8 codes (K1), then the tcgen05 GEMM with the fused epilogue
     uint8_t* codes = reinterpret_cast<uint8_t*>(range + 32);
-    st = run_quantize(x, x_dtype, m, k, params_of(*act_spec), nullptr, nullptr, codes, nullptr, p, sa,
-                      za, ra, bad, range, s);
+    unsigned long long* bad_word = range + 2;  // zero-filled workspace word
+    // per-token (or few-token per-tensor) ReQuant: one CTA per token, PDL into the GEMM
+    const bool fast_k1 = act_spec->granularity != ABQ_PER_TENSOR || m <= 8;
+    if (fast_k1) {
+      st = run_act_quant(x, x_dtype, m, k, 1, params_of(*act_spec), reinterpret_cast<uint32_t*>(codes),
+                         static_cast<int>(k), sa, za, reinterpret_cast<long long*>(ra), bad_word, s);
+    } else {
+      st = run_quantize(x, x_dtype, m, k, params_of(*act_spec), nullptr, nullptr, codes, nullptr, p, sa,
+                        za, ra, bad, range, s);
+    }
     if (st) return st;
     EpiParams e{};
     e.mode = mode;
     e.out = y;
     e.ldo = static_cast<long long>(w->n);
     e.s_a = sa;
-    e.sa_stride = act_spec->granularity == ABQ_PER_TENSOR ? 0 : 1;
+    e.sa_stride = fast_k1 || act_spec->granularity != ABQ_PER_TENSOR ? 1 : 0;
     e.z_a = za;
     e.za_stride = e.sa_stride;
     e.rowsum_a = ra;
@@ -587,7 +599,8 @@ int abq_linear(const void* x, int x_dtype, size_t m, size_t k, const abq_quant_s
     e.zb_stride = w->per_tensor ? 0 : 1;
     e.colsum_b = w->colsums;
     e.k = static_cast<long long>(k);
-    st = run_gemm_tc(w->tc, w->q, w->n, k, codes, k, m, e, s);
+    st = run_gemm_tc(w->tc, w->q, w->n, k, codes, k, m, e, s, fast_k1 ? bad_word : nullptr,
+                     fast_k1 ? bad : nullptr, fast_k1);
     if (st) return st;
   } else {
     st = run_quantize(x, x_dtype, m, k, params_of(*act_spec), nullptr, nullptr, nullptr, planes, p, sa,

@@ -145,16 +145,19 @@ template <int Q>
 __device__ __forceinline__ void rebuild32(const uint32_t (&w)[Q], uint32_t (&r)[8]) {
 #pragma unroll
   for (int c = 0; c < 8; ++c) r[c] = 0u;
+  // plane t lands on bit (8 - Q + t): the code scaled by 2^(8-Q), so that most
+  // bit moves are left shifts (IMAD.SHL on the fma pipe) next to the LOP3 merges
+  // on the alu pipe; the accumulator is divided back exactly in the epilogue.
 #define ABQ_PLACE(T)                                                 \
   if constexpr (Q > T) {                                             \
-    r[0] |= plane_to_codes<T, 0>(w[T]);                              \
-    r[1] |= plane_to_codes<T, 1>(w[T]);                              \
-    r[2] |= plane_to_codes<T, 2>(w[T]);                              \
-    r[3] |= plane_to_codes<T, 3>(w[T]);                              \
-    r[4] |= plane_to_codes<T, 4>(w[T]);                              \
-    r[5] |= plane_to_codes<T, 5>(w[T]);                              \
-    r[6] |= plane_to_codes<T, 6>(w[T]);                              \
-    r[7] |= plane_to_codes<T, 7>(w[T]);                              \
+    r[0] |= plane_to_codes<8 - Q + T, 0>(w[T]);                      \
+    r[1] |= plane_to_codes<8 - Q + T, 1>(w[T]);                      \
+    r[2] |= plane_to_codes<8 - Q + T, 2>(w[T]);                      \
+    r[3] |= plane_to_codes<8 - Q + T, 3>(w[T]);                      \
+    r[4] |= plane_to_codes<8 - Q + T, 4>(w[T]);                      \
+    r[5] |= plane_to_codes<8 - Q + T, 5>(w[T]);                      \
+    r[6] |= plane_to_codes<8 - Q + T, 6>(w[T]);                      \
+    r[7] |= plane_to_codes<8 - Q + T, 7>(w[T]);                      \
   }
   ABQ_PLACE(0)
   ABQ_PLACE(1)
@@ -172,6 +175,9 @@ struct TcParams {
   const uint8_t* act;   // u8 activation codes, row stride ldk (multiple of 16, 16B aligned)
   int q, n, k, m, ldk, rowtiles, kblocks;
   EpiParams e;
+  unsigned long long* bad_word;  // ReQuant status (~index, 0 = none), published to bad_out
+  unsigned long long* bad_out;
+  int pdl;                       // launched as a programmatic dependent of the ReQuant kernel
 };
 
 template <int Q, int TT, int S>
@@ -245,10 +251,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(TcParams P) {
       }
     }
   };
-#pragma unroll
-  for (int j = 0; j < DA; ++j) issue_act(j);
+  // weights do not depend on the preceding ReQuant kernel: start them first,
+  // then wait for its codes (programmatic dependent launch; a no-op otherwise)
 #pragma unroll
   for (int j = 0; j < DW; ++j) issue_w(j, wring[j]);
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (P.bad_out && blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) {
+    const unsigned long long w = *P.bad_word;
+    *P.bad_out = w ? ~w : ~0ull;
+    *P.bad_word = 0ull;
+  }
+#pragma unroll
+  for (int j = 0; j < DA; ++j) issue_act(j);
 
   // one copy of the stage body (compact hot loop); the weight ring shifts by one stage
   for (int kb = 0; kb < P.kblocks; ++kb) {
@@ -330,7 +344,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(TcParams P) {
     for (int i = 0; i < 8; ++i) {
       const int tk = tok0 + c0 + i;
       if (tk >= P.m) continue;
-      const long long acc = static_cast<long long>(static_cast<int32_t>(v[i]));
+      const long long acc = static_cast<long long>(static_cast<int32_t>(v[i]) >> (8 - Q));
       const long long o = static_cast<long long>(tk) * E.ldo + ch;
       if (raw) {
         if (E.mode == EPI_ACC_I32) static_cast<int32_t*>(E.out)[o] = static_cast<int32_t>(acc);
@@ -386,7 +400,18 @@ static int launch_tc(const TcParams& P, cudaStream_t st) {
                                          static_cast<int>(smem));
   if (err != cudaSuccess) return fail(ABQ_ERR_CUDA, "gemm_tc: smem attribute: %s", cudaGetErrorString(err));
   dim3 grid(static_cast<unsigned>(P.rowtiles), static_cast<unsigned>((P.m + TT - 1) / TT));
-  kern<<<grid, kTcThreads, smem, st>>>(P);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(kTcThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = P.pdl ? 1 : 0;
+  err = cudaLaunchKernelEx(&cfg, kern, P);
+  if (err != cudaSuccess) return fail(ABQ_ERR_CUDA, "gemm_tc: launch: %s", cudaGetErrorString(err));
   ABQ_LAUNCHED();
   return ABQ_OK;
 }
@@ -401,12 +426,19 @@ static int launch_tt(const TcParams& P, cudaStream_t st) {
 }
 
 // act: u8 codes [m][ldk]; requires k % 16 == 0, ldk % 16 == 0 and a 16-B aligned act.
-bool gemm_tc_supported(size_t k, size_t ldk) { return k > 0 && k % 16 == 0 && ldk % 16 == 0; }
+// K <= 32768 keeps the scaled-code accumulator (255 * 255 * K) inside s32
+bool gemm_tc_supported(size_t k, size_t ldk) {
+  return k > 0 && k <= 32768 && k % 16 == 0 && ldk % 16 == 0;
+}
 
 int run_gemm_tc(const uint32_t* wtc, unsigned q, size_t n, size_t k, const uint8_t* act, size_t ldk,
-                size_t m, const EpiParams& e, cudaStream_t st) {
+                size_t m, const EpiParams& e, cudaStream_t st, unsigned long long* bad_word,
+                unsigned long long* bad_out, bool pdl) {
   if (m == 0 || n == 0) return ABQ_OK;
   TcParams P{};
+  P.bad_word = bad_word;
+  P.bad_out = bad_out;
+  P.pdl = pdl ? 1 : 0;
   P.wtc = wtc;
   P.act = act;
   P.q = static_cast<int>(q);

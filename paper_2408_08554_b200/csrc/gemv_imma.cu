@@ -47,7 +47,6 @@ namespace abq_dev {
 
 constexpr int kRowTile = 16;
 constexpr int kKBlock = 256;
-constexpr int kWeightSmem = 176 * 1024;  // per-CTA TMA ring budget
 
 // ---------------------------------------------------------------------------
 // prepack: ABQP [q][n][wpr] -> fragment-major [rt][kb][q][lane][4]
@@ -149,13 +148,16 @@ __device__ __forceinline__ int act_frag_index(int v, int i, int mt) {
 // ---------------------------------------------------------------------------
 constexpr int kActThreads = 256;
 
-template <typename T>
+// ROW: write plain row-major u8 codes [m][row_ld] (tcgen05 GEMM operand)
+// instead of the GEMV's B-fragment order.
+template <typename T, bool ROW>
 __global__ void __launch_bounds__(kActThreads) act_quant_kernel(const T* __restrict__ x, int m, int k, int mt,
                                                                 QuantParams qp, uint32_t* __restrict__ act_frag,
-                                                                double* __restrict__ s_a, long long* __restrict__ z_a,
+                                                                int row_ld, double* __restrict__ s_a,
+                                                                int32_t* __restrict__ z_a,
                                                                 long long* __restrict__ rowsum,
                                                                 unsigned long long* __restrict__ bad_word) {
-  griddep_launch();  // let the dependent GEMV start streaming its weights now
+  griddep_launch();  // let the dependent GEMV / GEMM start streaming its weights now
   __shared__ double s_lo[kActThreads / 32], s_hi[kActThreads / 32];
   __shared__ long long s_sum[kActThreads / 32];
   __shared__ double s_step;
@@ -164,7 +166,10 @@ __global__ void __launch_bounds__(kActThreads) act_quant_kernel(const T* __restr
   const int tok = blockIdx.x;
   const int tb = tok / mt, i = tok % mt;
   const int kpad = ((k + kKBlock - 1) / kKBlock) * kKBlock;
-  uint32_t* dst = act_frag + static_cast<size_t>(tb) * mt * kpad / 4;
+  uint32_t* dst = ROW ? act_frag + static_cast<size_t>(tok) * row_ld / 4
+                      : act_frag + static_cast<size_t>(tb) * mt * kpad / 4;
+  // u32 slot of the codes of elements 4v..4v+3
+  auto slot_of = [&](int v) { return ROW ? v : act_frag_index(v, i, mt); };
   const T* row = x + static_cast<size_t>(tok) * k;
   if constexpr (sizeof(T) == 2) {
     // fp16 rows, per token, K % 8 == 0, K <= 8 * 4 * kActThreads: the row is read
@@ -232,12 +237,13 @@ __global__ void __launch_bounds__(kActThreads) act_quant_kernel(const T* __restr
             if (e < 4) w0 |= c << (8 * e);
             else w1 |= c << (8 * (e - 4));
           }
-          dst[act_frag_index(2 * idx, i, mt)] = w0;
-          dst[act_frag_index(2 * idx + 1, i, mt)] = w1;
+          dst[slot_of(2 * idx)] = w0;
+          dst[slot_of(2 * idx + 1)] = w1;
         }
       }
       // zero codes in the k padding of the last 256-block
-      for (int v4 = k / 4 + tid; v4 < kpad / 4; v4 += kActThreads) dst[act_frag_index(v4, i, mt)] = 0u;
+      if (!ROW)
+        for (int v4 = k / 4 + tid; v4 < kpad / 4; v4 += kActThreads) dst[act_frag_index(v4, i, mt)] = 0u;
       rsum = warp_sum(rsum);
       if (lane == 0) s_sum[warp] = rsum;
       __syncthreads();
@@ -302,7 +308,7 @@ __global__ void __launch_bounds__(kActThreads) act_quant_kernel(const T* __restr
         word |= c << (8 * b);
       }
     }
-    dst[act_frag_index(v, i, mt)] = word;
+    if (!ROW || 4 * v < k) dst[slot_of(v)] = word;
   }
   rsum = warp_sum(rsum);
   if (lane == 0) s_sum[warp] = rsum;
@@ -324,7 +330,7 @@ struct ImmaParams {
   // activations: codes from act_quant_kernel (act_frag + stats) or packed planes
   const uint32_t* act_frag;
   const double* s_a;
-  const long long* z_a;
+  const int32_t* z_a;
   const long long* rowsum;
   const uint64_t* a_planes;
   int p;
@@ -335,7 +341,10 @@ struct ImmaParams {
   unsigned long long* bad_word;  // written by act_quant_kernel (~index, 0 = none)
   unsigned long long* bad_out;   // published here: first bad index or ~0
   unsigned long long* trace;     // optional [grid][4] globaltimer stamps (profiling)
+  const __half* x16;             // fused path: fp16 activations quantized in the prologue
+  QuantParams qp;
   int slots;                     // TMA ring slots per warp
+  int upc;                       // units per TMA chunk (chunks of ~4 KB stream at full HBM rate)
 };
 
 // FROM_PLANES: activations are given as ABQP planes (API path) instead of
@@ -363,8 +372,9 @@ __global__ void __launch_bounds__(NWARP * 32, 1) gemv_imma_kernel(ImmaParams P) 
   const int unit_bytes = q * 512;
 
   // shared memory carve-up
-  unsigned char* wring = smem;                                                        // [16][slots][unit]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(wring + NWARP * P.slots * unit_bytes);  // [16][slots]
+  const int chunk_bytes = P.upc * unit_bytes;
+  unsigned char* wring = smem;                                                         // [warps][slots][chunk]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(wring + NWARP * P.slots * chunk_bytes);  // [warps][slots]
   uint32_t* act = reinterpret_cast<uint32_t*>(bars + NWARP * P.slots);           // MT * kpad bytes
   long long* accs = reinterpret_cast<long long*>(reinterpret_cast<unsigned char*>(act) + MT * kpad);
   double* c_sb = reinterpret_cast<double*>(accs + nlrt * 16 * MT);  // per-channel epilogue params
@@ -385,19 +395,27 @@ __global__ void __launch_bounds__(NWARP * 32, 1) gemv_imma_kernel(ImmaParams P) 
   // ---- 1. this warp's units; start its TMA weight ring immediately
   const long long wu0 = U0 + (U1 - U0) * warp / NWARP;
   const long long wu1 = U0 + (U1 - U0) * (warp + 1) / NWARP;
-  unsigned char* my_ring = wring + warp * P.slots * unit_bytes;
+  unsigned char* my_ring = wring + warp * P.slots * chunk_bytes;
   uint64_t* my_bars = bars + warp * P.slots;
   const unsigned char* wsrc = reinterpret_cast<const unsigned char*>(P.frag);
   if (lane == 0) {
     for (int s = 0; s < P.slots; ++s) mbar_init1(&my_bars[s]);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int s = 0; s < P.slots && wu0 + s < wu1; ++s) {
-      mbar_expect_tx(&my_bars[s], unit_bytes);
-      tma_bulk_g2s(my_ring + s * unit_bytes, wsrc + (wu0 + s) * unit_bytes, unit_bytes, &my_bars[s]);
+    for (int s = 0; s < P.slots; ++s) {
+      const long long un = wu0 + static_cast<long long>(s) * P.upc;
+      if (un >= wu1) break;
+      const long long un1 = un + P.upc < wu1 ? un + P.upc : wu1;
+      const uint32_t bytes = static_cast<uint32_t>((un1 - un) * unit_bytes);
+      mbar_expect_tx(&my_bars[s], bytes);
+      tma_bulk_g2s(my_ring + s * chunk_bytes, wsrc + un * unit_bytes, bytes, &my_bars[s]);
     }
   }
 
-  // ---- 2. per-channel epilogue parameters of this CTA's row-tiles, zero accumulators
+  // ---- 2. per-channel epilogue parameters of this CTA's row-tiles, zero accumulators.
+  // The epilogue's scalar parameters are copied to shared memory here, so
+  // their constant-bank loads happen now instead of after the main loop.
+  __shared__ EpiParams s_e;
+  if (tid == 0) s_e = P.e;
   const bool dequant = P.e.mode != EPI_ACC_I32 && P.e.mode != EPI_ACC_I64;
   for (int idx = tid; dequant && idx < nlrt * 16; idx += NWARP * 32) {
     const int j = rt_first * kRowTile + idx;
@@ -425,6 +443,94 @@ __global__ void __launch_bounds__(NWARP * 32, 1) gemv_imma_kernel(ImmaParams P) 
       }
       act[act_frag_index(v, i, MT)] = word;
     }
+  } else if (P.x16) {
+    // Fused ReQuant (decode, m <= 2, fp16, per token): every CTA quantizes the
+    // activation rows itself while its TMA weight ring fills -- no extra launch.
+    // Row held in registers (<= 4 x 16 B per thread), min/max in fp32 (exact for
+    // fp16), step / zero point / codes in FP64 exactly as quantizer.hpp:169-210.
+    for (int idx = tid; idx < MT * kpad / 4; idx += NWARP * 32) act[idx] = 0u;
+    const int nvec = P.k >> 3;
+    const double top = static_cast<double>(P.qp.levels - 1);
+    for (int i = 0; i < mb; ++i) {
+      const uint4* xr = reinterpret_cast<const uint4*>(P.x16 + static_cast<size_t>(tok0 + i) * P.k);
+      uint4 v[4];
+      float lo = CUDART_INF_F, hi = -CUDART_INF_F;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int idx = tid + r * NWARP * 32;
+        v[r] = make_uint4(0u, 0u, 0u, 0u);
+        if (idx < nvec) {
+          v[r] = __ldg(xr + idx);
+          const __half2* h2 = reinterpret_cast<const __half2*>(&v[r]);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 f = __half22float2(h2[e]);
+            if (blockIdx.x == 0 && P.bad_out) {
+              if (!isfinite(f.x)) atomicMax(P.bad_word, ~(static_cast<unsigned long long>(tok0 + i) * P.k + idx * 8 + 2 * e));
+              if (!isfinite(f.y)) atomicMax(P.bad_word, ~(static_cast<unsigned long long>(tok0 + i) * P.k + idx * 8 + 2 * e + 1));
+            }
+            lo = fminf(lo, fminf(f.x, f.y));
+            hi = fmaxf(hi, fmaxf(f.x, f.y));
+          }
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+      }
+      __shared__ float q_lo[NWARP], q_hi[NWARP];
+      __shared__ long long q_sum[NWARP];
+      if (lane == 0) {
+        q_lo[warp] = lo;
+        q_hi[warp] = hi;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        double l = q_lo[0], h = q_hi[0];
+        for (int w = 1; w < NWARP; ++w) {
+          l = fmin(l, static_cast<double>(q_lo[w]));
+          h = fmax(h, static_cast<double>(q_hi[w]));
+        }
+        double step;
+        int z;
+        group_params(P.qp, l, h, &step, &z);
+        s_sa[i] = step;
+        s_za[i] = z;
+      }
+      __syncthreads();
+      const double step = s_sa[i], zd = static_cast<double>(s_za[i]), inv = 1.0 / step;
+      long long rsum = 0;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int idx = tid + r * NWARP * 32;
+        if (idx < nvec) {
+          const __half* hv = reinterpret_cast<const __half*>(&v[r]);
+          uint32_t w0 = 0, w1 = 0;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const unsigned c = quant_code_fast(static_cast<double>(__half2float(hv[e])), step, inv, zd, top);
+            rsum += c;
+            if (e < 4) w0 |= c << (8 * e);
+            else w1 |= c << (8 * (e - 4));
+          }
+          act[act_frag_index(2 * idx, i, MT)] = w0;
+          act[act_frag_index(2 * idx + 1, i, MT)] = w1;
+        }
+      }
+      rsum = warp_sum(rsum);
+      if (lane == 0) q_sum[warp] = rsum;
+      __syncthreads();
+      if (tid == 0) {
+        long long rr = 0;
+        for (int w = 0; w < NWARP; ++w) rr += q_sum[w];
+        s_ra[i] = rr;
+      }
+    }
+    if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0 && P.bad_out) {  // only CTA 0 reports
+      const unsigned long long w = atomicExch(P.bad_word, 0ull);
+      *P.bad_out = w ? ~w : ~0ull;
+    }
   } else {
     griddep_wait();  // act_quant_kernel done and its writes visible
     const uint4* src = reinterpret_cast<const uint4*>(P.act_frag + static_cast<size_t>(blockIdx.y) * MT * kpad / 4);
@@ -445,21 +551,18 @@ __global__ void __launch_bounds__(NWARP * 32, 1) gemv_imma_kernel(ImmaParams P) 
   if (trace && tid == 0) trace[1] = clock64();
 
   // ---- 4. main loop over this warp's units (one body, TMA ring slots)
-  int acc[QMAX][4];
-#pragma unroll
-  for (int t = 0; t < QMAX; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0;
+  // one accumulator fragment: the q planes of a chunk are merged into one A
+  // register set holding code << (8 - q) (plane t on bit 8 - q + t), so each
+  // k32 chunk costs one IMMA; the 2^(8-q) scale is divided out exactly in flush.
+  int acc[4] = {0, 0, 0, 0};
   int cur_rt = wu0 < wu1 ? static_cast<int>(wu0 / P.kblocks) : -1;
   const uint2* act2 = reinterpret_cast<const uint2*>(act);
 
   auto flush = [&](int rt) {
     const int lrt = rt - rt_first;
-    long long v[4] = {0, 0, 0, 0};
+    long long v[4];
 #pragma unroll
-    for (int t = 0; t < QMAX; ++t)
-      if (t < q) {
-#pragma unroll
-        for (int r = 0; r < 4; ++r) v[r] += static_cast<long long>(acc[t][r] >> 7) << t;
-      }
+    for (int r = 0; r < 4; ++r) v[r] = static_cast<long long>(acc[r] >> (8 - q));
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       const int row = g + 8 * (r >> 1), tok = 2 * tig + (r & 1);
@@ -467,20 +570,18 @@ __global__ void __launch_bounds__(NWARP * 32, 1) gemv_imma_kernel(ImmaParams P) 
                               static_cast<unsigned long long>(v[r]));
     }
 #pragma unroll
-    for (int t = 0; t < QMAX; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0;
+    for (int r = 0; r < 4; ++r) acc[r] = 0;
   };
 
+  // incremental (row-tile, k-block, chunk) counters: no divisions in the loop
   int slot = 0;
   uint32_t phase = 0;
-  for (long long uu = wu0; uu < wu1; ++uu) {
-    const int rt = static_cast<int>(uu / P.kblocks);
-    const int kb = static_cast<int>(uu - static_cast<long long>(rt) * P.kblocks);
-    if (rt != cur_rt) {
-      flush(cur_rt);
-      cur_rt = rt;
-    }
-    mbar_wait_parity(&my_bars[slot], phase);
-    const uint4* wv = reinterpret_cast<const uint4*>(my_ring + slot * unit_bytes) + lane;
+  const int uend = static_cast<int>(wu1);
+  int rt = cur_rt, kb = wu0 < wu1 ? static_cast<int>(wu0 - static_cast<long long>(cur_rt) * P.kblocks) : 0;
+  int ui = 0, cidx = 0;  // unit within the chunk, chunk index
+  for (int uu = static_cast<int>(wu0); uu < uend; ++uu) {
+    if (ui == 0) mbar_wait_parity(&my_bars[slot], phase);
+    const uint4* wv = reinterpret_cast<const uint4*>(my_ring + slot * chunk_bytes + ui * unit_bytes) + lane;
     uint4 w[QMAX];
 #pragma unroll
     for (int t = 0; t < QMAX; ++t)
@@ -490,33 +591,71 @@ __global__ void __launch_bounds__(NWARP * 32, 1) gemv_imma_kernel(ImmaParams P) 
     for (int c = 0; c < 8; ++c) {
       uint2 b = make_uint2(0u, 0u);
       if (g < MT) b = ab[(c * MT + g) * 4 + tig];
+      uint32_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
 #pragma unroll
       for (int t = 0; t < QMAX; ++t) {
         if (t < q) {
-          const uint32_t a0 = (w[t].x << (7 - c)) & 0x80808080u;
-          const uint32_t a1 = (w[t].y << (7 - c)) & 0x80808080u;
-          const uint32_t a2 = (w[t].z << (7 - c)) & 0x80808080u;
-          const uint32_t a3 = (w[t].w << (7 - c)) & 0x80808080u;
-          imma_16832(acc[t], a0, a1, a2, a3, b.x, b.y);
+          // bit (8b + c) of the plane word -> bit (8b + 8 - q + t) of the code byte
+          const int tb = 8 - q + t;
+          const uint32_t m = 0x01010101u << tb;
+          if (tb >= c) {
+            a0 |= (w[t].x << (tb - c)) & m;
+            a1 |= (w[t].y << (tb - c)) & m;
+            a2 |= (w[t].z << (tb - c)) & m;
+            a3 |= (w[t].w << (tb - c)) & m;
+          } else {
+            // right shift as the high word of a multiply: IMAD.HI runs on the
+            // fma pipe and leaves the alu pipe to the LOP3 merges
+            const uint32_t f = 1u << (32 - (c - tb));
+            a0 |= __umulhi(w[t].x, f) & m;
+            a1 |= __umulhi(w[t].y, f) & m;
+            a2 |= __umulhi(w[t].z, f) & m;
+            a3 |= __umulhi(w[t].w, f) & m;
+          }
         }
       }
+      imma_16832(acc, a0, a1, a2, a3, b.x, b.y);
     }
-    // refill this slot with the unit `slots` ahead (the whole warp has read it)
-    __syncwarp();
-    const long long un = uu + P.slots;
-    if (lane == 0 && un < wu1) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_expect_tx(&my_bars[slot], unit_bytes);
-      tma_bulk_g2s(my_ring + slot * unit_bytes, wsrc + un * unit_bytes, unit_bytes, &my_bars[slot]);
+    // chunk finished: refill its slot with the chunk `slots` ahead (the whole
+    // warp has read it)
+    if (++ui == P.upc || uu + 1 == uend) {
+      __syncwarp();
+      const int un = static_cast<int>(wu0) + (cidx + P.slots) * P.upc;  // first unit to load next
+      if (lane == 0 && un < uend) {
+        const int un1 = un + P.upc < uend ? un + P.upc : uend;
+        const uint32_t bytes = static_cast<uint32_t>(un1 - un) * static_cast<uint32_t>(unit_bytes);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&my_bars[slot], bytes);
+        tma_bulk_g2s(my_ring + slot * chunk_bytes, wsrc + static_cast<size_t>(un) * unit_bytes, bytes,
+                     &my_bars[slot]);
+      }
+      ui = 0;
+      ++cidx;
+      if (++slot == P.slots) {
+        slot = 0;
+        phase ^= 1u;
+      }
     }
-    if (++slot == P.slots) {
-      slot = 0;
-      phase ^= 1u;
+    // row-tile finished: fold its plane accumulators into the CTA's sums
+    if (++kb == P.kblocks) {
+      flush(rt);
+      kb = 0;
+      ++rt;
     }
   }
-  if (cur_rt >= 0) flush(cur_rt);
+  if (wu0 < wu1 && kb != 0) flush(rt);  // last row-tile was cut inside this warp's range
+  __shared__ long long s_wend[NWARP];
+  if (trace && lane == 0) s_wend[warp] = clock64();
   __syncthreads();
-  if (trace && tid == 0) trace[2] = clock64();
+  if (trace && tid == 0) {  // earliest / latest warp finishing the main loop
+    long long lo = s_wend[0], hi = s_wend[0];
+    for (int w = 1; w < NWARP; ++w) {
+      lo = min(lo, s_wend[w]);
+      hi = max(hi, s_wend[w]);
+    }
+    trace[2] = lo;
+    trace[6] = hi;
+  }
 
   // ---- 5. epilogue.  Row-tiles owned by this CTA alone are stored straight
   // from shared memory; only the first / last row-tile can be cut between CTAs
@@ -536,36 +675,37 @@ __global__ void __launch_bounds__(NWARP * 32, 1) gemv_imma_kernel(ImmaParams P) 
     const int j = (rt_first + lrt) * kRowTile + row;
     if (j >= P.n) return;
     const int c = lrt * 16 + row;
-    if (P.e.mode == EPI_ACC_I32 || P.e.mode == EPI_ACC_I64) {
-      epi_store_v(P.e, tok0 + i, j, a, 0.0, 0, 0);
+    const EpiParams& E = s_e;
+    if (E.mode == EPI_ACC_I32 || E.mode == EPI_ACC_I64) {
+      epi_store_v(E, tok0 + i, j, a, 0.0, 0, 0);
       return;
     }
     // fused zero-point correction + dequant from the prefetched parameters
     double sa;
     long long za, ra;
     if (FROM_PLANES) {
-      sa = P.e.s_a[(tok0 + i) * P.e.sa_stride];
-      za = P.e.z_a[(tok0 + i) * P.e.za_stride];
-      ra = P.e.rowsum_a[tok0 + i];
+      sa = E.s_a[(tok0 + i) * E.sa_stride];
+      za = E.z_a[(tok0 + i) * E.za_stride];
+      ra = E.rowsum_a[tok0 + i];
     } else {
       sa = s_sa[i];
       za = s_za[i];
       ra = s_ra[i];
     }
     const long long zb = c_zb[c];
-    const long long corr = a - za * c_cs[c] - zb * ra + P.e.k * za * zb;
-    const long long o = static_cast<long long>(tok0 + i) * P.e.ldo + j;
-    if (P.e.mode == EPI_CORR_I64) {
-      static_cast<int64_t*>(P.e.out)[o] = corr;
+    const long long corr = a - za * c_cs[c] - zb * ra + E.k * za * zb;
+    const long long o = static_cast<long long>(tok0 + i) * E.ldo + j;
+    if (E.mode == EPI_CORR_I64) {
+      static_cast<int64_t*>(E.out)[o] = corr;
       return;
     }
     const double y = __dmul_rn(__dmul_rn(sa, c_sb[c]), static_cast<double>(corr));
-    if (P.e.mode == EPI_F64)
-      static_cast<double*>(P.e.out)[o] = y;
-    else if (P.e.mode == EPI_F16)
-      static_cast<__half*>(P.e.out)[o] = __double2half(y);
+    if (E.mode == EPI_F64)
+      static_cast<double*>(E.out)[o] = y;
+    else if (E.mode == EPI_F16)
+      static_cast<__half*>(E.out)[o] = __double2half(y);
     else
-      static_cast<float*>(P.e.out)[o] = __double2float_rn(y);
+      static_cast<float*>(E.out)[o] = __double2float_rn(y);
   };
   int nsplit = 0;
   if (trace && tid == 0) trace[4] = nlrt;
@@ -654,15 +794,20 @@ static size_t imma_smem_bytes(const ImmaParams& P, int mt, int grid_x, int nwarp
   const long long U = static_cast<long long>(P.rowtiles) * P.kblocks;
   const long long per_cta_units = (U + grid_x - 1) / grid_x + P.kblocks;
   const int nlrt_max = static_cast<int>(per_cta_units / P.kblocks + 2);
-  return static_cast<size_t>(nwarp) * P.slots * P.q * 512 + nwarp * P.slots * 8 +
+  return static_cast<size_t>(nwarp) * P.slots * P.upc * P.q * 512 + nwarp * P.slots * 8 +
          static_cast<size_t>(mt) * P.kblocks * kKBlock + static_cast<size_t>(nlrt_max) * 16 * mt * 8 +
          static_cast<size_t>(nlrt_max) * 16 * 24 + mt * 24 + 128;
 }
 
-// warps per CTA: 32 (1024 threads, <= 64 registers) for q <= 4 where the
-// unit body is ALU / issue bound and needs the extra latency hiding; 16 for
-// wider planes (more weight registers per unit)
-static int imma_warps(int q) { return q >= 1 && q <= 4 ? 32 : 16; }
+// warps per CTA: 16 (512 threads) -- leaves room on every SM for the
+// act_quant_kernel CTA that runs concurrently under programmatic dependent
+// launch, and gives each warp a 3-deep ring of ~4 KB TMA chunks
+// (profiles/r01_microbench_stream.txt: >= 4 KB bulk copies stream at ~7.2 TB/s,
+// 2 KB copies at ~5 TB/s).
+static int imma_warps(int q) {
+  (void)q;
+  return 16;
+}
 
 template <int QT, int MT, bool FROM_PLANES, int NWARP>
 static int launch_imma_w(ImmaParams P, int grid_x, int grid_y, bool pdl, cudaStream_t st) {
@@ -690,7 +835,6 @@ static int launch_imma_w(ImmaParams P, int grid_x, int grid_y, bool pdl, cudaStr
 
 template <int QT, int MT, bool FROM_PLANES>
 static int launch_imma(ImmaParams P, int grid_x, int grid_y, bool pdl, cudaStream_t st) {
-  if (QT >= 1 && QT <= 4) return launch_imma_w<QT, MT, FROM_PLANES, 32>(P, grid_x, grid_y, pdl, st);
   return launch_imma_w<QT, MT, FROM_PLANES, 16>(P, grid_x, grid_y, pdl, st);
 }
 
@@ -732,13 +876,14 @@ static void plan_grid(ImmaParams& P, int mt, bool stream_k, int* gx) {
     *gx = static_cast<int>(std::min<long long>(num_sms(), std::max<long long>(1, U / nwarp)));
   else
     *gx = std::min(num_sms(), P.rowtiles);
-  // TMA ring depth: as many unit slots per warp as the smem budget allows (<= 8)
+  // TMA chunks of ~4 KB (whole units), ring as deep as shared memory allows (<= 4)
   const int unit = P.q * 512;
-  const size_t other = static_cast<size_t>(mt) * P.kblocks * kKBlock + 48 * 1024;
-  int slots = static_cast<int>((kWeightSmem + 48 * 1024 - other) / (nwarp * unit));
-  if (slots > 8) slots = 8;
-  if (slots < 2) slots = 2;
-  P.slots = slots;
+  P.upc = unit >= 4096 ? 1 : 4096 / unit;
+  P.slots = 1;
+  for (int s = 4; s >= 2; --s) {
+    P.slots = s;
+    if (imma_smem_bytes(P, mt, *gx, nwarp) <= 220 * 1024) break;
+  }
 }
 
 static ImmaParams base_params(const uint32_t* frag, unsigned q, size_t n, size_t k, size_t m,
@@ -771,6 +916,34 @@ int run_gemv_imma_planes(const uint32_t* frag, unsigned q, size_t n, size_t k, s
   return launch_mt<true>(P, mt, gx, gy, false, st);
 }
 
+// K1 launcher: one CTA per token.  row_ld == 0: B-fragment order for the decode
+// GEMV (token blocks of mt); row_ld > 0: row-major u8 codes for the tcgen05 GEMM
+// (row_ld % 16 == 0).  bad_word: zero-initialised, receives atomicMax(~index).
+int run_act_quant(const void* x, int x_dtype, size_t m, size_t k, int mt, const QuantParams& qp,
+                  uint32_t* out, int row_ld, double* s_a, int32_t* z_a, long long* rowsum,
+                  unsigned long long* bad_word, cudaStream_t st) {
+  const dim3 grid(static_cast<unsigned>(m)), block(kActThreads);
+  const int im = static_cast<int>(m), ik = static_cast<int>(k);
+#define ABQ_ACTQ(T, ROWL)                                                                                  \
+  act_quant_kernel<T, ROWL><<<grid, block, 0, st>>>(static_cast<const T*>(x), im, ik, mt, qp, out, row_ld, s_a, \
+                                                   z_a, rowsum, bad_word)
+  const bool row = row_ld > 0;
+  switch (x_dtype) {
+    case ABQ_F16:
+      if (row) ABQ_ACTQ(__half, true); else ABQ_ACTQ(__half, false);
+      break;
+    case ABQ_F32:
+      if (row) ABQ_ACTQ(float, true); else ABQ_ACTQ(float, false);
+      break;
+    default:
+      if (row) ABQ_ACTQ(double, true); else ABQ_ACTQ(double, false);
+      break;
+  }
+#undef ABQ_ACTQ
+  ABQ_LAUNCHED();
+  return ABQ_OK;
+}
+
 // Serving path: act_quant_kernel (ReQuant into B-fragment codes) followed by the
 // stream-K GEMV with programmatic dependent launch.  `ws` must be
 // imma_ws_bytes(n, k) of zero-filled device memory (left zeroed).
@@ -790,7 +963,7 @@ int run_gemv_imma_fused(const uint32_t* frag, unsigned q, size_t n, size_t k, si
   uint32_t* act_frag = reinterpret_cast<uint32_t*>(w);
   w += 8 * kpad;
   double* s_a = reinterpret_cast<double*>(w);
-  long long* z_a = reinterpret_cast<long long*>(w + 64);
+  int32_t* z_a = reinterpret_cast<int32_t*>(w + 64);
   long long* rowsum = reinterpret_cast<long long*>(w + 128);
   unsigned long long* bad_word = reinterpret_cast<unsigned long long*>(w + 192);
   P.act_frag = act_frag;
@@ -799,30 +972,31 @@ int run_gemv_imma_fused(const uint32_t* frag, unsigned q, size_t n, size_t k, si
   P.rowsum = rowsum;
   P.bad_word = bad_word;
   P.bad_out = bad_out;
-  // K1: one CTA per token
-  switch (x_dtype) {
-    case ABQ_F16:
-      act_quant_kernel<__half><<<static_cast<unsigned>(m), kActThreads, 0, st>>>(
-          static_cast<const __half*>(x), static_cast<int>(m), static_cast<int>(k), mt, qp, act_frag, s_a, z_a,
-          rowsum, bad_word);
-      break;
-    case ABQ_F32:
-      act_quant_kernel<float><<<static_cast<unsigned>(m), kActThreads, 0, st>>>(
-          static_cast<const float*>(x), static_cast<int>(m), static_cast<int>(k), mt, qp, act_frag, s_a, z_a,
-          rowsum, bad_word);
-      break;
-    default:
-      act_quant_kernel<double><<<static_cast<unsigned>(m), kActThreads, 0, st>>>(
-          static_cast<const double*>(x), static_cast<int>(m), static_cast<int>(k), mt, qp, act_frag, s_a, z_a,
-          rowsum, bad_word);
-      break;
+  P.qp = qp;
+  // m <= 2 fp16 per-token rows: ReQuant fused into every CTA's prologue (one
+  // launch); otherwise a separate ReQuant kernel overlapped by PDL.
+  const bool fused = x_dtype == ABQ_F16 && !qp.per_tensor && m <= 2 && k % 8 == 0 &&
+                     k <= static_cast<size_t>(8 * 4 * imma_warps(P.q) * 32);
+  if (fused) {
+    P.x16 = static_cast<const __half*>(x);
+  } else {
+    int st_code = run_act_quant(x, x_dtype, m, k, mt, qp, act_frag, 0, s_a, z_a, rowsum, bad_word, st);
+    if (st_code) return st_code;
   }
-  ABQ_LAUNCHED();
+  // Stream-K (unit-granular split, cross-CTA partial sums) pays a global fence
+  // and atomics; with >= 4 row-tiles per SM the row-tile-granular split is
+  // balanced enough and has no cross-CTA traffic.  ABQ_GEMV_STREAMK=0/1 overrides.
+  bool stream_k = P.rowtiles < 4 * num_sms();
+  if (const char* env = std::getenv("ABQ_GEMV_STREAMK")) stream_k = env[0] == '1';
+  if (!stream_k) {
+    P.gacc = nullptr;
+    P.gcnt = nullptr;
+  }
   int gx;
-  plan_grid(P, mt, true, &gx);
+  plan_grid(P, mt, stream_k, &gx);
   const int gy = static_cast<int>((m + mt - 1) / mt);
   if (gy != 1) return fail(ABQ_ERR_VALUE, "gemv_imma: fused path supports m <= 8");
-  return launch_mt<false>(P, mt, gx, gy, true, st);
+  return launch_mt<false>(P, mt, gx, gy, !fused, st);
 }
 
 }  // namespace abq_dev

@@ -30,6 +30,8 @@ def stat(a, lab):
     print(f"  {lab:28s} median {np.median(a) / ghz / 1e3:6.2f} us  max {a.max() / ghz / 1e3:6.2f} us")
 print(f"{name}: {len(t)} CTAs, local row-tiles/CTA median {np.median(t[:, 4]):.0f}")
 stat(t[:, 1] - t[:, 0], "prologue (wait + act copy)")
-stat(t[:, 2] - t[:, 1], "main loop")
-stat(t[:, 5] - t[:, 2], "owned-tile epilogue")
+stat(t[:, 2] - t[:, 1], "main loop (first warp done)")
+stat(t[:, 6] - t[:, 1], "main loop (last warp done)")
+stat(t[:, 5] - t[:, 6], "owned-tile epilogue")
+stat(t[:, 6] - t[:, 0], "start -> last warp done")
 stat(t[:, 3] - t[:, 5], "split-tile atomics")
