@@ -283,17 +283,21 @@ def run_ours(args, world, rank, local):
     import torch
 
     import paper_2408_08554_b200 as abq
-    m, n_full, k, wb, ab, desc = WORKLOADS[args.workload]
-    # column-parallel sharding: rank r owns channels [r*N/G, (r+1)*N/G)
-    n_lo, n_hi = n_full * rank // world, n_full * (rank + 1) // world
-    n = n_hi - n_lo
+    m, n, k, wb, ab, desc = WORKLOADS[args.workload]
+    # column-parallel sharding, weak scaling: the layer has
+    # world x N output channels and rank r owns channels [r*N, (r+1)*N) -- the
+    # workload's N per GPU at every GPU count.  No data-path collective; the
+    # output all-gather (where a layer's output must be reassembled) is timed
+    # as a separate leg below.
+    n_full = n * world
     wbytes_full = packed_bytes(n_full, k, wb)
     wbytes = packed_bytes(n, k, wb)
     l2 = torch.cuda.get_device_properties(local).L2_cache_size
     copies = int(min(256, max(2, math.ceil(4 * l2 / wbytes))))
-    x_np, wc, sb, zb, ws = build_layer(abq, torch, m, n_full, k, wb, ab, 1)
-    full = ws[0]
-    shard = full.shard(rank, world) if world > 1 else full
+    # every rank draws the same activations (seeded) and its own weight shard
+    x_np, wc, sb, zb, ws = build_layer(abq, torch, m, n, k, wb, ab, 1, seed=42 + rank)
+    x_np = np.random.default_rng(42).standard_normal((m, k)).astype(np.float16)
+    shard = ws[0]
     if args.variant != "auto":
         abq.api.set_gemv_variant(args.variant)
     weights = [shard] + [shard.copy() for _ in range(copies - 1)]
@@ -313,7 +317,7 @@ def run_ours(args, world, rank, local):
         orc = COracle()
         y64 = lins[0](x, out_dtype=torch.float64).cpu().numpy()
         ac, sa, za = orc.quantize(x_np.astype(np.float64), ab, 0, 2)
-        want = orc.quantized_linear(ac, ab, sa, za, wc[n_lo:n_hi], wb, sb[n_lo:n_hi], zb[n_lo:n_hi])
+        want = orc.quantized_linear(ac, ab, sa, za, wc, wb, sb, zb)
         y16 = lins[0](x, out_dtype=torch.float16).cpu().numpy()
         parity = bool(np.array_equal(y64, want) and np.array_equal(y16, want.astype(np.float16)))
         if not parity:
@@ -363,20 +367,21 @@ def run_ours(args, world, rank, local):
     # ---- end to end through the public API with host buffers (GraphedLinear:
     # H2D x from pinned host, engine, D2H y into pinned host, every step)
     e2e = None
-    if world == 1:
+    if True:
         gl = [abq.GraphedLinear(lins[i], m) for i in range(min(copies, 64))]
         for g in gl:
             g.x_host.copy_(torch.from_numpy(x_np))
         for i in range(args.warmup):
             gl[i % len(gl)].step()
         torch.cuda.synchronize()
+        barrier(world)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for i in range(args.steps):
             gl[i % len(gl)].step()
         e1.record()
         torch.cuda.synchronize()
-        e_ms = e0.elapsed_time(e1) / args.steps
+        e_ms = max_over_ranks(e0.elapsed_time(e1), world) / args.steps
         # eager (per-call Python API, no graph) for reference
         t0 = time.perf_counter()
         eager_steps = min(args.steps, 2000)
@@ -394,6 +399,35 @@ def run_ours(args, world, rank, local):
                "ms_per_step": round(e_ms, 5), "api": "abq.GraphedLinear.step()",
                "eager_api_ms_per_step": round(eager_ms, 5)}
 
+    # ---- reassembly leg (N > 1): the same step followed by the NCCL all-gather
+    # of the fp16 output slices over NVLink (sharded.gather_columns), captured in
+    # the same kind of CUDA graph; reported beside the compute-only headline.
+    gather = None
+    if world > 1:
+        import torch.distributed as dist
+        buf = torch.empty((world, m, n), dtype=torch.float16, device="cuda")
+
+        def step_gather(i):
+            lins[i](x, out=y, check=False)
+            dist.all_gather_into_tensor(buf, y)
+        try:
+            g_ms, _ = time_graph(torch, step_gather, copies, args.steps, args.warmup, world)
+            how = "CUDA graph (engine step + ncclAllGather)"
+        except Exception as exc:  # graph capture of the collective unavailable: eager loop
+            torch.cuda.synchronize()
+            barrier(world)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for i in range(args.steps):
+                step_gather(i % copies)
+            e1.record()
+            torch.cuda.synchronize()
+            g_ms = max_over_ranks(e0.elapsed_time(e1), world)
+            how = f"eager loop ({type(exc).__name__} capturing the collective)"
+        g_step = g_ms / args.steps
+        gather = {"ms_per_step": round(g_step, 6), "value": round(wbytes_full / (g_step * 1e-3) / 1e9, 1),
+                  "unit": "GB/s", "gather_bytes_per_rank": m * n * 2, "timing": how}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline_sample(m, n_full, k, wb, ab, budget_s=args.cpu_seconds)
@@ -401,15 +435,16 @@ def run_ours(args, world, rank, local):
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 6),
-        "higher_is_better": True, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "int32", "data": "synthetic",
-        "config": {"workload": desc, "m": m, "n": n_full, "k": k, "w_bits": wb, "a_bits": ab,
-                   "parallelism": f"N-sharded x{world}" if world > 1 else "single",
+        "config": {"workload": desc, "m": m, "n": n_full, "n_per_gpu": n, "k": k, "w_bits": wb, "a_bits": ab,
+                   "parallelism": f"N-sharded x{world} (column-parallel)" if world > 1 else "single",
                    "l2": f"rotating {copies} packed-weight copies ({copies * wbytes / 1e6:.0f} MB > 4x L2)",
                    "step": "fp16 x -> ReQuant+BitPack -> plane GEMV -> zero-point+dequant -> fp16 y",
                    "graph": "CUDA graph replay"},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches,
         "launches_per_step": per_step, "clocks": clk, "parity": "bit-exact vs oracle" if parity else None,
+        "allgather": gather,
     }
     if args.sweep and rank == 0:
         line["sweep"] = sweep(abq, torch, world)

@@ -140,8 +140,9 @@ int abq_quantize(const void* x, int x_dtype, size_t rows, size_t cols, const abq
 /* K1: ReQuant + BitPacking of activations, fused: x -> act planes + per-row
  * scale / zero point + code row sums (quantizer.hpp:146-213 -> bitplane.hpp:47-64
  * -> gemm.hpp:256-261).  `codes` may be NULL.  If err_index is non-NULL the
- * call is asynchronous: the first non-finite flat index (or INT64_MAX) is
- * written there; otherwise the call synchronises and reports ValueError. */
+ * call is asynchronous: the first non-finite flat index (or -1, all bits set,
+ * when every element is finite) is written there; otherwise the call
+ * synchronises and reports ValueError. */
 int abq_quant_pack_act(const void* x, int x_dtype, size_t m, size_t k, const abq_quant_spec* spec,
                        uint64_t* planes, double* scales, int32_t* zero_points, int64_t* rowsums,
                        uint8_t* codes, int64_t* err_index, void* stream);

@@ -96,10 +96,11 @@ int run_gemv_imma_fused(const uint32_t* frag, unsigned q, size_t n, size_t k, si
 size_t tc_words(unsigned q, size_t n, size_t k);
 int run_prepack_tc(const uint64_t* planes, unsigned q, size_t n, size_t k, uint32_t* out,
                    cudaStream_t st);
-bool gemm_tc_supported(size_t k, size_t ldk);
-int run_gemm_tc(const uint32_t* wtc, unsigned q, size_t n, size_t k, const uint8_t* act, size_t ldk,
-                size_t m, const EpiParams& e, cudaStream_t st, unsigned long long* bad_word = nullptr,
+bool gemm_tc_supported(size_t k);
+int run_gemm_tc(const uint32_t* wtc, unsigned q, size_t n, size_t k, const uint8_t* act, size_t m,
+                const EpiParams& e, cudaStream_t st, unsigned long long* bad_word = nullptr,
                 unsigned long long* bad_out = nullptr, bool pdl = false);
+int run_tile_codes(const uint8_t* src, size_t m, size_t k, uint8_t* dst, cudaStream_t st);
 int run_act_quant(const void* x, int x_dtype, size_t m, size_t k, int mt, const QuantParams& qp,
                   uint32_t* out, int row_ld, double* s_a, int32_t* z_a, long long* rowsum,
                   unsigned long long* bad_word, cudaStream_t st);
@@ -111,7 +112,7 @@ static bool use_imma(const abq_weights* w, size_t m, size_t k) {
 }
 // prefill GEMM on tcgen05: weights prepacked (tc planes), M >= 9 tokens
 static bool use_tc(const abq_weights* w, size_t m, size_t k, bool wide) {
-  return w->tc != nullptr && m >= 9 && !wide && gemm_tc_supported(k, k) &&
+  return w->tc != nullptr && m >= 9 && !wide && gemm_tc_supported(k) &&
          g_gemv_variant != ABQ_GEMV_POPC;
 }
 
@@ -197,14 +198,17 @@ static void add_stats(abq_gemm_stats* stats, const abq_tile_config& t, size_t m,
 }
 
 // tcgen05 GEMM from packed activation planes: recombine the activation planes
-// to u8 codes (unpack kernel) and, when no tc-layout weights are resident,
-// re-lay the ABQP weight planes out for the GEMM, in stream-ordered scratch.
+// to u8 codes (unpack kernel), tile them into the GEMM operand layout and,
+// when no tc-layout weights are resident, re-lay the ABQP weight planes out
+// for the GEMM, in stream-ordered scratch.
 static int gemm_tc_from_planes(const uint64_t* a, unsigned p, size_t m, const uint64_t* w_planes,
                                const uint32_t* wtc, unsigned q, size_t n, size_t k,
                                const EpiParams& e, cudaStream_t s) {
   uint8_t* codes = nullptr;
-  ABQ_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&codes), m * k, s));
+  ABQ_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&codes), m * k + tc_act_bytes(m, k), s));
+  uint8_t* tiled = codes + m * k;  // 16-B aligned: k % 16 == 0
   int st = run_unpack(a, p, m, k, codes, s);
+  if (!st) st = run_tile_codes(codes, m, k, tiled, s);
   uint32_t* tmp = nullptr;
   if (!st && !wtc) {
     cudaError_t err = cudaMallocAsync(reinterpret_cast<void**>(&tmp), tc_words(q, n, k) * 4, s);
@@ -212,7 +216,7 @@ static int gemm_tc_from_planes(const uint64_t* a, unsigned p, size_t m, const ui
     if (!st) st = run_prepack_tc(w_planes, q, n, k, tmp, s);
     wtc = tmp;
   }
-  if (!st) st = run_gemm_tc(wtc, q, n, k, codes, k, m, e, s);
+  if (!st) st = run_gemm_tc(wtc, q, n, k, tiled, m, e, s);
   cudaFreeAsync(codes, s);
   if (tmp) cudaFreeAsync(tmp, s);
   return st;
@@ -379,7 +383,7 @@ static int gemm_common(const char* name, const uint64_t* a, unsigned p, size_t m
   if (m * n > 0 && a_k == 0) {
     // K == 0: every sum is empty
     ABQ_CUDA_TRY(cudaMemsetAsync(out, 0, m * n * (wide ? 8 : 4), as_stream(stream)));
-  } else if (m >= 16 && !wide && gemm_tc_supported(a_k, a_k) && g_gemv_variant != ABQ_GEMV_POPC) {
+  } else if (m >= 16 && !wide && gemm_tc_supported(a_k) && g_gemv_variant != ABQ_GEMV_POPC) {
     // prefill-shaped: recombined planes on tcgen05 (weights re-laid out per call)
     st = gemm_tc_from_planes(a, p, m, bt, nullptr, q, n, a_k, raw_epi(out, n, wide), as_stream(stream));
     if (st) return st;
@@ -517,9 +521,10 @@ static size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 
 size_t abq_linear_workspace_bytes(size_t m, size_t n, size_t k, unsigned act_planes) {
   // [gacc + gcnt for the stream-K decode GEMV][act planes][s_a][z_a][rowsum_a][range 256 B]
-  // [u8 act codes m x k for the tcgen05 GEMM]
+  // [tiled u8 act codes for the tcgen05 GEMM][row-major u8 codes m x k]
   return align256(imma_ws_bytes(n, k)) + align256(size_t(act_planes) * m * wpr_of(k) * 8) +
-         align256(m * 8) + align256(m * 4) + align256(m * 8) + 256 + align256(m * k);
+         align256(m * 8) + align256(m * 4) + align256(m * 8) + 256 + align256(tc_act_bytes(m, k)) +
+         align256(m * k);
 }
 
 int abq_linear(const void* x, int x_dtype, size_t m, size_t k, const abq_quant_spec* act_spec,
@@ -572,16 +577,19 @@ int abq_linear(const void* x, int x_dtype, size_t m, size_t k, const abq_quant_s
     if (st) return st;
   } else if (use_tc(w, m, k, !fits_int32_host(p, w->q, k))) {
     // ReQuant straight to u8 codes (K1), then the tcgen05 GEMM with the fused epilogue
-    uint8_t* codes = reinterpret_cast<uint8_t*>(range + 32);
+    uint8_t* codes = reinterpret_cast<uint8_t*>(range + 32);  // tiled operand
+    uint8_t* rowmajor = codes + align256(tc_act_bytes(m, k));
     unsigned long long* bad_word = range + 2;  // zero-filled workspace word
     // per-token (or few-token per-tensor) ReQuant: one CTA per token, PDL into the GEMM
     const bool fast_k1 = act_spec->granularity != ABQ_PER_TENSOR || m <= 8;
     if (fast_k1) {
       st = run_act_quant(x, x_dtype, m, k, 1, params_of(*act_spec), reinterpret_cast<uint32_t*>(codes),
-                         static_cast<int>(k), sa, za, reinterpret_cast<long long*>(ra), bad_word, s);
+                         tc_act_groups(static_cast<long long>(m)), sa, za, reinterpret_cast<long long*>(ra),
+                         bad_word, s);
     } else {
-      st = run_quantize(x, x_dtype, m, k, params_of(*act_spec), nullptr, nullptr, codes, nullptr, p, sa,
+      st = run_quantize(x, x_dtype, m, k, params_of(*act_spec), nullptr, nullptr, rowmajor, nullptr, p, sa,
                         za, ra, bad, range, s);
+      if (!st) st = run_tile_codes(rowmajor, m, k, codes, s);
     }
     if (st) return st;
     EpiParams e{};
@@ -599,7 +607,7 @@ int abq_linear(const void* x, int x_dtype, size_t m, size_t k, const abq_quant_s
     e.zb_stride = w->per_tensor ? 0 : 1;
     e.colsum_b = w->colsums;
     e.k = static_cast<long long>(k);
-    st = run_gemm_tc(w->tc, w->q, w->n, k, codes, k, m, e, s, fast_k1 ? bad_word : nullptr,
+    st = run_gemm_tc(w->tc, w->q, w->n, k, codes, m, e, s, fast_k1 ? bad_word : nullptr,
                      fast_k1 ? bad : nullptr, fast_k1);
     if (st) return st;
   } else {

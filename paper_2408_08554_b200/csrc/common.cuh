@@ -41,6 +41,51 @@ int num_sms();
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 inline size_t wpr_of(size_t cols) { return (cols + 63) / 64; }
 
+// "Code slices": the prepacked weight layouts store the q-bit weight codes
+// split into power-of-two-wide slices (the binary decomposition of q, widest
+// first: 7 = 4 + 2 + 1), slice i holding code bits [slice_off(q,i),
+// slice_off + slice_width).  A w-bit slice packs 32/w fields per u32 word as
+// (8/w) groups of 4 byte lanes -- bits [8b + w*s, 8b + w*s + w) -- so the
+// kernels widen it to byte codes with one shift and one mask per group,
+// ((x >> w*s) & ((2^w - 1) * 0x01010101)), instead of one shift + merge per
+// bit plane.  Same byte count as the ABQP planes; q = 1 is exactly a plane.
+__host__ __device__ constexpr int slice_count(int q) { return (q & 1) + ((q >> 1) & 1) + ((q >> 2) & 1) + (q >> 3); }
+__host__ __device__ constexpr int slice_width(int q, int i) {
+  int seen = 0;
+  for (int b = 3; b >= 0; --b)
+    if (q & (1 << b)) {
+      if (seen == i) return 1 << b;
+      ++seen;
+    }
+  return 0;
+}
+__host__ __device__ constexpr int slice_off(int q, int i) {
+  int off = 0;
+  for (int j = 0; j < i; ++j) off += slice_width(q, j);
+  return off;
+}
+// slice holding code bit `bit`
+__host__ __device__ constexpr int slice_of_bit(int q, int bit) {
+  int i = 0;
+  while (slice_off(q, i) + slice_width(q, i) <= bit) ++i;
+  return i;
+}
+
+// u8 activation codes of the tcgen05 GEMM, "tiled": [k-block of 128][token
+// group of 8][16-k chunk][token % 8][16 B].  A tile of TT tokens x 128 k is
+// one contiguous TT * 128-byte run (one TMA bulk copy) that is directly a UMMA
+// K-major no-swizzle operand (core matrices 8 tokens x 16 B).  Groups are
+// allocated for m rounded up to 256 tokens so that every token tile is in
+// bounds; codes past K (to the 128 multiple) are zero.
+__host__ __device__ inline int tc_act_groups(long long m) { return static_cast<int>(((m + 255) / 256) * 32); }
+__host__ __device__ inline size_t tc_act_offset(long long tok, long long k, int groups) {
+  return ((static_cast<size_t>(k >> 7) * groups + static_cast<size_t>(tok >> 3)) * 8 + ((k >> 4) & 7)) * 128 +
+         (tok & 7) * 16 + (k & 15);
+}
+inline size_t tc_act_bytes(size_t m, size_t k) {
+  return static_cast<size_t>(tc_act_groups(static_cast<long long>(m))) * 8 * ((k + 127) / 128) * 128;
+}
+
 // QuantSpec as the kernels see it (quantizer.hpp:37-71)
 struct QuantParams {
   unsigned bits;

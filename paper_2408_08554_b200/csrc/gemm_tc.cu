@@ -5,26 +5,33 @@
 // popc(A_s & W_t) over p x q binary plane pairs.  sm_100a has no binary
 // tensor-core instruction (b1 mma.sync is emulated with 8 IMMA + ~100 ALU
 // ops per m16n8k256; measured 700 bit-MAC/clk/SM vs ~8192
-// int8 MAC/clk/SM for tcgen05), so this kernel recombines the q weight planes
-// into u8 codes on the fly in shared memory and issues one exact u8 x u8 ->
-// s32 UMMA per 32-k step:   acc[i][j] = sum_k a_ik * (sum_t 2^t W_t[j][k]).
+// int8 MAC/clk/SM for tcgen05), so the q weight bits are recombined into u8
+// codes and one exact u8 x u8 -> s32 UMMA is issued per 32-k step:
+//     acc[j][i] = sum_k (sum_t 2^t W_t[j][k]) * a_ik.
 //
-// Per CTA: 128 output channels (UMMA M) x TT tokens (UMMA N), K streamed in
-// 128-wide stages through a 3-4 deep shared-memory ring:
-//   * all 256 threads: load this stage's packed weight planes (one coalesced
-//     8-byte load per plane per thread), rebuild 64 u8 codes per thread with
-//     shift / mask / merge, store them in the UMMA canonical K-major
-//     (no-swizzle) layout; cp.async the u8 activation codes of the stage;
-//   * thread 0: waits for the stage, issues 4 x tcgen05.mma (K = 32 each) into
-//     the TMEM accumulator and tcgen05.commit's the stage back to the
-//     producers;
-//   * epilogue: tcgen05.ld (32x32b) -> registers -> fused zero-point
-//     correction + dequant (gemm.hpp:235-254, 292-306) -> global.
-// Weight layout ("tc planes", prepack_tc_kernel): [row-tile 128][k-block 128]
-// [plane][row][4 x u32]; word j of a (row, plane) holds k = 32j..32j+31 of the
-// block with bit (8b + c) <-> k = 32j + 4c + b, so code register c is
-// sum_t ((w_t >> c) & 0x01010101) << t.  Same bits as ABQP, rows padded to
-// 128 and K to 128 with zeros.
+// Per CTA: 128 output channels (UMMA M) x TT tokens (UMMA N); K streamed in
+// 128-wide stages through an S-deep shared-memory ring.  Warp roles:
+//   * warp 0 (one thread): TMA producer -- per stage one 1-D bulk copy of the
+//     packed weight codes (q x 2 KB) and one of the activation tile (TT x 128
+//     bytes, already in the UMMA operand layout, see tc_act_offset); weights
+//     of the first S stages are requested before griddepcontrol.wait, i.e.
+//     while the ReQuant kernel is still running;
+//   * warps 4-7 (q < 8): widen the packed code slices (common.cuh) of one
+//     weight row each to u8 codes (q = 4: 1.5 ALU ops per 4 codes) and store
+//     them as the UMMA A operand; q = 8 weights are copied by TMA straight
+//     into the operand buffer;
+//   * warp 1 (one thread): waits for a stage, issues 4 x tcgen05.mma (K = 32)
+//     into the TMEM accumulator, tcgen05.commit's the stage back to the
+//     producer;
+//   * epilogue, all warps: tcgen05.ld (32x32b) -> fused zero-point correction
+//     + dequant (gemm.hpp:235-254, 292-306) -> global.
+//
+// Weight layout ("tc code slices", prepack_tc_kernel): [row-tile 128][k-block
+// 128][q][row 128][4 x u32]: row r's 4q words hold its 128 codes of the block
+// as code slices; widened register o = 4 kc + u holds k = 16 kc + 4 u + b in
+// byte b, stored to the operand at (kc * 128 + r) * 16 (core matrices 8 rows x
+// 16 B: LBO 2048 B along K, SBO 128 B along M).  For q = 8 the packed words
+// ARE that operand.
 #include "common.cuh"
 
 namespace abq_dev {
@@ -34,34 +41,52 @@ constexpr int kTcK = 128;
 constexpr int kTcThreads = 256;
 
 // ---------------------------------------------------------------------------
-// prepack: ABQP [q][n][wpr] -> tc planes
+// prepack: ABQP [q][n][wpr] -> tc code slices
 // ---------------------------------------------------------------------------
 __global__ void prepack_tc_kernel(const uint64_t* __restrict__ planes, int q, int n, int k, int wpr,
                                   int rowtiles, int kblocks, uint32_t* __restrict__ out) {
   const size_t total = static_cast<size_t>(rowtiles) * kblocks * q * kTcM * 4;
   for (size_t idx = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; idx < total;
        idx += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    const int j = static_cast<int>(idx & 3);
     const int row = static_cast<int>((idx >> 2) & (kTcM - 1));
     size_t rest = idx >> 9;
-    const int t = static_cast<int>(rest % q);
+    const int J = static_cast<int>(rest % q) * 4 + static_cast<int>(idx & 3);
     rest /= q;
     const int kb = static_cast<int>(rest % kblocks);
     const int rt = static_cast<int>(rest / kblocks);
     const int grow = rt * kTcM + row;
-    const int kbase = kb * kTcK + 32 * j;
+    const int si = slice_of_bit(q, J >> 2), sw = slice_width(q, si), so = slice_off(q, si);
+    const int j = J - 4 * so;
     uint32_t w = 0;
     if (grow < n) {
-      const uint64_t* src = planes + (static_cast<size_t>(t) * n + grow) * wpr;
-#pragma unroll
-      for (int c = 0; c < 8; ++c)
-#pragma unroll
+      for (int s = 0; s < 8 / sw; ++s) {
+        const int o = s * 4 * sw + j;  // widened register: k = 16 (o >> 2) + 4 (o & 3) + b
         for (int b = 0; b < 4; ++b) {
-          const int kk = kbase + 4 * c + b;
-          if (kk < k) w |= static_cast<uint32_t>((src[kk >> 6] >> (kk & 63)) & 1ull) << (8 * b + c);
+          const int kk = kb * kTcK + 16 * (o >> 2) + 4 * (o & 3) + b;
+          if (kk >= k) continue;
+          for (int e = 0; e < sw; ++e) {
+            const uint64_t* src = planes + (static_cast<size_t>(so + e) * n + grow) * wpr;
+            w |= static_cast<uint32_t>((src[kk >> 6] >> (kk & 63)) & 1ull) << (8 * b + sw * s + e);
+          }
         }
+      }
     }
     out[idx] = w;
+  }
+}
+
+// row-major u8 codes [m][k] (k % 16 == 0, 16-B aligned rows) -> tiled operand
+// layout; zero codes past k.  One thread per 16-byte run.
+__global__ void tile_codes_kernel(const uint8_t* __restrict__ src, int m, int k, int groups,
+                                  uint8_t* __restrict__ dst) {
+  const int kp = (k + kTcK - 1) / kTcK * kTcK;
+  const size_t runs = static_cast<size_t>(m) * (kp / 16);
+  for (size_t idx = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; idx < runs;
+       idx += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int tok = static_cast<int>(idx / (kp / 16)), kk = static_cast<int>(idx % (kp / 16)) * 16;
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (kk < k) v = *reinterpret_cast<const uint4*>(src + static_cast<size_t>(tok) * k + kk);
+    *reinterpret_cast<uint4*>(dst + tc_act_offset(tok, kk, groups)) = v;
   }
 }
 
@@ -77,6 +102,10 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
@@ -84,6 +113,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
 __device__ __forceinline__ void fence_async_smem() {
@@ -100,8 +136,9 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
                    smem_u32(bar))
                : "memory");
 }
-// UMMA shared-memory descriptor, K-major, no swizzle (canonical layout
-// ((8,m),2):((16B,SBO),LBO)), version 1 for sm_100.
+// UMMA shared-memory descriptor, K-major, no swizzle: core matrices of 8 rows
+// x 16 B, LBO = byte step between core matrices along K, SBO = along M/N;
+// version 1 (bit 46) for sm_100.
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   return static_cast<uint64_t>((saddr >> 4) & 0x3FFFu) |
          (static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16) |
@@ -117,86 +154,67 @@ __device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t adesc, uint64_
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(mask0), "r"(mask1), "r"(mask2),
       "r"(mask3));
 }
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
-}
-__device__ __forceinline__ uint2 ld_nc_u2(const uint32_t* p) {
-  uint2 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+
+// u8 code register o (k = 16 (o >> 2) + 4 (o & 3) + b in byte b) of one row
+// from its 4Q code-slice words: one shift + one mask-merge per slice.
+template <int Q>
+__device__ __forceinline__ uint32_t widen_row(const uint4 (&w)[Q], int o) {
+  uint32_t r = 0;
+#pragma unroll
+  for (int i = 0; i < slice_count(Q); ++i) {
+    const int sw = slice_width(Q, i), so = slice_off(Q, i);
+    const int J = 4 * so + o % (4 * sw), sh = sw * (o / (4 * sw));
+    const uint4 v = w[J >> 2];
+    const uint32_t x = (J & 3) == 0 ? v.x : (J & 3) == 1 ? v.y : (J & 3) == 2 ? v.z : v.w;
+    const uint32_t m = static_cast<uint32_t>((1u << sw) - 1u) * 0x01010101u;
+    r |= so >= sh ? (x << (so - sh)) & (m << so) : (x >> (sh - so)) & (m << so);
+  }
   return r;
 }
 
-template <int T, int C>
-__device__ __forceinline__ uint32_t plane_to_codes(uint32_t w) {
-  uint32_t x;
-  if constexpr (T >= C)
-    x = w << (T - C);
-  else
-    x = w >> (C - T);
-  return x & (0x01010101u << T);
-}
-
-// 8 code registers (32 codes, k = 4c..4c+3 in register c) from the q plane words
-template <int Q>
-__device__ __forceinline__ void rebuild32(const uint32_t (&w)[Q], uint32_t (&r)[8]) {
-#pragma unroll
-  for (int c = 0; c < 8; ++c) r[c] = 0u;
-  // plane t lands on bit (8 - Q + t): the code scaled by 2^(8-Q), so that most
-  // bit moves are left shifts (IMAD.SHL on the fma pipe) next to the LOP3 merges
-  // on the alu pipe; the accumulator is divided back exactly in the epilogue.
-#define ABQ_PLACE(T)                                                 \
-  if constexpr (Q > T) {                                             \
-    r[0] |= plane_to_codes<8 - Q + T, 0>(w[T]);                      \
-    r[1] |= plane_to_codes<8 - Q + T, 1>(w[T]);                      \
-    r[2] |= plane_to_codes<8 - Q + T, 2>(w[T]);                      \
-    r[3] |= plane_to_codes<8 - Q + T, 3>(w[T]);                      \
-    r[4] |= plane_to_codes<8 - Q + T, 4>(w[T]);                      \
-    r[5] |= plane_to_codes<8 - Q + T, 5>(w[T]);                      \
-    r[6] |= plane_to_codes<8 - Q + T, 6>(w[T]);                      \
-    r[7] |= plane_to_codes<8 - Q + T, 7>(w[T]);                      \
-  }
-  ABQ_PLACE(0)
-  ABQ_PLACE(1)
-  ABQ_PLACE(2)
-  ABQ_PLACE(3)
-  ABQ_PLACE(4)
-  ABQ_PLACE(5)
-  ABQ_PLACE(6)
-  ABQ_PLACE(7)
-#undef ABQ_PLACE
-}
-
 struct TcParams {
-  const uint32_t* wtc;  // tc planes
-  const uint8_t* act;   // u8 activation codes, row stride ldk (multiple of 16, 16B aligned)
-  int q, n, k, m, ldk, rowtiles, kblocks;
+  const uint32_t* wtc;  // tc code slices
+  const uint8_t* act;   // tiled u8 activation codes (tc_act_offset)
+  int q, n, k, m, groups, rowtiles, kblocks;
   EpiParams e;
   unsigned long long* bad_word;  // ReQuant status (~index, 0 = none), published to bad_out
   unsigned long long* bad_out;
-  int pdl;                       // launched as a programmatic dependent of the ReQuant kernel
 };
 
-template <int Q, int TT, int S>
+template <int Q, int TT>
+struct TcShape {
+  static constexpr bool kExpand = Q < 8;
+  static constexpr int kA = kTcM * kTcK;          // u8 operand A (weights), 16 KB
+  static constexpr int kB = TT * kTcK;            // u8 operand B (activations)
+  static constexpr int kW = kExpand ? Q * kTcM * 16 : 0;  // packed slices staging
+  static constexpr int kStage = kA + kB + kW;
+  static constexpr int kS = (200 * 1024) / kStage > 6 ? 6 : (200 * 1024) / kStage;
+  static constexpr int kSmem = kS * kStage + 1024;  // + alignment slack
+};
+
+template <int Q, int TT>
 __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(TcParams P) {
-  constexpr int A_BYTES = kTcM * kTcK;  // 16 KB
-  constexpr int B_BYTES = TT * kTcK;
-  constexpr int STAGE = A_BYTES + B_BYTES;
+  using Sh = TcShape<Q, TT>;
+  constexpr int S = Sh::kS;
   constexpr int TMEM_COLS = TT <= 32 ? 32 : (TT <= 64 ? 64 : (TT <= 128 ? 128 : 256));
-  extern __shared__ __align__(1024) unsigned char smem[];
-  __shared__ __align__(8) uint64_t full_bar[S], empty_bar[S], done_bar;
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t wbar[S], abar[S], rbar[S], ebar[S], done_bar;
   __shared__ uint32_t tmem_base_s;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int rt = blockIdx.x, tok0 = blockIdx.y * TT;
+  const int nkb = P.kblocks;
+  auto a_of = [&](int s) { return smem + s * Sh::kStage; };
+  auto b_of = [&](int s) { return smem + s * Sh::kStage + Sh::kA; };
+  auto w_of = [&](int s) { return smem + s * Sh::kStage + Sh::kA + Sh::kB; };
 
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
-      mbar_init(&full_bar[s], kTcThreads);
-      mbar_init(&empty_bar[s], 1);
+      mbar_init(&wbar[s], 1);
+      mbar_init(&abar[s], 1);
+      mbar_init(&rbar[s], 128);
+      mbar_init(&ebar[s], 1);
     }
     mbar_init(&done_bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -212,106 +230,82 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(TcParams P) {
   tc_fence_after();
   const uint32_t tmem_d = tmem_base_s;
 
-  // instruction descriptor: D=s32, A=B=u8, K-major both, N=TT, M=128
-  const uint32_t idesc = (2u << 4) | (static_cast<uint32_t>(TT >> 3) << 17) | (static_cast<uint32_t>(kTcM >> 4) << 24);
-  const int prow = tid >> 1, phalf = tid & 1;  // producer: weight row, 64-k half
-  const size_t stage_words = static_cast<size_t>(Q) * kTcM * 4;
-
-  // Software pipeline (per thread): the packed weight words of stage kb + DW
-  // and the activation tile of stage kb + DA are requested while stage kb is
-  // rebuilt, so every thread keeps several HBM / L2 round trips in flight.
-  constexpr int DW = 3;                    // weight-word prefetch distance (registers)
-  constexpr int DA = S >= 3 ? S - 2 : 1;   // activation cp.async distance (smem stages)
-  auto issue_act = [&](int j) {            // cp.async of stage j's activations, one group
-    if (j < P.kblocks) {
-      const int sj = j % S;
-      if (j >= S) mbar_wait(&empty_bar[sj], ((j / S) + 1) & 1);
-      unsigned char* b_st = smem + sj * STAGE + A_BYTES;
-      for (int piece = tid; piece < TT * 8; piece += kTcThreads) {
-        const int token = piece >> 3, kc = piece & 7;
-        const int tk = tok0 + token;
-        const int kk = j * kTcK + kc * 16;
-        const bool ok = tk < P.m && kk < P.k;
-        const uint8_t* src = ok ? P.act + static_cast<size_t>(tk) * P.ldk + kk : P.act;
-        cp_async16(smem_u32(b_st + (kc * (TT / 8) + (token >> 3)) * 128 + (token & 7) * 16), src,
-                   ok ? 16u : 0u);
-      }
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-  uint32_t wring[DW + 1][2][Q];
-  auto issue_w = [&](int j, uint32_t (&dst)[2][Q]) {
-    if (j < P.kblocks) {
-      const uint32_t* wsrc = P.wtc + (static_cast<size_t>(rt) * P.kblocks + j) * stage_words;
-#pragma unroll
-      for (int t = 0; t < Q; ++t) {
-        const uint2 v = ld_nc_u2(wsrc + (t * kTcM + prow) * 4 + 2 * phalf);
-        dst[0][t] = v.x;
-        dst[1][t] = v.y;
-      }
-    }
-  };
-  // weights do not depend on the preceding ReQuant kernel: start them first,
-  // then wait for its codes (programmatic dependent launch; a no-op otherwise)
-#pragma unroll
-  for (int j = 0; j < DW; ++j) issue_w(j, wring[j]);
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  if (P.bad_out && blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) {
-    const unsigned long long w = *P.bad_word;
-    *P.bad_out = w ? ~w : ~0ull;
-    *P.bad_word = 0ull;
-  }
-#pragma unroll
-  for (int j = 0; j < DA; ++j) issue_act(j);
-
-  // one copy of the stage body (compact hot loop); the weight ring shifts by one stage
-  for (int kb = 0; kb < P.kblocks; ++kb) {
-    const int s = kb % S;
-    const uint32_t use = static_cast<uint32_t>(kb / S);
-    issue_act(kb + DA);  // also guarantees stage s is free (waited DA stages ago)
-    uint32_t wn[2][Q];
-    issue_w(kb + DW, wn);
-    unsigned char* a_st = smem + s * STAGE;
-    unsigned char* b_st = a_st + A_BYTES;
-    {
-      uint32_t r0[8], r1[8];
-      rebuild32<Q>(wring[0][0], r0);
-      rebuild32<Q>(wring[0][1], r1);
-      const int kc0 = 4 * phalf;  // 16-byte k chunk index of r0[0..3]
-      auto sts = [&](int kc, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
-        *reinterpret_cast<uint4*>(a_st + (kc * (kTcM / 8) + (prow >> 3)) * 128 + (prow & 7) * 16) =
-            make_uint4(x, y, z, w);
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---- TMA producer
+      constexpr uint32_t WB = Sh::kExpand ? Sh::kW : Sh::kA;
+      const unsigned char* wsrc = reinterpret_cast<const unsigned char*>(P.wtc) +
+                                  static_cast<size_t>(rt) * nkb * WB;
+      const unsigned char* asrc = P.act + static_cast<size_t>(tok0 / 8) * 1024;
+      auto issue_w = [&](int kb) {
+        const int s = kb % S;
+        mbar_expect_tx(&wbar[s], WB);
+        bulk_g2s(Sh::kExpand ? w_of(s) : a_of(s), wsrc + static_cast<size_t>(kb) * WB, WB, &wbar[s]);
       };
-      sts(kc0 + 0, r0[0], r0[1], r0[2], r0[3]);
-      sts(kc0 + 1, r0[4], r0[5], r0[6], r0[7]);
-      sts(kc0 + 2, r1[0], r1[1], r1[2], r1[3]);
-      sts(kc0 + 3, r1[4], r1[5], r1[6], r1[7]);
-    }
-#pragma unroll
-    for (int d = 0; d < DW; ++d)
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-#pragma unroll
-        for (int t = 0; t < Q; ++t) wring[d][h][t] = d + 1 < DW ? wring[d + 1][h][t] : wn[h][t];
-    // this thread's activation pieces of stage kb have landed (DA newer groups may still fly)
-    asm volatile("cp.async.wait_group %0;" ::"n"(DA) : "memory");
-    fence_async_smem();
-    mbar_arrive(&full_bar[s]);
-    if (tid == 0) {
-      mbar_wait(&full_bar[s], use & 1);
-      tc_fence_after();
-      const uint32_t a_addr = smem_u32(a_st), b_addr = smem_u32(b_st);
-#pragma unroll
-      for (int j = 0; j < kTcK / 32; ++j) {
-        const uint64_t ad = umma_desc(a_addr + j * 2 * (kTcM / 8) * 128, (kTcM / 8) * 128, 128);
-        const uint64_t bd = umma_desc(b_addr + j * 2 * (TT / 8) * 128, (TT / 8) * 128, 128);
-        umma_i8(tmem_d, ad, bd, idesc, (kb | j) != 0 ? 1u : 0u);
+      auto issue_a = [&](int kb) {
+        const int s = kb % S;
+        mbar_expect_tx(&abar[s], Sh::kB);
+        bulk_g2s(b_of(s), asrc + static_cast<size_t>(kb) * P.groups * 1024, Sh::kB, &abar[s]);
+      };
+      const int pre = nkb < S ? nkb : S;
+      for (int kb = 0; kb < pre; ++kb) issue_w(kb);
+      // the weights do not depend on the preceding ReQuant kernel; its codes do
+      // (programmatic dependent launch; a no-op otherwise)
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      if (P.bad_out && blockIdx.x == 0 && blockIdx.y == 0) {
+        const unsigned long long w = *P.bad_word;
+        *P.bad_out = w ? ~w : ~0ull;
+        *P.bad_word = 0ull;
       }
-      tc_commit(&empty_bar[s]);
-      if (kb == P.kblocks - 1) tc_commit(&done_bar);
+      for (int kb = 0; kb < pre; ++kb) issue_a(kb);
+      for (int kb = S; kb < nkb; ++kb) {
+        mbar_wait(&ebar[kb % S], ((kb / S) - 1) & 1);  // MMA of kb - S done with the stage
+        issue_w(kb);
+        issue_a(kb);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---- MMA issuer: D=s32, A=B=u8, both K-major, N=TT, M=128
+      const uint32_t idesc = (2u << 4) | (static_cast<uint32_t>(TT >> 3) << 17) |
+                             (static_cast<uint32_t>(kTcM >> 4) << 24);
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % S;
+        const uint32_t ph = static_cast<uint32_t>(kb / S) & 1u;
+        mbar_wait(Sh::kExpand ? &rbar[s] : &wbar[s], ph);
+        mbar_wait(&abar[s], ph);
+        tc_fence_after();
+        const uint32_t a_addr = smem_u32(a_of(s)), b_addr = smem_u32(b_of(s));
+#pragma unroll
+        for (int j = 0; j < kTcK / 32; ++j) {
+          const uint64_t ad = umma_desc(a_addr + j * 2 * (kTcM * 16), kTcM * 16, 128);
+          const uint64_t bd = umma_desc(b_addr + j * 2 * 128, 128, 1024);
+          umma_i8(tmem_d, ad, bd, idesc, (kb | j) != 0 ? 1u : 0u);
+        }
+        tc_commit(&ebar[s]);
+      }
+      tc_commit(&done_bar);
+    }
+  } else if (Sh::kExpand && warp >= 4) {
+    // ---- widen packed code slices of row r into the A operand
+    const int r = tid - 128;
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % S;
+      mbar_wait(&wbar[s], static_cast<uint32_t>(kb / S) & 1u);
+      const uint4* wsl = reinterpret_cast<const uint4*>(w_of(s)) + r;
+      uint4 w[Q > 0 ? Q : 1];
+#pragma unroll
+      for (int t = 0; t < Q; ++t) w[t] = wsl[t * kTcM];
+      uint4* adst = reinterpret_cast<uint4*>(a_of(s)) + r;
+#pragma unroll
+      for (int kc = 0; kc < 8; ++kc)
+        adst[kc * kTcM] = make_uint4(widen_row<Q>(w, 4 * kc), widen_row<Q>(w, 4 * kc + 1),
+                                     widen_row<Q>(w, 4 * kc + 2), widen_row<Q>(w, 4 * kc + 3));
+      fence_async_smem();  // generic-proxy stores -> visible to the tensor core
+      mbar_arrive(&rbar[s]);
     }
   }
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncwarp();
 
   // ---- epilogue: TMEM -> registers -> zero-point correction + dequant.  A
   // thread owns one output channel (TMEM lane) and half of the token columns,
@@ -344,7 +338,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(TcParams P) {
     for (int i = 0; i < 8; ++i) {
       const int tk = tok0 + c0 + i;
       if (tk >= P.m) continue;
-      const long long acc = static_cast<long long>(static_cast<int32_t>(v[i]) >> (8 - Q));
+      // the true sum is < 2^32 (K <= 65536, codes <= 255): exact as unsigned
+      const long long acc = static_cast<long long>(v[i]);
       const long long o = static_cast<long long>(tk) * E.ldo + ch;
       if (raw) {
         if (E.mode == EPI_ACC_I32) static_cast<int32_t*>(E.out)[o] = static_cast<int32_t>(acc);
@@ -390,26 +385,35 @@ int run_prepack_tc(const uint64_t* planes, unsigned q, size_t n, size_t k, uint3
   return ABQ_OK;
 }
 
+// row-major codes [m][k] -> tiled operand layout (tc_act_bytes(m, k) bytes)
+int run_tile_codes(const uint8_t* src, size_t m, size_t k, uint8_t* dst, cudaStream_t st) {
+  if (m == 0) return ABQ_OK;
+  const size_t runs = m * ((k + kTcK - 1) / kTcK) * (kTcK / 16);
+  size_t grid = (runs + 255) / 256;
+  if (grid > static_cast<size_t>(num_sms()) * 16) grid = num_sms() * 16;
+  tile_codes_kernel<<<static_cast<unsigned>(grid), 256, 0, st>>>(src, static_cast<int>(m), static_cast<int>(k),
+                                                                  tc_act_groups(static_cast<long long>(m)), dst);
+  ABQ_LAUNCHED();
+  return ABQ_OK;
+}
+
 template <int Q, int TT>
-static int launch_tc(const TcParams& P, cudaStream_t st) {
-  constexpr int STAGE = kTcM * kTcK + TT * kTcK;
-  constexpr int S = (200 * 1024) / STAGE >= 4 ? 4 : ((200 * 1024) / STAGE >= 3 ? 3 : 2);
-  auto kern = gemm_tc_kernel<Q, TT, S>;
-  const size_t smem = static_cast<size_t>(S) * STAGE;
-  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
+static int launch_tc(const TcParams& P, bool pdl, cudaStream_t st) {
+  using Sh = TcShape<Q, TT>;
+  auto kern = gemm_tc_kernel<Q, TT>;
+  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Sh::kSmem);
   if (err != cudaSuccess) return fail(ABQ_ERR_CUDA, "gemm_tc: smem attribute: %s", cudaGetErrorString(err));
   dim3 grid(static_cast<unsigned>(P.rowtiles), static_cast<unsigned>((P.m + TT - 1) / TT));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(kTcThreads);
-  cfg.dynamicSmemBytes = smem;
+  cfg.dynamicSmemBytes = Sh::kSmem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = P.pdl ? 1 : 0;
+  cfg.numAttrs = pdl ? 1 : 0;
   err = cudaLaunchKernelEx(&cfg, kern, P);
   if (err != cudaSuccess) return fail(ABQ_ERR_CUDA, "gemm_tc: launch: %s", cudaGetErrorString(err));
   ABQ_LAUNCHED();
@@ -417,47 +421,44 @@ static int launch_tc(const TcParams& P, cudaStream_t st) {
 }
 
 template <int Q>
-static int launch_tt(const TcParams& P, cudaStream_t st) {
-  if (P.m <= 16) return launch_tc<Q, 16>(P, st);
-  if (P.m <= 32) return launch_tc<Q, 32>(P, st);
-  if (P.m <= 64) return launch_tc<Q, 64>(P, st);
-  if (P.m <= 128) return launch_tc<Q, 128>(P, st);
-  return launch_tc<Q, 256>(P, st);
+static int launch_tt(const TcParams& P, bool pdl, cudaStream_t st) {
+  if (P.m <= 16) return launch_tc<Q, 16>(P, pdl, st);
+  if (P.m <= 32) return launch_tc<Q, 32>(P, pdl, st);
+  if (P.m <= 64) return launch_tc<Q, 64>(P, pdl, st);
+  if (P.m <= 128) return launch_tc<Q, 128>(P, pdl, st);
+  return launch_tc<Q, 256>(P, pdl, st);
 }
 
-// act: u8 codes [m][ldk]; requires k % 16 == 0, ldk % 16 == 0 and a 16-B aligned act.
-// K <= 32768 keeps the scaled-code accumulator (255 * 255 * K) inside s32
-bool gemm_tc_supported(size_t k, size_t ldk) {
-  return k > 0 && k <= 32768 && k % 16 == 0 && ldk % 16 == 0;
-}
+// k % 16 == 0 (16-byte code runs); the unsigned accumulator is exact to K = 65536
+bool gemm_tc_supported(size_t k) { return k > 0 && k <= 65536 && k % 16 == 0; }
 
-int run_gemm_tc(const uint32_t* wtc, unsigned q, size_t n, size_t k, const uint8_t* act, size_t ldk,
-                size_t m, const EpiParams& e, cudaStream_t st, unsigned long long* bad_word,
+// act: tiled u8 codes (tc_act_offset, groups = tc_act_groups(m)), 16-B aligned
+int run_gemm_tc(const uint32_t* wtc, unsigned q, size_t n, size_t k, const uint8_t* act, size_t m,
+                const EpiParams& e, cudaStream_t st, unsigned long long* bad_word,
                 unsigned long long* bad_out, bool pdl) {
   if (m == 0 || n == 0) return ABQ_OK;
   TcParams P{};
   P.bad_word = bad_word;
   P.bad_out = bad_out;
-  P.pdl = pdl ? 1 : 0;
   P.wtc = wtc;
   P.act = act;
   P.q = static_cast<int>(q);
   P.n = static_cast<int>(n);
   P.k = static_cast<int>(k);
   P.m = static_cast<int>(m);
-  P.ldk = static_cast<int>(ldk);
+  P.groups = tc_act_groups(static_cast<long long>(m));
   P.rowtiles = static_cast<int>((n + kTcM - 1) / kTcM);
   P.kblocks = static_cast<int>((k + kTcK - 1) / kTcK);
   P.e = e;
   switch (q) {
-    case 1: return launch_tt<1>(P, st);
-    case 2: return launch_tt<2>(P, st);
-    case 3: return launch_tt<3>(P, st);
-    case 4: return launch_tt<4>(P, st);
-    case 5: return launch_tt<5>(P, st);
-    case 6: return launch_tt<6>(P, st);
-    case 7: return launch_tt<7>(P, st);
-    default: return launch_tt<8>(P, st);
+    case 1: return launch_tt<1>(P, pdl, st);
+    case 2: return launch_tt<2>(P, pdl, st);
+    case 3: return launch_tt<3>(P, pdl, st);
+    case 4: return launch_tt<4>(P, pdl, st);
+    case 5: return launch_tt<5>(P, pdl, st);
+    case 6: return launch_tt<6>(P, pdl, st);
+    case 7: return launch_tt<7>(P, pdl, st);
+    default: return launch_tt<8>(P, pdl, st);
   }
 }
 

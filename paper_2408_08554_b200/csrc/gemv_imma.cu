@@ -1,30 +1,31 @@
 // gemv_imma.cu -- K2 "recombination" variant: decode GEMV (M <= 8 tokens per
-// token block) that feeds the weight BIT PLANES to the int8 tensor pipe, one
-// plane at a time, against u8 activation codes.  sm_100a.
+// token block) that feeds the q-bit weight codes to the int8 tensor pipe
+// against u8 activation codes.  sm_100a.
 //
 // Why (measured in profiles/r01_microbench_pipes.txt): on
 // sm_100a POPC issues at 16/clk/SM, so the AND+popcount decomposition of a
 // p-bit activation x q-bit weight product needs p POPCs per 32 weight-plane
 // bits -- 36% of HBM at p=8.  The int8 tensor pipe (legacy IMMA m16n8k32,
-// ~1950 MAC/clk/SM) is idle in that kernel.  Here each 32-bit weight-plane
-// word is expanded to 0/128 bytes with one shift + one AND (fma and alu pipes)
-// and multiplied on the tensor pipe against the activation codes:
+// ~1950 MAC/clk/SM) is idle in that kernel.  Here the weight bit planes are
+// recombined into u8 codes and multiplied on the tensor pipe:
 //
-//   acc = sum_t 2^t * sum_k a_k * W_t[k]        (paper Eq. 11 with the
-//                                                 activation planes recombined)
+//   acc = sum_k a_k * (sum_t 2^t W_t[k])       (paper Eq. 11 with both sides'
+//                                                planes recombined)
 //
 // which is the same exact unsigned code product as the reference's
-// gemm_plane_rows (include/abq/gemm.hpp:94-146).  Accumulation is exact:
-// every IMMA partial is an integer < 2^31 and planes are combined after the
-// 2^-7 scale is divided out exactly.
+// gemm_plane_rows (include/abq/gemm.hpp:94-146).  Accumulation is exact: the
+// per-row-tile sum is < 2^32 for K <= 65536 and read back as unsigned.
 //
-// Weight layout ("fragment-major planes", built once by prepack_frag_kernel
-// from the ABQP planes): [row-tile of 16][k-block of 256][plane][lane][4 x u32].
-// Lane l = (g = l/4, tig = l%4) holds exactly the bits its IMMA A fragments
-// need for the 8 k32 chunks of the block; bit (8b + c) of word u is element
-// (row g + 8*(u&1), k = 32c + 16*(u>>1) + 4*tig + b), so chunk c's register
-// is (w << (7 - c)) & 0x80808080.  Same byte count as ABQP; each (tile, block)
-// "unit" is q x 512 contiguous bytes.
+// Weight layout (built once by prepack_frag_kernel from the ABQP planes):
+// [row-tile of 16][k-block of 256][q][lane][4 x u32] holding the codes as
+// "code slices" (common.cuh): the binary decomposition of q into slices of
+// width 8/4/2/1, each packing its code bits in byte lanes so that widening
+// to the u8 A register o = 4c + u (chunk c, register u: element row g + 8*(u&1),
+// k = 32c + 16*(u>>1) + 4*tig + b in byte b) is one shift + one mask per slice
+// (q = 4: 1.5 ALU ops per register; q = 8: none).  Same byte count as ABQP;
+// each (tile, block) "unit" is q x 512 contiguous bytes.
+// (profiles/r01_microbench_gemv_body.txt: the earlier per-plane merge needed
+// 8 ALU ops per register and capped the loop at ~19 B/clk/SM.)
 //
 // Pipeline (one persistent CTA of 16 warps per SM):
 //   * work split, stream-K: the (row-tile, k-block) units are divided evenly
@@ -49,33 +50,38 @@ constexpr int kRowTile = 16;
 constexpr int kKBlock = 256;
 
 // ---------------------------------------------------------------------------
-// prepack: ABQP [q][n][wpr] -> fragment-major [rt][kb][q][lane][4]
+// prepack: ABQP [q][n][wpr] -> fragment-major code slices [rt][kb][q][lane][4]
+// (the lane's 4q words; word J belongs to the slice holding code bit J / 4)
 // ---------------------------------------------------------------------------
 __global__ void prepack_frag_kernel(const uint64_t* __restrict__ planes, int q, int n, int k, int wpr,
                                     int rowtiles, int kblocks, uint32_t* __restrict__ frag) {
   const size_t total = static_cast<size_t>(rowtiles) * kblocks * q * 128;
   for (size_t idx = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; idx < total;
        idx += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    const int u = static_cast<int>(idx & 3);
+    // word J (0..4q-1) of this lane; J / 4 is a code bit of slice `si`
     const int lane = static_cast<int>((idx >> 2) & 31);
     size_t rest = idx >> 7;
-    const int t = static_cast<int>(rest % q);
+    const int J = static_cast<int>(rest % q) * 4 + static_cast<int>(idx & 3);
     rest /= q;
     const int kb = static_cast<int>(rest % kblocks);
     const int rt = static_cast<int>(rest / kblocks);
+    const int si = slice_of_bit(q, J >> 2), sw = slice_width(q, si), so = slice_off(q, si);
+    const int j = J - 4 * so;  // word within the slice (0..4w-1)
     const int g = lane >> 2, tig = lane & 3;
-    const int row = rt * kRowTile + g + 8 * (u & 1);
-    const int kbase = kb * kKBlock + 16 * (u >> 1) + 4 * tig;
     uint32_t w = 0;
-    if (row < n) {
-      const uint64_t* src = planes + (static_cast<size_t>(t) * n + row) * wpr;
-#pragma unroll
-      for (int c = 0; c < 8; ++c)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const int kk = kbase + 32 * c + b;
-          if (kk < k) w |= static_cast<uint32_t>((src[kk >> 6] >> (kk & 63)) & 1ull) << (8 * b + c);
+    for (int s = 0; s < 8 / sw; ++s) {
+      // output register o = 4c + u of the lane's A fragments
+      const int o = s * 4 * sw + j, c = o >> 2, u = o & 3;
+      const int row = rt * kRowTile + g + 8 * (u & 1);
+      if (row >= n) continue;
+      for (int b = 0; b < 4; ++b) {
+        const int kk = kb * kKBlock + 32 * c + 16 * (u >> 1) + 4 * tig + b;
+        if (kk >= k) continue;
+        for (int e = 0; e < sw; ++e) {
+          const uint64_t* src = planes + (static_cast<size_t>(so + e) * n + row) * wpr;
+          w |= static_cast<uint32_t>((src[kk >> 6] >> (kk & 63)) & 1ull) << (8 * b + sw * s + e);
         }
+      }
     }
     frag[idx] = w;
   }
@@ -128,6 +134,24 @@ __device__ __forceinline__ void imma_16832(int (&d)[4], uint32_t a0, uint32_t a1
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
+// Byte-code register o (= 4c + u: chunk c, A register u) of a lane's unit from
+// its 4Q code-slice words (layout in prepack_frag_kernel / common.cuh):
+// one shift + one mask-merge per slice, all shifts compile-time constants.
+template <int Q>
+__device__ __forceinline__ uint32_t widen_slices(const uint4 (&w)[Q], int o) {
+  uint32_t r = 0;
+#pragma unroll
+  for (int i = 0; i < slice_count(Q); ++i) {
+    const int sw = slice_width(Q, i), so = slice_off(Q, i);
+    const int J = 4 * so + o % (4 * sw), sh = sw * (o / (4 * sw));
+    const uint4 v = w[J >> 2];
+    const uint32_t x = (J & 3) == 0 ? v.x : (J & 3) == 1 ? v.y : (J & 3) == 2 ? v.z : v.w;
+    const uint32_t m = static_cast<uint32_t>((1u << sw) - 1u) * 0x01010101u;
+    r |= so >= sh ? (x << (so - sh)) & (m << so) : (x >> (sh - so)) & (m << so);
+  }
+  return r;
+}
+
 // CTA that owns unit u under the even split (c*U)/G
 __device__ __forceinline__ int cta_of_unit(long long u, long long U, int G) {
   return static_cast<int>(((u + 1) * G - 1) / U);
@@ -148,8 +172,8 @@ __device__ __forceinline__ int act_frag_index(int v, int i, int mt) {
 // ---------------------------------------------------------------------------
 constexpr int kActThreads = 256;
 
-// ROW: write plain row-major u8 codes [m][row_ld] (tcgen05 GEMM operand)
-// instead of the GEMV's B-fragment order.
+// ROW: write the tcgen05 GEMM's tiled u8 operand (tc_act_offset, `row_ld` =
+// token groups) instead of the GEMV's B-fragment order.
 template <typename T, bool ROW>
 __global__ void __launch_bounds__(kActThreads) act_quant_kernel(const T* __restrict__ x, int m, int k, int mt,
                                                                 QuantParams qp, uint32_t* __restrict__ act_frag,
@@ -157,7 +181,6 @@ __global__ void __launch_bounds__(kActThreads) act_quant_kernel(const T* __restr
                                                                 int32_t* __restrict__ z_a,
                                                                 long long* __restrict__ rowsum,
                                                                 unsigned long long* __restrict__ bad_word) {
-  griddep_launch();  // let the dependent GEMV / GEMM start streaming its weights now
   __shared__ double s_lo[kActThreads / 32], s_hi[kActThreads / 32];
   __shared__ long long s_sum[kActThreads / 32];
   __shared__ double s_step;
@@ -166,10 +189,13 @@ __global__ void __launch_bounds__(kActThreads) act_quant_kernel(const T* __restr
   const int tok = blockIdx.x;
   const int tb = tok / mt, i = tok % mt;
   const int kpad = ((k + kKBlock - 1) / kKBlock) * kKBlock;
-  uint32_t* dst = ROW ? act_frag + static_cast<size_t>(tok) * row_ld / 4
-                      : act_frag + static_cast<size_t>(tb) * mt * kpad / 4;
+  uint32_t* dst = ROW ? act_frag : act_frag + static_cast<size_t>(tb) * mt * kpad / 4;
   // u32 slot of the codes of elements 4v..4v+3
-  auto slot_of = [&](int v) { return ROW ? v : act_frag_index(v, i, mt); };
+  auto slot_of = [&](int v) {
+    return ROW ? static_cast<int>(tc_act_offset(tok, 4 * v, row_ld) >> 2) : act_frag_index(v, i, mt);
+  };
+  // codes past k are zero: to the 256-block (GEMV) / 128-block (GEMM)
+  const int kzero = ROW ? (k + 127) / 128 * 128 : kpad;
   const T* row = x + static_cast<size_t>(tok) * k;
   if constexpr (sizeof(T) == 2) {
     // fp16 rows, per token, K % 8 == 0, K <= 8 * 4 * kActThreads: the row is read
@@ -196,6 +222,9 @@ __global__ void __launch_bounds__(kActThreads) act_quant_kernel(const T* __restr
           }
         }
       }
+      // the row is requested: let the dependent GEMV / GEMM start streaming its
+      // weights now (issued after our loads, so they do not queue behind them)
+      griddep_launch();
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         flo = fminf(flo, __shfl_xor_sync(0xffffffffu, flo, o));
@@ -241,9 +270,8 @@ __global__ void __launch_bounds__(kActThreads) act_quant_kernel(const T* __restr
           dst[slot_of(2 * idx + 1)] = w1;
         }
       }
-      // zero codes in the k padding of the last 256-block
-      if (!ROW)
-        for (int v4 = k / 4 + tid; v4 < kpad / 4; v4 += kActThreads) dst[act_frag_index(v4, i, mt)] = 0u;
+      // zero codes in the k padding of the last block
+      for (int v4 = k / 4 + tid; v4 < kzero / 4; v4 += kActThreads) dst[slot_of(v4)] = 0u;
       rsum = warp_sum(rsum);
       if (lane == 0) s_sum[warp] = rsum;
       __syncthreads();
@@ -255,6 +283,7 @@ __global__ void __launch_bounds__(kActThreads) act_quant_kernel(const T* __restr
       return;
     }
   }
+  griddep_launch();
   double lo = CUDART_INF, hi = -CUDART_INF;
   if (qp.per_tensor) {
     for (int t = 0; t < m; ++t)
@@ -296,7 +325,7 @@ __global__ void __launch_bounds__(kActThreads) act_quant_kernel(const T* __restr
   const double step = s_step, zd = static_cast<double>(s_z), inv = 1.0 / step;
   const double top = static_cast<double>(qp.levels - 1);
   long long rsum = 0;
-  const int ngroups = kpad / 4;  // zero codes past k
+  const int ngroups = kzero / 4;  // zero codes past k
   for (int v = tid; v < ngroups; v += kActThreads) {
     uint32_t word = 0;
 #pragma unroll
@@ -308,7 +337,7 @@ __global__ void __launch_bounds__(kActThreads) act_quant_kernel(const T* __restr
         word |= c << (8 * b);
       }
     }
-    if (!ROW || 4 * v < k) dst[slot_of(v)] = word;
+    dst[slot_of(v)] = word;
   }
   rsum = warp_sum(rsum);
   if (lane == 0) s_sum[warp] = rsum;
@@ -351,8 +380,7 @@ struct ImmaParams {
 // codes from act_quant_kernel.
 template <int QT, int MT, bool FROM_PLANES, int NWARP>
 __global__ void __launch_bounds__(NWARP * 32, 1) gemv_imma_kernel(ImmaParams P) {
-  constexpr int QMAX = QT > 0 ? QT : 8;
-  const int q = QT > 0 ? QT : P.q;
+  constexpr int q = QT;
   extern __shared__ __align__(128) unsigned char smem[];
   const int kpad = P.kblocks * kKBlock;
   const int G = gridDim.x;
@@ -391,6 +419,22 @@ __global__ void __launch_bounds__(NWARP * 32, 1) gemv_imma_kernel(ImmaParams P) 
   const int mb = min(MT, P.m - tok0);
   unsigned long long* trace = P.trace ? P.trace + 8 * (blockIdx.y * gridDim.x + blockIdx.x) : nullptr;
   if (trace && tid == 0) trace[0] = clock64();
+
+  // ---- 0. fused ReQuant: request the activation rows first, so that they are
+  // not queued behind the ~200 KB of weight-ring TMA traffic every SM issues next
+  constexpr int XT = MT < 2 ? MT : 2;
+  uint4 xv[XT][4];
+  if (!FROM_PLANES && P.x16) {
+#pragma unroll
+    for (int i = 0; i < XT; ++i)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int idx = tid + r * NWARP * 32;
+        xv[i][r] = make_uint4(0u, 0u, 0u, 0u);
+        if (i < mb && idx < (P.k >> 3))
+          xv[i][r] = __ldg(reinterpret_cast<const uint4*>(P.x16 + static_cast<size_t>(tok0 + i) * P.k) + idx);
+      }
+  }
 
   // ---- 1. this warp's units; start its TMA weight ring immediately
   const long long wu0 = U0 + (U1 - U0) * warp / NWARP;
@@ -451,16 +495,15 @@ __global__ void __launch_bounds__(NWARP * 32, 1) gemv_imma_kernel(ImmaParams P) 
     for (int idx = tid; idx < MT * kpad / 4; idx += NWARP * 32) act[idx] = 0u;
     const int nvec = P.k >> 3;
     const double top = static_cast<double>(P.qp.levels - 1);
-    for (int i = 0; i < mb; ++i) {
-      const uint4* xr = reinterpret_cast<const uint4*>(P.x16 + static_cast<size_t>(tok0 + i) * P.k);
-      uint4 v[4];
+#pragma unroll
+    for (int i = 0; i < XT; ++i) {
+      if (i >= mb) break;  // uniform across the CTA
+      uint4 (&v)[4] = xv[i];
       float lo = CUDART_INF_F, hi = -CUDART_INF_F;
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
         const int idx = tid + r * NWARP * 32;
-        v[r] = make_uint4(0u, 0u, 0u, 0u);
         if (idx < nvec) {
-          v[r] = __ldg(xr + idx);
           const __half2* h2 = reinterpret_cast<const __half2*>(&v[r]);
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
@@ -551,9 +594,8 @@ __global__ void __launch_bounds__(NWARP * 32, 1) gemv_imma_kernel(ImmaParams P) 
   if (trace && tid == 0) trace[1] = clock64();
 
   // ---- 4. main loop over this warp's units (one body, TMA ring slots)
-  // one accumulator fragment: the q planes of a chunk are merged into one A
-  // register set holding code << (8 - q) (plane t on bit 8 - q + t), so each
-  // k32 chunk costs one IMMA; the 2^(8-q) scale is divided out exactly in flush.
+  // one accumulator fragment: the code slices of a chunk are widened into one
+  // A register set of u8 codes, so each k32 chunk costs one IMMA.
   int acc[4] = {0, 0, 0, 0};
   int cur_rt = wu0 < wu1 ? static_cast<int>(wu0 / P.kblocks) : -1;
   const uint2* act2 = reinterpret_cast<const uint2*>(act);
@@ -562,7 +604,8 @@ __global__ void __launch_bounds__(NWARP * 32, 1) gemv_imma_kernel(ImmaParams P) 
     const int lrt = rt - rt_first;
     long long v[4];
 #pragma unroll
-    for (int r = 0; r < 4; ++r) v[r] = static_cast<long long>(acc[r] >> (8 - q));
+    // the true sum is < 2^32 (K <= 65536, codes <= 255): exact as unsigned
+    for (int r = 0; r < 4; ++r) v[r] = static_cast<long long>(static_cast<uint32_t>(acc[r]));
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       const int row = g + 8 * (r >> 1), tok = 2 * tig + (r & 1);
@@ -582,39 +625,18 @@ __global__ void __launch_bounds__(NWARP * 32, 1) gemv_imma_kernel(ImmaParams P) 
   for (int uu = static_cast<int>(wu0); uu < uend; ++uu) {
     if (ui == 0) mbar_wait_parity(&my_bars[slot], phase);
     const uint4* wv = reinterpret_cast<const uint4*>(my_ring + slot * chunk_bytes + ui * unit_bytes) + lane;
-    uint4 w[QMAX];
+    uint4 w[QT];
 #pragma unroll
-    for (int t = 0; t < QMAX; ++t)
-      if (t < q) w[t] = wv[t * 32];
+    for (int t = 0; t < QT; ++t) w[t] = wv[t * 32];
     const uint2* ab = act2 + static_cast<size_t>(kb) * 8 * MT * 4;
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       uint2 b = make_uint2(0u, 0u);
       if (g < MT) b = ab[(c * MT + g) * 4 + tig];
-      uint32_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+      uint32_t a[4];
 #pragma unroll
-      for (int t = 0; t < QMAX; ++t) {
-        if (t < q) {
-          // bit (8b + c) of the plane word -> bit (8b + 8 - q + t) of the code byte
-          const int tb = 8 - q + t;
-          const uint32_t m = 0x01010101u << tb;
-          if (tb >= c) {
-            a0 |= (w[t].x << (tb - c)) & m;
-            a1 |= (w[t].y << (tb - c)) & m;
-            a2 |= (w[t].z << (tb - c)) & m;
-            a3 |= (w[t].w << (tb - c)) & m;
-          } else {
-            // right shift as the high word of a multiply: IMAD.HI runs on the
-            // fma pipe and leaves the alu pipe to the LOP3 merges
-            const uint32_t f = 1u << (32 - (c - tb));
-            a0 |= __umulhi(w[t].x, f) & m;
-            a1 |= __umulhi(w[t].y, f) & m;
-            a2 |= __umulhi(w[t].z, f) & m;
-            a3 |= __umulhi(w[t].w, f) & m;
-          }
-        }
-      }
-      imma_16832(acc, a0, a1, a2, a3, b.x, b.y);
+      for (int u = 0; u < 4; ++u) a[u] = widen_slices<QT>(w, 4 * c + u);
+      imma_16832(acc, a[0], a[1], a[2], a[3], b.x, b.y);
     }
     // chunk finished: refill its slot with the chunk `slots` ahead (the whole
     // warp has read it)
@@ -845,8 +867,10 @@ static int launch_q(ImmaParams P, int gx, int gy, bool pdl, cudaStream_t st) {
     case 2: return launch_imma<2, MT, FP>(P, gx, gy, pdl, st);
     case 3: return launch_imma<3, MT, FP>(P, gx, gy, pdl, st);
     case 4: return launch_imma<4, MT, FP>(P, gx, gy, pdl, st);
-    case 8: return launch_imma<8, MT, FP>(P, gx, gy, pdl, st);
-    default: return launch_imma<0, MT, FP>(P, gx, gy, pdl, st);
+    case 5: return launch_imma<5, MT, FP>(P, gx, gy, pdl, st);
+    case 6: return launch_imma<6, MT, FP>(P, gx, gy, pdl, st);
+    case 7: return launch_imma<7, MT, FP>(P, gx, gy, pdl, st);
+    default: return launch_imma<8, MT, FP>(P, gx, gy, pdl, st);
   }
 }
 
@@ -917,8 +941,8 @@ int run_gemv_imma_planes(const uint32_t* frag, unsigned q, size_t n, size_t k, s
 }
 
 // K1 launcher: one CTA per token.  row_ld == 0: B-fragment order for the decode
-// GEMV (token blocks of mt); row_ld > 0: row-major u8 codes for the tcgen05 GEMM
-// (row_ld % 16 == 0).  bad_word: zero-initialised, receives atomicMax(~index).
+// GEMV (token blocks of mt); row_ld > 0: the tcgen05 GEMM's tiled operand with
+// row_ld = tc_act_groups(m) token groups (k % 16 == 0).  bad_word: zero-initialised, receives atomicMax(~index).
 int run_act_quant(const void* x, int x_dtype, size_t m, size_t k, int mt, const QuantParams& qp,
                   uint32_t* out, int row_ld, double* s_a, int32_t* z_a, long long* rowsum,
                   unsigned long long* bad_word, cudaStream_t st) {
