@@ -473,6 +473,11 @@ def sweep(abq, torch, world):
         step_us, kern_us = ms * 1e3 / steps, kms * 1e3 / steps
         row = {"workload": name, "step_us": round(step_us, 3), "kernel_us": round(kern_us, 3),
                "kernel_GBps": round(wbytes / kern_us / 1e3, 1), "TOPS": round(2 * m * n * k / step_us / 1e6, 2)}
+        if m >= 16 and (ab, wb) in ((4, 4), (8, 8), (8, 2), (8, 4), (4, 8), (2, 2)):
+            # b1 tensor-core (mma.sync .b1 and.popc) plane GEMM, the BTC alternative
+            bsteps = 40
+            bms, _ = time_graph(torch, lambda i: abq.gemm_btc(a_planes, ws[i].planes), copies, bsteps, 3, world)
+            row["btc_b1_gemm_us"] = round(bms * 1e3 / bsteps, 3)
         if m >= 8:
             # cuBLAS fp16 comparator at the same shape (weights rotated past L2)
             wf = [torch.randn((n, k), dtype=torch.float16, device="cuda") for _ in range(

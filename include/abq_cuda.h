@@ -170,6 +170,12 @@ int abq_gemm_arbitrary_wide(const uint64_t* a, unsigned p, size_t m, size_t a_k,
                             const uint64_t* bt, unsigned q, size_t n, size_t b_k,
                             const abq_tile_config* tile, int64_t* out, abq_gemm_stats* stats,
                             void* stream);
+/* gemm_btc: the same plane GEMM as gemm_arbitrary (gemm.hpp:94-146, int32
+ * accumulators) on the b1 tensor-core path (mma.sync m16n8k256 .b1 and.popc),
+ * kept as the measured comparator of the tcgen05 recombination GEMM; (p, q) in
+ * {(4,4), (8,8), (8,2), (8,4), (4,8), (2,2)}.  Validation as gemm_arbitrary. */
+int abq_gemm_btc(const uint64_t* a, unsigned p, size_t m, size_t a_k, const uint64_t* bt, unsigned q,
+                 size_t n, size_t b_k, int32_t* out, void* stream);
 /* gemm_naive  gemm.hpp:213-231 */
 int abq_gemm_naive(const uint64_t* a, unsigned p, size_t m, size_t a_k, const uint64_t* bt,
                    unsigned q, size_t n, size_t b_k, int32_t* out, void* stream);

@@ -9,6 +9,6 @@ from . import _lib  # noqa: F401
 from .api import *  # noqa: F401,F403
 from .api import (BitPlaneMatrix, Error, GemmStats, IoError, Linear, OverflowError,  # noqa: F401
                   PackedWeights, QuantizedTensor, QuantSpec, ShapeError, TileConfig, ValueError,
-                  bitpack, bmma, code_rowsums, default_tile, dequantize, fits_int32, gemm_arbitrary,
+                  bitpack, bmma, code_rowsums, default_tile, dequantize, fits_int32, gemm_arbitrary, gemm_btc,
                   gemm_arbitrary_wide, gemm_naive, linear_planes, padding_redundancy, plane_rowsums,
                   quantize, quantize_balanced, quantized_linear, unpack, zero_point_correct)

@@ -68,6 +68,7 @@ _SIGNATURES = {
     "abq_bitpack": (_I, [_P, _S, _S, _U, _P, _P]),
     "abq_unpack": (_I, [_P, _U, _S, _S, _P, _P]),
     "abq_bmma": (_I, [_P, _U, _S, _U, _P, _U, _S, _U, _S, _P, _P]),
+    "abq_gemm_btc": (_I, [_P, _U, _S, _S, _P, _U, _S, _S, _P, _P]),
     "abq_gemm_arbitrary": (_I, [_P, _U, _S, _S, _P, _U, _S, _S, C.POINTER(TileConfigC), _P,
                                 C.POINTER(GemmStatsC), _P]),
     "abq_gemm_arbitrary_wide": (_I, [_P, _U, _S, _S, _P, _U, _S, _S, C.POINTER(TileConfigC), _P,

@@ -259,6 +259,16 @@ def bmma(a: BitPlaneMatrix, a_plane: int, bt: BitPlaneMatrix, b_plane: int) -> t
     return out
 
 
+def gemm_btc(a: BitPlaneMatrix, bt: BitPlaneMatrix) -> torch.Tensor:
+    """The plane GEMM of gemm_arbitrary (gemm.hpp:94-146) on the b1 tensor-core
+    path (mma.sync m16n8k256 .b1 and.popc): the measured comparator of the
+    tcgen05 recombination GEMM.  Returns int32 [M][N]."""
+    out = torch.empty((a.rows, bt.rows), dtype=torch.int32, device=_dev())
+    _check(L.lib().abq_gemm_btc(_ptr(a.data), a.planes, a.rows, a.cols, _ptr(bt.data), bt.planes, bt.rows,
+                                bt.cols, _ptr(out), _stream()))
+    return out
+
+
 # ---------------------------------------------------------------------------
 # engine (gemm.hpp)
 # ---------------------------------------------------------------------------

@@ -93,6 +93,8 @@ int run_gemv_imma_fused(const uint32_t* frag, unsigned q, size_t n, size_t k, si
                         int x_dtype, const QuantParams& qp, const EpiParams& e, void* ws,
                         unsigned long long* bad_out, cudaStream_t st);
 
+int run_gemm_bmma(const uint64_t* a, unsigned p, size_t m, const uint64_t* w, unsigned q, size_t n, size_t k,
+                  int32_t* out, cudaStream_t st);
 size_t tc_words(unsigned q, size_t n, size_t k);
 int run_prepack_tc(const uint64_t* planes, unsigned q, size_t n, size_t k, uint32_t* out,
                    cudaStream_t st);
@@ -350,6 +352,16 @@ int abq_unpack(const uint64_t* planes, unsigned bits, size_t rows, size_t cols, 
   int st = check_device();
   if (st) return st;
   return run_unpack(planes, bits, rows, cols, codes, as_stream(stream));
+}
+
+int abq_gemm_btc(const uint64_t* a, unsigned p, size_t m, size_t a_k, const uint64_t* bt, unsigned q,
+                 size_t n, size_t b_k, int32_t* out, void* stream) {
+  if (a_k != b_k) return fail(ABQ_ERR_SHAPE, "gemm_btc: shared K dimension differs");
+  if (!fits_int32_host(p, q, a_k))
+    return fail(ABQ_ERR_OVERFLOW, "gemm_btc: p+q+ceil(log2(K+1)) = %u+%u+log2(%zu+1) exceeds 31", p, q, a_k);
+  int st = check_device();
+  if (st) return st;
+  return run_gemm_bmma(a, p, m, bt, q, n, a_k, out, as_stream(stream));
 }
 
 int abq_bmma(const uint64_t* a, unsigned a_planes, size_t m, unsigned a_plane, const uint64_t* bt,

@@ -86,6 +86,21 @@ inline size_t tc_act_bytes(size_t m, size_t k) {
   return static_cast<size_t>(tc_act_groups(static_cast<long long>(m))) * 8 * ((k + 127) / 128) * 128;
 }
 
+// Kernel parameters live in constant bank 0 and are fetched through the
+// constant cache on first use.  Kernels that start a TMA stream of ~200 KB per
+// SM must touch their parameter block BEFORE the stream: a constant-cache miss
+// issued behind it waits microseconds for the SM's memory queue to drain.
+// One warp reads one word per 32 B of the block and consumes it.
+template <typename T>
+__device__ __forceinline__ void warm_param_block(const T& params, int lane) {
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(&params);
+  constexpr int kWords = static_cast<int>(sizeof(T) / 4);
+  for (int i = lane * 8; i < kWords; i += 256) {
+    const uint32_t v = w[i];
+    asm volatile("" ::"r"(v));
+  }
+}
+
 // QuantSpec as the kernels see it (quantizer.hpp:37-71)
 struct QuantParams {
   unsigned bits;

@@ -36,6 +36,8 @@
 
 namespace abq_dev {
 
+unsigned long long*& trace_buffer();
+
 constexpr int kTcM = 128;
 constexpr int kTcK = 128;
 constexpr int kTcThreads = 256;
@@ -172,6 +174,88 @@ __device__ __forceinline__ uint32_t widen_row(const uint4 (&w)[Q], int o) {
   return r;
 }
 
+// Epilogue of one CTA tile, one output channel (TMEM lane) and half of the
+// token columns per thread, specialised per output mode so the loop body is
+// branch-free: 8 accumulators per tcgen05.ld, zero-point correction in
+// unsigned 32x32 -> 64-bit products, exact int64 -> double by the 1.5 * 2^52
+// magic add (|corr| < 2^51; keeps the conversion unit for the final F2F),
+// dequant as RN64(RN64(s_a * s_b) * corr) like gemm.hpp:292-306; all 8 values
+// are computed before the (token-bounded) stores.  fp16 results go to a
+// [token][channel] shared-memory tile first (written out with 16-byte stores
+// by tc_store_f16).
+template <int MODE, int TT>
+__device__ __forceinline__ void tc_epilogue(const EpiParams& E, uint32_t taddr, int half, int tok0, int m, int ch,
+                                            int n, const double* t_sa, const unsigned* t_za, const unsigned* t_kz,
+                                            const unsigned* t_ra, __half* stage, int lch) {
+  constexpr bool kRaw = MODE == EPI_ACC_I32 || MODE == EPI_ACC_I64;
+  const bool chan_ok = ch < n;
+  // |colsum_b|, |u| <= 255 K < 2^31 for K <= 65536
+  double sb = 0.0;
+  int zb = 0, cs = 0;
+  if (!kRaw && chan_ok) {
+    sb = E.s_b[ch * E.sb_stride];
+    zb = E.z_b[ch * E.zb_stride];
+    cs = static_cast<int>(E.colsum_b[ch]);
+  }
+#pragma unroll 1
+  for (int c0 = half * (TT / 2); c0 < (half + 1) * (TT / 2); c0 += 8) {
+    uint32_t v[8];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+        : "r"(taddr + static_cast<uint32_t>(c0)));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    if (!chan_ok) continue;
+    const bool full = tok0 + c0 + 8 <= m;  // uniform: no per-token bound in the common case
+    const long long o0 = static_cast<long long>(tok0 + c0) * E.ldo + ch;
+    if constexpr (kRaw) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        // the true sum is < 2^32 (K <= 65536, codes <= 255): exact as unsigned
+        if (full || tok0 + c0 + i < m) {
+          if constexpr (MODE == EPI_ACC_I32) static_cast<int32_t*>(E.out)[o0 + i * E.ldo] = static_cast<int32_t>(v[i]);
+          else static_cast<int64_t*>(E.out)[o0 + i * E.ldo] = static_cast<long long>(v[i]);
+        }
+      }
+    } else {
+      // corrected = acc + (K z_a) z_b - z_a colsum_b - z_b rowsum_a: every factor
+      // is a non-negative 32-bit value, every product one IMAD.WIDE.U32
+      long long corr[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int ti = c0 + i;
+        const unsigned long long plus = static_cast<unsigned long long>(v[i]) +
+                                        static_cast<unsigned long long>(t_kz[ti]) * static_cast<unsigned>(zb);
+        const unsigned long long minus = static_cast<unsigned long long>(t_za[ti]) * static_cast<unsigned>(cs) +
+                                         static_cast<unsigned long long>(t_ra[ti]) * static_cast<unsigned>(zb);
+        corr[i] = static_cast<long long>(plus - minus);
+      }
+      if constexpr (MODE == EPI_CORR_I64) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          if (full || tok0 + c0 + i < m) static_cast<int64_t*>(E.out)[o0 + i * E.ldo] = corr[i];
+      } else {
+        double y[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          // exact int64 -> double (|corr| < 2^51) by the 1.5 * 2^52 magic add
+          const double cd = __dsub_rn(__longlong_as_double(0x4338000000000000LL + corr[i]), 6755399441055744.0);
+          y[i] = __dmul_rn(__dmul_rn(t_sa[c0 + i], sb), cd);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if (full || tok0 + c0 + i < m) {
+            const long long o = o0 + i * E.ldo;
+            if constexpr (MODE == EPI_F64) static_cast<double*>(E.out)[o] = y[i];
+            else if constexpr (MODE == EPI_F16) stage[(c0 + i) * kTcM + lch] = __double2half(y[i]);
+            else static_cast<float*>(E.out)[o] = __double2float_rn(y[i]);
+          }
+        }
+      }
+    }
+  }
+}
+
 struct TcParams {
   const uint32_t* wtc;  // tc code slices
   const uint8_t* act;   // tiled u8 activation codes (tc_act_offset)
@@ -179,6 +263,7 @@ struct TcParams {
   EpiParams e;
   unsigned long long* bad_word;  // ReQuant status (~index, 0 = none), published to bad_out
   unsigned long long* bad_out;
+  unsigned long long* trace;  // optional [grid][16] clock64 / globaltimer stamps (profiling)
 };
 
 template <int Q, int TT>
@@ -193,7 +278,7 @@ struct TcShape {
 };
 
 template <int Q, int TT>
-__global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(TcParams P) {
+__global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_constant__ TcParams P) {
   using Sh = TcShape<Q, TT>;
   constexpr int S = Sh::kS;
   constexpr int TMEM_COLS = TT <= 32 ? 32 : (TT <= 64 ? 64 : (TT <= 128 ? 128 : 256));
@@ -201,10 +286,22 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(TcParams P) {
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ __align__(8) uint64_t wbar[S], abar[S], rbar[S], ebar[S], done_bar;
   __shared__ uint32_t tmem_base_s;
+  // per-token epilogue values, loaded by the otherwise idle warps 2-3:
+  // s_a, z_a, K z_a, rowsum_a (all non-negative, < 2^32 for K <= 65536)
+  __shared__ double t_sa[TT];
+  __shared__ unsigned t_za[TT], t_kz[TT], t_ra[TT];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (warp == 7) warm_param_block(P, lane);
   const int rt = blockIdx.x, tok0 = blockIdx.y * TT;
   const int nkb = P.kblocks;
+  unsigned long long* trace = P.trace ? P.trace + 16 * (blockIdx.y * gridDim.x + blockIdx.x) : nullptr;
+  if (trace && tid == 0) {
+    unsigned long long g;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g));
+    trace[0] = clock64();
+    trace[8] = g;
+  }
   auto a_of = [&](int s) { return smem + s * Sh::kStage; };
   auto b_of = [&](int s) { return smem + s * Sh::kStage + Sh::kA; };
   auto w_of = [&](int s) { return smem + s * Sh::kStage + Sh::kA + Sh::kB; };
@@ -275,6 +372,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(TcParams P) {
         mbar_wait(Sh::kExpand ? &rbar[s] : &wbar[s], ph);
         mbar_wait(&abar[s], ph);
         tc_fence_after();
+        if (trace && (kb & 7) == 0 && kb < 64) trace[10 + (kb >> 3)] = clock64();
         const uint32_t a_addr = smem_u32(a_of(s)), b_addr = smem_u32(b_of(s));
 #pragma unroll
         for (int j = 0; j < kTcK / 32; ++j) {
@@ -285,6 +383,22 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(TcParams P) {
         tc_commit(&ebar[s]);
       }
       tc_commit(&done_bar);
+      if (trace) trace[3] = clock64();
+    }
+  } else if (warp == 2 || warp == 3) {
+    const EpiParams& E = P.e;
+    if (E.mode != EPI_ACC_I32 && E.mode != EPI_ACC_I64) {
+      asm volatile("griddepcontrol.wait;" ::: "memory");  // ReQuant results visible
+      for (int i = tid - 64; i < TT; i += 64) {
+        const int tk = tok0 + i;
+        if (tk < P.m) {
+          const int za = E.z_a[tk * E.za_stride];
+          t_sa[i] = E.s_a[tk * E.sa_stride];
+          t_za[i] = static_cast<unsigned>(za);
+          t_kz[i] = static_cast<unsigned>(E.k * za);
+          t_ra[i] = static_cast<unsigned>(E.rowsum_a[tk]);
+        }
+      }
     }
   } else if (Sh::kExpand && warp >= 4) {
     // ---- widen packed code slices of row r into the A operand
@@ -305,61 +419,52 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(TcParams P) {
       mbar_arrive(&rbar[s]);
     }
   }
-  __syncwarp();
+  __syncthreads();  // per-token values in shared memory
 
   // ---- epilogue: TMEM -> registers -> zero-point correction + dequant.  A
   // thread owns one output channel (TMEM lane) and half of the token columns,
   // so the per-channel parameters are loaded once.
   mbar_wait(&done_bar, 0);
   tc_fence_after();
+  if (trace && tid == 0) trace[4] = clock64();
   const int quarter = warp & 3, half = warp >> 2;
-  const int ch = rt * kTcM + quarter * 32 + lane;
-  const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
-  const EpiParams& E = P.e;
-  const bool raw = E.mode == EPI_ACC_I32 || E.mode == EPI_ACC_I64;
-  const bool chan_ok = ch < P.n;
-  double sb = 0.0;
-  long long zb = 0, cs = 0;
-  if (!raw && chan_ok) {
-    sb = E.s_b[ch * E.sb_stride];
-    zb = E.z_b[ch * E.zb_stride];
-    cs = E.colsum_b[ch];
+  const int lch = quarter * 32 + lane, ch = rt * kTcM + lch;
+  __half* stage = reinterpret_cast<__half*>(smem);  // the operand ring is idle now
+  const uint32_t taddr = tmem_d + (static_cast<uint32_t>(quarter * 32) << 16);
+  switch (P.e.mode) {
+    case EPI_ACC_I32: tc_epilogue<EPI_ACC_I32, TT>(P.e, taddr, half, tok0, P.m, ch, P.n, t_sa, t_za, t_kz, t_ra, stage, lch); break;
+    case EPI_ACC_I64: tc_epilogue<EPI_ACC_I64, TT>(P.e, taddr, half, tok0, P.m, ch, P.n, t_sa, t_za, t_kz, t_ra, stage, lch); break;
+    case EPI_F64: tc_epilogue<EPI_F64, TT>(P.e, taddr, half, tok0, P.m, ch, P.n, t_sa, t_za, t_kz, t_ra, stage, lch); break;
+    case EPI_F16: tc_epilogue<EPI_F16, TT>(P.e, taddr, half, tok0, P.m, ch, P.n, t_sa, t_za, t_kz, t_ra, stage, lch); break;
+    case EPI_F32: tc_epilogue<EPI_F32, TT>(P.e, taddr, half, tok0, P.m, ch, P.n, t_sa, t_za, t_kz, t_ra, stage, lch); break;
+    default: tc_epilogue<EPI_CORR_I64, TT>(P.e, taddr, half, tok0, P.m, ch, P.n, t_sa, t_za, t_kz, t_ra, stage, lch); break;
   }
-#pragma unroll 1
-  for (int c0 = half * (TT / 2); c0 < (half + 1) * (TT / 2); c0 += 8) {
-    uint32_t v[8];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
-        : "r"(tmem_d + lane_base + static_cast<uint32_t>(c0)));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    if (!chan_ok) continue;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int tk = tok0 + c0 + i;
-      if (tk >= P.m) continue;
-      // the true sum is < 2^32 (K <= 65536, codes <= 255): exact as unsigned
-      const long long acc = static_cast<long long>(v[i]);
-      const long long o = static_cast<long long>(tk) * E.ldo + ch;
-      if (raw) {
-        if (E.mode == EPI_ACC_I32) static_cast<int32_t*>(E.out)[o] = static_cast<int32_t>(acc);
-        else static_cast<int64_t*>(E.out)[o] = acc;
-        continue;
+  if (P.e.mode == EPI_F16) {
+    // staged fp16 tile -> global, 8 channels (16 B) per store where aligned
+    __syncthreads();
+    const int rows = min(TT, P.m - tok0), cols = min(kTcM, P.n - rt * kTcM);
+    __half* out = static_cast<__half*>(P.e.out);
+    const bool vec = (P.e.ldo & 7) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+    for (int idx = tid; idx < rows * (kTcM / 8); idx += kTcThreads) {
+      const int r = idx / (kTcM / 8), c8 = (idx % (kTcM / 8)) * 8;
+      if (c8 >= cols) continue;
+      const __half* src = stage + r * kTcM + c8;
+      __half* dst = out + static_cast<long long>(tok0 + r) * P.e.ldo + rt * kTcM + c8;
+      if (vec && c8 + 8 <= cols) {
+        *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(src);
+      } else {
+        for (int j = 0; j < 8 && c8 + j < cols; ++j) dst[j] = src[j];
       }
-      const long long za = E.z_a[tk * E.za_stride];
-      const long long corr = acc - za * cs - zb * E.rowsum_a[tk] + E.k * za * zb;
-      if (E.mode == EPI_CORR_I64) {
-        static_cast<int64_t*>(E.out)[o] = corr;
-        continue;
-      }
-      const double y = __dmul_rn(__dmul_rn(E.s_a[tk * E.sa_stride], sb), static_cast<double>(corr));
-      if (E.mode == EPI_F64) static_cast<double*>(E.out)[o] = y;
-      else if (E.mode == EPI_F16) static_cast<__half*>(E.out)[o] = __double2half(y);
-      else static_cast<float*>(E.out)[o] = __double2float_rn(y);
     }
   }
   tc_fence_before();
   __syncthreads();
+  if (trace && tid == 0) {
+    unsigned long long g;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g));
+    trace[5] = clock64();
+    trace[9] = g;
+  }
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d), "r"(TMEM_COLS));
 }
@@ -450,6 +555,7 @@ int run_gemm_tc(const uint32_t* wtc, unsigned q, size_t n, size_t k, const uint8
   P.rowtiles = static_cast<int>((n + kTcM - 1) / kTcM);
   P.kblocks = static_cast<int>((k + kTcK - 1) / kTcK);
   P.e = e;
+  P.trace = trace_buffer();
   switch (q) {
     case 1: return launch_tt<1>(P, pdl, st);
     case 2: return launch_tt<2>(P, pdl, st);

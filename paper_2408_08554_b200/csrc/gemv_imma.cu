@@ -250,8 +250,9 @@ __global__ void __launch_bounds__(kActThreads) act_quant_kernel(const T* __restr
         z_a[tok] = z;
       }
       __syncthreads();
-      const double step = s_step, zd = static_cast<double>(s_z), inv = 1.0 / step;
-      const double top = static_cast<double>(qp.levels - 1);
+      const double step = s_step;
+      const float inv32 = f32_reciprocal(step);
+      const int zi = s_z, topi = static_cast<int>(qp.levels - 1);
       long long rsum = 0;
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
@@ -261,7 +262,7 @@ __global__ void __launch_bounds__(kActThreads) act_quant_kernel(const T* __restr
           uint32_t w0 = 0, w1 = 0;
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
-            const unsigned c = quant_code_fast(static_cast<double>(__half2float(hv[e])), step, inv, zd, top);
+            const unsigned c = quant_code_f32(__half2float(hv[e]), step, inv32, zi, topi);
             rsum += c;
             if (e < 4) w0 |= c << (8 * e);
             else w1 |= c << (8 * (e - 4));
@@ -373,13 +374,14 @@ struct ImmaParams {
   const __half* x16;             // fused path: fp16 activations quantized in the prologue
   QuantParams qp;
   int slots;                     // TMA ring slots per warp
+  int late_ring;                 // experiment: start the whole ring after the prologue
   int upc;                       // units per TMA chunk (chunks of ~4 KB stream at full HBM rate)
 };
 
 // FROM_PLANES: activations are given as ABQP planes (API path) instead of
 // codes from act_quant_kernel.
 template <int QT, int MT, bool FROM_PLANES, int NWARP>
-__global__ void __launch_bounds__(NWARP * 32, 1) gemv_imma_kernel(ImmaParams P) {
+__global__ void __launch_bounds__(NWARP * 32, 1) gemv_imma_kernel(const __grid_constant__ ImmaParams P) {
   constexpr int q = QT;
   extern __shared__ __align__(128) unsigned char smem[];
   const int kpad = P.kblocks * kKBlock;
@@ -417,11 +419,28 @@ __global__ void __launch_bounds__(NWARP * 32, 1) gemv_imma_kernel(ImmaParams P) 
   const int g = lane >> 2, tig = lane & 3;
   const int tok0 = blockIdx.y * MT;
   const int mb = min(MT, P.m - tok0);
-  unsigned long long* trace = P.trace ? P.trace + 8 * (blockIdx.y * gridDim.x + blockIdx.x) : nullptr;
-  if (trace && tid == 0) trace[0] = clock64();
+  if (warp == NWARP - 1) warm_param_block(P, lane);
+  unsigned long long* trace = P.trace ? P.trace + 16 * (blockIdx.y * gridDim.x + blockIdx.x) : nullptr;
+  if (trace && tid == 0) {
+    trace[0] = clock64();
+    trace[8] = gtimer();
+  }
 
-  // ---- 0. fused ReQuant: request the activation rows first, so that they are
-  // not queued behind the ~200 KB of weight-ring TMA traffic every SM issues next
+  // ring barriers first: the release fence that publishes their init would
+  // otherwise wait for the loads below to complete
+  const long long wu0 = U0 + (U1 - U0) * warp / NWARP;
+  const long long wu1 = U0 + (U1 - U0) * (warp + 1) / NWARP;
+  unsigned char* my_ring = wring + warp * P.slots * chunk_bytes;
+  uint64_t* my_bars = bars + warp * P.slots;
+  if (lane == 0) {
+    for (int s = 0; s < P.slots; ++s) mbar_init1(&my_bars[s]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+
+  // ---- 0. global reads of the prologue are REQUESTED before the weight ring
+  // is started: every SM queues ~200 KB of TMA traffic next, and a load issued
+  // behind it waits for that queue to drain (~4 us at the per-SM share of HBM).
+  // (a) fused ReQuant: the activation rows (registers)
   constexpr int XT = MT < 2 ? MT : 2;
   uint4 xv[XT][4];
   if (!FROM_PLANES && P.x16) {
@@ -435,17 +454,26 @@ __global__ void __launch_bounds__(NWARP * 32, 1) gemv_imma_kernel(ImmaParams P) 
           xv[i][r] = __ldg(reinterpret_cast<const uint4*>(P.x16 + static_cast<size_t>(tok0 + i) * P.k) + idx);
       }
   }
+  // (b) per-channel epilogue parameters of this CTA's row-tiles (<= 1 channel
+  // per thread; stored to shared memory after the ring is started)
+  const bool dequant = P.e.mode != EPI_ACC_I32 && P.e.mode != EPI_ACC_I64;
+  const int pj = rt_first * kRowTile + tid;
+  const bool has_param = dequant && tid < nlrt * 16 && pj < P.n;
+  double p_sb = 0.0;
+  long long p_zb = 0, p_cs = 0;
+  if (has_param) {
+    p_sb = P.e.s_b[pj * P.e.sb_stride];
+    p_zb = P.e.z_b[pj * P.e.zb_stride];
+    p_cs = P.e.colsum_b[pj];
+  }
 
-  // ---- 1. this warp's units; start its TMA weight ring immediately
-  const long long wu0 = U0 + (U1 - U0) * warp / NWARP;
-  const long long wu1 = U0 + (U1 - U0) * (warp + 1) / NWARP;
-  unsigned char* my_ring = wring + warp * P.slots * chunk_bytes;
-  uint64_t* my_bars = bars + warp * P.slots;
+  // ---- 1. this warp's units; start its TMA weight ring.  Paths that still
+  // read activations from global memory after this point (ReQuant kernel
+  // codes, packed planes) start one slot per warp now (64 KB per SM, enough to
+  // keep HBM busy) and the rest once those reads are issued.
   const unsigned char* wsrc = reinterpret_cast<const unsigned char*>(P.frag);
-  if (lane == 0) {
-    for (int s = 0; s < P.slots; ++s) mbar_init1(&my_bars[s]);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int s = 0; s < P.slots; ++s) {
+  auto start_slots = [&](int s0, int s1) {  // lane 0 only
+    for (int s = s0; s < s1; ++s) {
       const long long un = wu0 + static_cast<long long>(s) * P.upc;
       if (un >= wu1) break;
       const long long un1 = un + P.upc < wu1 ? un + P.upc : wu1;
@@ -453,15 +481,23 @@ __global__ void __launch_bounds__(NWARP * 32, 1) gemv_imma_kernel(ImmaParams P) 
       mbar_expect_tx(&my_bars[s], bytes);
       tma_bulk_g2s(my_ring + s * chunk_bytes, wsrc + un * unit_bytes, bytes, &my_bars[s]);
     }
-  }
+  };
+  const bool late_act = FROM_PLANES || P.x16 == nullptr;
+  const int first_slots = P.late_ring ? 0 : (late_act ? 1 : P.slots);
+  if (lane == 0) start_slots(0, first_slots);
 
-  // ---- 2. per-channel epilogue parameters of this CTA's row-tiles, zero accumulators.
-  // The epilogue's scalar parameters are copied to shared memory here, so
-  // their constant-bank loads happen now instead of after the main loop.
+  // ---- 2. epilogue parameters to shared memory, zero accumulators.  The
+  // epilogue's scalar parameters are copied to shared memory too, so their
+  // constant-bank loads happen now instead of after the main loop.
   __shared__ EpiParams s_e;
+  if (trace && tid == 0) trace[7] = clock64();
   if (tid == 0) s_e = P.e;
-  const bool dequant = P.e.mode != EPI_ACC_I32 && P.e.mode != EPI_ACC_I64;
-  for (int idx = tid; dequant && idx < nlrt * 16; idx += NWARP * 32) {
+  if (has_param) {
+    c_sb[tid] = p_sb;
+    c_zb[tid] = p_zb;
+    c_cs[tid] = p_cs;
+  }
+  for (int idx = tid + NWARP * 32; dequant && idx < nlrt * 16; idx += NWARP * 32) {  // > 32 row-tiles per CTA
     const int j = rt_first * kRowTile + idx;
     if (j < P.n) {
       c_sb[idx] = P.e.s_b[j * P.e.sb_stride];
@@ -487,14 +523,15 @@ __global__ void __launch_bounds__(NWARP * 32, 1) gemv_imma_kernel(ImmaParams P) 
       }
       act[act_frag_index(v, i, MT)] = word;
     }
+    if (lane == 0) start_slots(first_slots, P.slots);
   } else if (P.x16) {
     // Fused ReQuant (decode, m <= 2, fp16, per token): every CTA quantizes the
     // activation rows itself while its TMA weight ring fills -- no extra launch.
     // Row held in registers (<= 4 x 16 B per thread), min/max in fp32 (exact for
-    // fp16), step / zero point / codes in FP64 exactly as quantizer.hpp:169-210.
+    // fp16), step / zero point in FP64 as quantizer.hpp:169-201, codes on the
+    // fp32 pipe with the exact FP64 decision near ties (quant_code_f32, :205-210).
     for (int idx = tid; idx < MT * kpad / 4; idx += NWARP * 32) act[idx] = 0u;
     const int nvec = P.k >> 3;
-    const double top = static_cast<double>(P.qp.levels - 1);
 #pragma unroll
     for (int i = 0; i < XT; ++i) {
       if (i >= mb) break;  // uniform across the CTA
@@ -522,28 +559,37 @@ __global__ void __launch_bounds__(NWARP * 32, 1) gemv_imma_kernel(ImmaParams P) 
         lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
         hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
       }
-      __shared__ float q_lo[NWARP], q_hi[NWARP];
-      __shared__ long long q_sum[NWARP];
+      __shared__ float q_lo[NWARP], q_hi[NWARP], q_inv;
+      __shared__ int q_sum[NWARP];
       if (lane == 0) {
         q_lo[warp] = lo;
         q_hi[warp] = hi;
       }
       __syncthreads();
-      if (tid == 0) {
-        double l = q_lo[0], h = q_hi[0];
-        for (int w = 1; w < NWARP; ++w) {
-          l = fmin(l, static_cast<double>(q_lo[w]));
-          h = fmax(h, static_cast<double>(q_hi[w]));
+      if (trace && tid == 0 && i == 0) trace[10] = clock64();
+      if (warp == 0) {  // row range -> step, zero point, fp32 reciprocal (one thread)
+        // every lane loads (lane % NWARP): no divergence before the shuffles
+        float l = q_lo[lane & (NWARP - 1)], h = q_hi[lane & (NWARP - 1)];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          l = fminf(l, __shfl_xor_sync(0xffffffffu, l, o));
+          h = fmaxf(h, __shfl_xor_sync(0xffffffffu, h, o));
         }
-        double step;
-        int z;
-        group_params(P.qp, l, h, &step, &z);
-        s_sa[i] = step;
-        s_za[i] = z;
+        if (lane == 0) {
+          double step;
+          int z;
+          group_params(P.qp, l, h, &step, &z);
+          s_sa[i] = step;
+          s_za[i] = z;
+          q_inv = f32_reciprocal(step);
+        }
       }
       __syncthreads();
-      const double step = s_sa[i], zd = static_cast<double>(s_za[i]), inv = 1.0 / step;
-      long long rsum = 0;
+      if (trace && tid == 0 && i == 0) trace[11] = clock64();
+      const double step = s_sa[i];
+      const float inv32 = q_inv;
+      const int zi = static_cast<int>(s_za[i]), topi = static_cast<int>(P.qp.levels - 1);
+      int rsum = 0;  // <= 255 K
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
         const int idx = tid + r * NWARP * 32;
@@ -552,7 +598,7 @@ __global__ void __launch_bounds__(NWARP * 32, 1) gemv_imma_kernel(ImmaParams P) 
           uint32_t w0 = 0, w1 = 0;
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
-            const unsigned c = quant_code_fast(static_cast<double>(__half2float(hv[e])), step, inv, zd, top);
+            const unsigned c = quant_code_f32(__half2float(hv[e]), step, inv32, zi, topi);
             rsum += c;
             if (e < 4) w0 |= c << (8 * e);
             else w1 |= c << (8 * (e - 4));
@@ -561,13 +607,16 @@ __global__ void __launch_bounds__(NWARP * 32, 1) gemv_imma_kernel(ImmaParams P) 
           act[act_frag_index(2 * idx + 1, i, MT)] = w1;
         }
       }
-      rsum = warp_sum(rsum);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) rsum += __shfl_xor_sync(0xffffffffu, rsum, o);
       if (lane == 0) q_sum[warp] = rsum;
       __syncthreads();
-      if (tid == 0) {
-        long long rr = 0;
-        for (int w = 0; w < NWARP; ++w) rr += q_sum[w];
-        s_ra[i] = rr;
+      if (trace && tid == 0 && i == 0) trace[12] = clock64();
+      if (warp == 0) {
+        int rr = q_sum[lane & (NWARP - 1)] * (lane < NWARP ? 1 : 0);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) rr += __shfl_xor_sync(0xffffffffu, rr, o);
+        if (lane == 0) s_ra[i] = rr;
       }
     }
     if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0 && P.bad_out) {  // only CTA 0 reports
@@ -576,13 +625,35 @@ __global__ void __launch_bounds__(NWARP * 32, 1) gemv_imma_kernel(ImmaParams P) 
     }
   } else {
     griddep_wait();  // act_quant_kernel done and its writes visible
+    // codes (<= 64 KB: <= 8 x 16 B per thread) and stats requested into
+    // registers, then the rest of the weight ring, then the shared-memory stores
     const uint4* src = reinterpret_cast<const uint4*>(P.act_frag + static_cast<size_t>(blockIdx.y) * MT * kpad / 4);
     uint4* dst = reinterpret_cast<uint4*>(act);
-    for (int idx = tid; idx < MT * kpad / 16; idx += NWARP * 32) dst[idx] = __ldcg(src + idx);
+    constexpr int AR = 8;
+    const int nv = MT * kpad / 16;
+    uint4 av[AR];
+#pragma unroll
+    for (int r = 0; r < AR; ++r) {
+      const int idx = tid + r * NWARP * 32;
+      if (idx < nv) av[r] = __ldcg(src + idx);
+    }
+    double t_sa = 0.0;
+    long long t_za = 0, t_ra = 0;
     if (tid < mb) {
-      s_sa[tid] = P.s_a[tok0 + tid];
-      s_za[tid] = P.z_a[tok0 + tid];
-      s_ra[tid] = P.rowsum[tok0 + tid];
+      t_sa = P.s_a[tok0 + tid];
+      t_za = P.z_a[tok0 + tid];
+      t_ra = P.rowsum[tok0 + tid];
+    }
+    if (lane == 0) start_slots(first_slots, P.slots);
+#pragma unroll
+    for (int r = 0; r < AR; ++r) {
+      const int idx = tid + r * NWARP * 32;
+      if (idx < nv) dst[idx] = av[r];
+    }
+    if (tid < mb) {
+      s_sa[tid] = t_sa;
+      s_za[tid] = t_za;
+      s_ra[tid] = t_ra;
     }
     if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0 && P.bad_out) {
       const unsigned long long w = *P.bad_word;
@@ -591,6 +662,7 @@ __global__ void __launch_bounds__(NWARP * 32, 1) gemv_imma_kernel(ImmaParams P) 
     }
   }
   __syncthreads();
+  if (P.late_ring && !late_act && lane == 0) start_slots(0, P.slots);
   if (trace && tid == 0) trace[1] = clock64();
 
   // ---- 4. main loop over this warp's units (one body, TMA ring slots)
@@ -744,7 +816,10 @@ __global__ void __launch_bounds__(NWARP * 32, 1) gemv_imma_kernel(ImmaParams P) 
       atomicAdd(reinterpret_cast<unsigned long long*>(&gslot[(idx / mb) * 8 + idx % mb]),
                 static_cast<unsigned long long>(accs[(lrt * 16 + idx / mb) * MT + idx % mb]));
   }
-  if (trace && tid == 0) trace[3] = clock64();
+  if (trace && tid == 0) {
+    trace[3] = clock64();
+    trace[9] = gtimer();
+  }
   if (nsplit == 0) return;  // uniform across the CTA
   __syncthreads();
   // release: one gpu-scope fence by thread 0 after the CTA barrier orders every
@@ -999,8 +1074,10 @@ int run_gemv_imma_fused(const uint32_t* frag, unsigned q, size_t n, size_t k, si
   P.qp = qp;
   // m <= 2 fp16 per-token rows: ReQuant fused into every CTA's prologue (one
   // launch); otherwise a separate ReQuant kernel overlapped by PDL.
-  const bool fused = x_dtype == ABQ_F16 && !qp.per_tensor && m <= 2 && k % 8 == 0 &&
-                     k <= static_cast<size_t>(8 * 4 * imma_warps(P.q) * 32);
+  bool fused = x_dtype == ABQ_F16 && !qp.per_tensor && m <= 2 && k % 8 == 0 &&
+               k <= static_cast<size_t>(8 * 4 * imma_warps(P.q) * 32);
+  if (const char* env = std::getenv("ABQ_GEMV_FUSED")) fused = fused && env[0] == '1';
+  if (const char* env = std::getenv("ABQ_EXP_LATE_RING")) P.late_ring = env[0] == '1';
   if (fused) {
     P.x16 = static_cast<const __half*>(x);
   } else {

@@ -113,4 +113,29 @@ __device__ __forceinline__ unsigned quant_code_fast(double v, double step, doubl
   return static_cast<unsigned>(c);
 }
 
+// RN32(1/step) for quant_code_f32, or NaN (forcing its exact path) where the
+// fp32 reciprocal would lose precision (denormal) or overflow.
+__device__ __forceinline__ float f32_reciprocal(double step) {
+  return step > 0x1p-100 && step < 0x1p100 ? static_cast<float>(1.0 / step) : CUDART_NAN_F;
+}
+
+// Same result as quant_code for a value exactly representable in fp32 (fp16 /
+// fp32 activations without a compensation pair), on the fp32 pipe.
+// q = RN32(v * RN32(1/step)) is within |q| * 2^-22.9 of the reference's
+// RN64(v / step); round() only changes value across half-integers, so when q is
+// farther than |q| * 2^-21 from the nearest n + 1/2 both round to the same
+// integer r, which is then rint(q) (magic-number add, no conversion unit).
+// Otherwise -- or for |q| >= 2^22 -- the exact FP64 path decides.
+// z, top: integers in [0, 255] (group_params clamps the zero point).
+__device__ __forceinline__ unsigned quant_code_f32(float v, double step, float inv32, int z, int top) {
+  const float q = __fmul_rn(v, inv32);
+  const float t = __fadd_rn(q, 12582912.0f);  // 1.5 * 2^23: rint(q) in the low mantissa bits
+  const float r = __fsub_rn(t, 12582912.0f);
+  const float d = __fsub_rn(0.5f, fabsf(__fsub_rn(q, r)));  // distance to the nearest n + 1/2
+  if (!(fabsf(q) < 4194304.0f && d > fmaxf(fabsf(q), 1.0f) * 4.76837158203125e-07f))  // 2^22, 2^-21
+    return quant_code(static_cast<double>(v), step, static_cast<double>(z), static_cast<double>(top));
+  const int c = (__float_as_int(t) - 0x4B400000) + z;
+  return static_cast<unsigned>(c < 0 ? 0 : (c > top ? top : c));
+}
+
 }  // namespace abq_dev

@@ -67,3 +67,14 @@ def test_tc_variant_matches_popc(abq):
     finally:
         abq.api.set_gemv_variant("auto")
     assert torch.equal(tc, popc)
+
+
+@pytest.mark.parametrize("m,n,k,p,q", [(128, 1000, 4096, 4, 4), (37, 300, 1000, 8, 8), (128, 512, 2048, 8, 2),
+                                       (9, 77, 300, 2, 2)])
+def test_btc_gemm_matches_oracle(abq, orc, m, n, k, p, q):
+    """b1 tensor-core comparator (mma.sync m16n8k256 .b1 and.popc) is exact"""
+    rng = np.random.default_rng(m + n + k)
+    a = rng.integers(0, 1 << p, (m, k), dtype=np.uint8)
+    b = rng.integers(0, 1 << q, (n, k), dtype=np.uint8)
+    got = abq.gemm_btc(abq.bitpack(a, p), abq.bitpack(b, q)).cpu().numpy()
+    assert np.array_equal(got, orc.gemm_codes(a, p, b, q))

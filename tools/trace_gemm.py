@@ -1,0 +1,49 @@
+"""Phase timing (per CTA, SM clock) of the tcgen05 prefill GEMM: time to the
+first MMA, MMA issue progress every 8 k-blocks, epilogue, plus the device span
+of the launch (globaltimer).  Usage: python tools/trace_gemm.py [workload]"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_2408_08554_b200 as abq  # noqa: E402
+
+name = sys.argv[1] if len(sys.argv) > 1 else "cfg2_w4a4_m128"
+m, n, k, wb, ab, desc = bench.WORKLOADS[name]
+x_np, wc, sb, zb, ws = bench.build_layer(abq, torch, m, n, k, wb, ab, 2)
+spec = abq.QuantSpec(bits=ab, granularity=abq.api.PER_TOKEN)
+lins = [abq.Linear(w, spec, max_m=m) for w in ws]
+x = torch.from_numpy(x_np).cuda()
+y = torch.empty((m, n), dtype=torch.float16, device="cuda")
+buf = torch.zeros(16 * 4096, dtype=torch.int64, device="cuda")
+for _ in range(3):
+    lins[0](x, out=y, check=False)
+torch.cuda.synchronize()
+lib = abq._lib.lib()
+lib.abq_set_trace_buffer(buf.data_ptr())
+lins[1](x, out=y, check=False)
+torch.cuda.synchronize()
+lib.abq_set_trace_buffer(None)
+t = buf.view(-1, 16).cpu().numpy().astype(np.int64)
+t = t[t[:, 0] > 0]
+ghz = 1.965
+
+
+def us(a):
+    return a / ghz / 1e3
+
+
+print(f"{name}: {len(t)} CTAs")
+for j in range(6):
+    c = t[:, 10 + j]
+    ok = c > 0
+    if ok.any():
+        print(f"  MMA of k-block {8 * j:3d} issued   median {np.median(us(c[ok] - t[ok, 0])):7.2f} us after CTA start")
+print(f"  last MMA issued          median {np.median(us(t[:, 3] - t[:, 0])):7.2f} us")
+print(f"  epilogue start (done)    median {np.median(us(t[:, 4] - t[:, 0])):7.2f} us")
+print(f"  CTA end                  median {np.median(us(t[:, 5] - t[:, 0])):7.2f} us  max {us(t[:, 5] - t[:, 0]).max():7.2f}")
+print(f"  launch span (globaltimer) {(t[:, 9].max() - t[:, 8].min()) / 1e3:7.2f} us; CTA start skew "
+      f"{(t[:, 8].max() - t[:, 8].min()) / 1e3:6.2f} us")
