@@ -41,13 +41,15 @@
 //   * partial row-tile sums meet in shared memory (64-bit atomics) and, for the
 //     row-tiles cut between CTAs, in a self-cleaning global accumulator where
 //     the last contributing CTA runs the fused zero-point/dequant epilogue.
+#include <cstdlib>
+#include <cstring>
+
 #include "common.cuh"
 #include "quant_dev.cuh"
+#include "gemv_frag.cuh"
 
 namespace abq_dev {
 
-constexpr int kRowTile = 16;
-constexpr int kKBlock = 256;
 
 // ---------------------------------------------------------------------------
 // prepack: ABQP [q][n][wpr] -> fragment-major code slices [rt][kb][q][lane][4]
@@ -85,83 +87,6 @@ __global__ void prepack_frag_kernel(const uint64_t* __restrict__ planes, int q, 
     }
     frag[idx] = w;
   }
-}
-
-// ---------------------------------------------------------------------------
-// PTX helpers
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init1(uint64_t* bar) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "WAITG_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAITG_%=;\n\t}" ::"r"(smem_addr(bar)),
-      "r"(parity)
-      : "memory");
-}
-// 1-D TMA bulk copy global -> shared, completion counted on an mbarrier
-__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_addr(dst)),
-      "l"(src), "r"(bytes), "r"(smem_addr(bar))
-      : "memory");
-}
-__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;"); }
-
-__device__ __forceinline__ void imma_16832(int (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
-                                           uint32_t a3, uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};"
-      : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
-      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
-}
-
-// Byte-code register o (= 4c + u: chunk c, A register u) of a lane's unit from
-// its 4Q code-slice words (layout in prepack_frag_kernel / common.cuh):
-// one shift + one mask-merge per slice, all shifts compile-time constants.
-template <int Q>
-__device__ __forceinline__ uint32_t widen_slices(const uint4 (&w)[Q], int o) {
-  uint32_t r = 0;
-#pragma unroll
-  for (int i = 0; i < slice_count(Q); ++i) {
-    const int sw = slice_width(Q, i), so = slice_off(Q, i);
-    const int J = 4 * so + o % (4 * sw), sh = sw * (o / (4 * sw));
-    const uint4 v = w[J >> 2];
-    const uint32_t x = (J & 3) == 0 ? v.x : (J & 3) == 1 ? v.y : (J & 3) == 2 ? v.z : v.w;
-    const uint32_t m = static_cast<uint32_t>((1u << sw) - 1u) * 0x01010101u;
-    r |= so >= sh ? (x << (so - sh)) & (m << so) : (x >> (sh - so)) & (m << so);
-  }
-  return r;
-}
-
-// CTA that owns unit u under the even split (c*U)/G
-__device__ __forceinline__ int cta_of_unit(long long u, long long U, int G) {
-  return static_cast<int>(((u + 1) * G - 1) / U);
-}
-
-// u32 index of activation codes (k-group v of 4, token i) in B-fragment order:
-// [kb][c][token i][tig][h]   (kb = v/64, c = (v%64)/8, h = (v%8)/4, tig = v%4)
-__device__ __forceinline__ int act_frag_index(int v, int i, int mt) {
-  const int kb = v >> 6, rem = v & 63;
-  return ((((kb * 8 + (rem >> 3)) * mt + i) * 4 + (rem & 3)) * 2) + ((rem >> 2) & 1);
 }
 
 // ---------------------------------------------------------------------------
@@ -1043,6 +968,10 @@ int run_act_quant(const void* x, int x_dtype, size_t m, size_t k, int mt, const 
   return ABQ_OK;
 }
 
+int run_gemv_dec(const uint32_t* frag, unsigned q, size_t n, size_t k, size_t m, const void* x, int x_dtype,
+                 const QuantParams& qp, const EpiParams& e, void* ws, unsigned long long* bad_out,
+                 cudaStream_t st);
+
 // Serving path: act_quant_kernel (ReQuant into B-fragment codes) followed by the
 // stream-K GEMV with programmatic dependent launch.  `ws` must be
 // imma_ws_bytes(n, k) of zero-filled device memory (left zeroed).
@@ -1050,6 +979,11 @@ int run_gemv_imma_fused(const uint32_t* frag, unsigned q, size_t n, size_t k, si
                         int x_dtype, const QuantParams& qp, const EpiParams& e, void* ws,
                         unsigned long long* bad_out, cudaStream_t st) {
   if (m == 0 || n == 0) return ABQ_OK;
+  // the serving kernel is gemv_dec_kernel (gemv_dec.cu); ABQ_GEMV_KERNEL=imma
+  // selects this earlier per-warp-ring kernel for comparison
+  const char* kern_env = std::getenv("ABQ_GEMV_KERNEL");
+  if (!(kern_env && std::strcmp(kern_env, "imma") == 0))
+    return run_gemv_dec(frag, q, n, k, m, x, x_dtype, qp, e, ws, bad_out, st);
   ImmaParams P = base_params(frag, q, n, k, m, e);
   const int mt = pick_imma_mt(static_cast<int>(m));
   const size_t rowtiles = P.rowtiles;

@@ -138,4 +138,66 @@ __device__ __forceinline__ unsigned quant_code_f32(float v, double step, float i
   return static_cast<unsigned>(c < 0 ? 0 : (c > top ? top : c));
 }
 
+// Eight fp16 activations (one 16-byte vector) -> eight u8 codes (two words,
+// element e in byte e%4 of word e/4), all on the fp32 pipe; the exact FP64
+// path (quant_code) runs out of line, for the whole vector, only when one of
+// the eight is inside the tie band of quant_code_f32.  Returns the code sum.
+// (returns {word 0, word 1, code sum}; by value: a pointer argument would put
+// the words in local memory, and a local-memory miss behind the weight stream
+// costs a full memory round trip)
+static __device__ __noinline__ uint3 quant_codes8_exact(uint4 xv, double step, int z, int top) {
+  const __half* hv = reinterpret_cast<const __half*>(&xv);
+  uint3 r = make_uint3(0u, 0u, 0u);
+  for (int e = 0; e < 8; ++e) {
+    const unsigned c = quant_code(static_cast<double>(__half2float(hv[e])), step, static_cast<double>(z),
+                                  static_cast<double>(top));
+    r.z += c;
+    if (e < 4) r.x |= c << (8 * e);
+    else r.y |= c << (8 * (e - 4));
+  }
+  return r;
+}
+__device__ __forceinline__ int quant_codes8_f16(const uint4& xv, double step, float inv32, int z, int top,
+                                                uint32_t* w0, uint32_t* w1) {
+  const __half2* h2 = reinterpret_cast<const __half2*>(&xv);
+  int c[8];
+  bool ok = true;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float2 f = __half22float2(h2[e]);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const float v = h ? f.y : f.x;
+      const float q = __fmul_rn(v, inv32);
+      const float t = __fadd_rn(q, 12582912.0f);
+      const float r = __fsub_rn(t, 12582912.0f);
+      const float d = __fsub_rn(0.5f, fabsf(__fsub_rn(q, r)));
+      ok = ok && fabsf(q) < 4194304.0f && d > fmaxf(fabsf(q), 1.0f) * 4.76837158203125e-07f;
+      const int ci = (__float_as_int(t) - 0x4B400000) + z;
+      c[2 * e + h] = ci < 0 ? 0 : (ci > top ? top : ci);
+    }
+  }
+  if (!ok) {
+    const uint3 r = quant_codes8_exact(xv, step, z, top);
+    *w0 = r.x;
+    *w1 = r.y;
+    return static_cast<int>(r.z);
+  }
+  *w0 = static_cast<uint32_t>(c[0]) | (static_cast<uint32_t>(c[1]) << 8) | (static_cast<uint32_t>(c[2]) << 16) |
+        (static_cast<uint32_t>(c[3]) << 24);
+  *w1 = static_cast<uint32_t>(c[4]) | (static_cast<uint32_t>(c[5]) << 8) | (static_cast<uint32_t>(c[6]) << 16) |
+        (static_cast<uint32_t>(c[7]) << 24);
+  return c[0] + c[1] + c[2] + c[3] + c[4] + c[5] + c[6] + c[7];
+}
+
+// nonzero iff one of the eight fp16 values is Inf or NaN (exponent all ones)
+__device__ __forceinline__ uint32_t f16x8_nonfinite(const uint4& v) {
+  const uint32_t m = 0x7C007C00u;
+  auto one = [&](uint32_t w) {
+    const uint32_t e = w & m;
+    return static_cast<uint32_t>((e & 0xFFFFu) == 0x7C00u) | static_cast<uint32_t>((e >> 16) == 0x7C00u);
+  };
+  return one(v.x) | one(v.y) | one(v.z) | one(v.w);
+}
+
 }  // namespace abq_dev
