@@ -307,6 +307,9 @@ def run_ours(args, world, rank, local):
             w.tc = None
     spec = abq.QuantSpec(bits=ab, granularity=abq.api.PER_TOKEN)
     lins = [abq.Linear(w, spec, max_m=m) for w in weights]
+    if not args.no_prefetch_next:  # the layer sequence is known: hint each layer's successor
+        for i, lin in enumerate(lins):
+            lin.prefetch_next(lins[(i + 1) % len(lins)])
     x = torch.from_numpy(x_np).cuda()
     y = torch.empty((m, n), dtype=torch.float16, device="cuda")
 
@@ -349,7 +352,7 @@ def run_ours(args, world, rank, local):
     fused = per_step == 1
     if fused:
         kernel_us = ms_per_step * 1e3
-        kernel_name = "gemv_imma_kernel (ReQuant prologue + tensor-pipe plane GEMV + epilogue)"
+        kernel_name = "gemv_dec_kernel (ReQuant prologue + tensor-pipe plane GEMV + epilogue)"
     else:
         a_planes, sa, za, ra = abq.api.quant_pack_act(x, spec)
         kms, _ = time_graph(torch, lambda i: abq.linear_planes(a_planes, sa, za, ra, weights[i], out=y),
@@ -441,7 +444,8 @@ def run_ours(args, world, rank, local):
                    "parallelism": f"N-sharded x{world} (column-parallel)" if world > 1 else "single",
                    "l2": f"rotating {copies} packed-weight copies ({copies * wbytes / 1e6:.0f} MB > 4x L2)",
                    "step": "fp16 x -> ReQuant+BitPack -> plane GEMV -> zero-point+dequant -> fp16 y",
-                   "graph": "CUDA graph replay"},
+                   "graph": "CUDA graph replay",
+                   "prefetch_next": not args.no_prefetch_next},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches,
         "launches_per_step": per_step, "clocks": clk, "parity": "bit-exact vs oracle" if parity else None,
         "allgather": gather,
@@ -503,6 +507,8 @@ def main():
     ap.add_argument("--sweep", action="store_true")
     ap.add_argument("--no-check", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-prefetch-next", action="store_true",
+                    help="do not give each layer its successor as an L2 prefetch hint")
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--variant", default="auto", choices=["auto", "popc", "recomb"],
                     help="decode GEMV: auto | popc (AND+popcount) | recomb (planes on the int8 tensor pipe)")

@@ -94,6 +94,13 @@ typedef struct {
   /* optional tcgen05-GEMM copy of the planes (abq_weights_prepack_tc) used
    * for M >= 9 tokens; NULL = no prefill tensor-core path */
   const uint32_t* tc;
+  /* optional L2 prefetch hint for the decode GEMV: the fragment-major weights
+   * (frag) of the layer that runs after this one and their byte count.  The
+   * GEMV streams them into L2 (evict-first) behind its own weights, so the
+   * next layer's input-independent weight traffic overlaps this layer's
+   * activation-dependent work.  NULL = no hint. */
+  const void* prefetch_next;
+  size_t prefetch_next_bytes;
 } abq_weights;
 
 /* Activation-side metadata produced by abq_quant_pack_act (per-token or

@@ -39,7 +39,8 @@ class GemmStatsC(C.Structure):
 class WeightsC(C.Structure):
     _fields_ = [("planes", C.c_void_p), ("q", C.c_uint), ("n", C.c_size_t), ("k", C.c_size_t),
                 ("scales", C.c_void_p), ("zero_points", C.c_void_p), ("colsums", C.c_void_p),
-                ("per_tensor", C.c_int), ("frag", C.c_void_p), ("tc", C.c_void_p)]
+                ("per_tensor", C.c_int), ("frag", C.c_void_p), ("tc", C.c_void_p),
+                ("prefetch_next", C.c_void_p), ("prefetch_next_bytes", C.c_size_t)]
 
 
 class ActC(C.Structure):

@@ -91,7 +91,8 @@ int run_gemv_imma_planes(const uint32_t* frag, unsigned q, size_t n, size_t k, s
                          const uint64_t* a_planes, unsigned p, const EpiParams& e, cudaStream_t st);
 int run_gemv_imma_fused(const uint32_t* frag, unsigned q, size_t n, size_t k, size_t m, const void* x,
                         int x_dtype, const QuantParams& qp, const EpiParams& e, void* ws,
-                        unsigned long long* bad_out, cudaStream_t st);
+                        unsigned long long* bad_out, cudaStream_t st, const void* next_frag,
+                        size_t next_bytes);
 
 int run_gemm_bmma(const uint64_t* a, unsigned p, size_t m, const uint64_t* w, unsigned q, size_t n, size_t k,
                   int32_t* out, cudaStream_t st);
@@ -585,7 +586,8 @@ int abq_linear(const void* x, int x_dtype, size_t m, size_t k, const abq_quant_s
     e.colsum_b = w->colsums;
     e.k = static_cast<long long>(k);
     const QuantParams qp = params_of(*act_spec);
-    st = run_gemv_imma_fused(w->frag, w->q, w->n, k, m, x, x_dtype, qp, e, ws_imma, bad, s);
+    st = run_gemv_imma_fused(w->frag, w->q, w->n, k, m, x, x_dtype, qp, e, ws_imma, bad, s, w->prefetch_next,
+                             w->prefetch_next ? w->prefetch_next_bytes : 0);
     if (st) return st;
   } else if (use_tc(w, m, k, !fits_int32_host(p, w->q, k))) {
     // ReQuant straight to u8 codes (K1), then the tcgen05 GEMM with the fused epilogue

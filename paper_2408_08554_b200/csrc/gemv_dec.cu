@@ -11,29 +11,21 @@
 // q x 512 contiguous bytes, units ordered row-tile-major.  Same byte count as
 // the ABQP planes.
 //
-// Designed around three measurements (profiles/r01_microbench_burst.txt,
-// profiles/r01_trace_gemv.txt):
-//  * a memory access issued by an SM while ~200 KB per SM of weight stream is
-//    queued waits ~0.8 us even when it hits L2 (64 KB in flight: ~0.33 us), so
-//    the kernel keeps a bounded ring (~64-96 KB per CTA) and issues every
-//    prologue load (parameters, per-channel epilogue values, activations) in
-//    one batch;
-//  * back-to-back launches lose ~1.5-2 us each to launch + ramp; with
-//    programmatic dependent launch and two co-resident CTAs per SM the next
-//    layer's CTA starts streaming its (input-independent) weights during this
-//    layer's tail -- it only waits (griddepcontrol.wait) before it reads the
-//    activations and before it writes anything;
-//  * a single IMMA accumulator chain per warp runs at ~45 cycles per IMMA;
-//    four independent chains per warp.
-//
-// CTA = 8 consumer warps + 1 producer warp.  The producer streams the CTA's
-// contiguous unit range [U0, U1) (stream-K split, balanced to one unit)
-// through a ring of S slots of 8 units with 1-D TMA bulk copies (full / empty
-// mbarriers); consumer warp w multiplies unit w of every slot on the int8
-// tensor pipe (legacy IMMA m16n8k32: 16 weight rows x 32 k x 8 tokens).
-// Row-tile partial sums meet in shared memory; the (at most two) row-tiles cut
-// between CTAs meet in a self-cleaning global accumulator and the last
-// contributing CTA runs the epilogue for them.
+// Shape of the kernel (measurements: profiles/r01_microbench_burst.txt,
+// r01_microbench_sync.txt, r01_trace_dec_*.txt):
+//  * each CTA owns whole row-tiles (no cross-CTA reduction) and, first thing,
+//    asks L2 to prefetch its entire weight range with bulk prefetches
+//    (cp.async.bulk.prefetch.L2, evict-first): HBM streams at full rate while
+//    the CTA quantizes the activations, with no shared-memory or register
+//    cost; the weights are then read with 16-byte loads that hit L2;
+//  * 16 warps, one IMMA m16n8k32 (16 weight rows x 32 k x 8 tokens) stream
+//    per warp over units U0 + warp + 16 j, D units of loads in flight per warp;
+//  * power-of-two code slices (q = 1, 2, 4, 8) are fed to IMMA as raw masked
+//    bytes (w & (mask << w*f)): one ALU op per A register, the field's 2^(w f)
+//    scale divided out exactly at the row-tile flush; other q widen the slices
+//    to byte codes;
+//  * launches are programmatic-dependent: parameters and weights are fetched
+//    before griddepcontrol.wait, the activations after it.
 #include <algorithm>
 #include <cstdlib>
 
@@ -43,15 +35,14 @@
 
 namespace abq_dev {
 
-constexpr int kDecWarps = 16;  // consumer warps (4 per SM sub-partition: the loop is latency-bound)
-constexpr int kDecUPS = 8;     // units per ring slot = consumer warps sharing one slot
-constexpr int kDecThreads = (kDecWarps + 1) * 32;
+constexpr int kDecWarps = 16;  // 4 per SM sub-partition, <= 128 registers each
+constexpr int kDecUPS = 8;     // units per ring slot = warps sharing a slot
+constexpr int kDecThreads = kDecWarps * 32;
 
 struct DecParams {
   const uint32_t* frag;
   int q, n, k, rowtiles, kblocks, m;
-  int slots;       // ring slots of kDecUPS units
-  int U;           // rowtiles * kblocks
+  int U;  // rowtiles * kblocks
   // activations: fp16 rows quantized in the prologue, or codes + stats written
   // by act_quant_kernel (the PDL primary of this launch)
   const __half* x16;
@@ -61,23 +52,22 @@ struct DecParams {
   const long long* rowsum;
   QuantParams qp;
   EpiParams e;
-  long long* gacc;               // [rowtiles][16][8] int64, zero on entry and exit
-  unsigned* gcnt;                // [rowtiles], zero on entry and exit
   unsigned long long* bad_word;  // non-finite input report (see run_gemv_dec)
   unsigned long long* bad_out;
   unsigned long long* trace;     // optional [grid][64] stamps (tools/trace_dec.py)
-  int rowsplit;                  // 1: CTAs own whole row-tiles (no cross-CTA sums); 0: stream-K
+  int prefetch;                  // L2 bulk prefetch of the CTA's weights (default 1)
+  int slots;                     // TMA ring slots of kDecUPS units
+  const unsigned char* next_frag;  // L2 prefetch hint: the next layer's weights (or null)
+  size_t next_bytes;
 };
 
+// named barrier over the consumer warps (the producer never joins)
+__device__ __forceinline__ void cta_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kDecWarps * 32) : "memory"); }
 __device__ __forceinline__ void mbar_init_n(uint64_t* bar, unsigned n) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(n));
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
-}
-// named barrier over the consumer warps only (the producer never joins)
-__device__ __forceinline__ void consumers_sync() {
-  asm volatile("bar.sync 1, %0;" ::"n"(kDecWarps * 32) : "memory");
 }
 
 struct DecSmem {  // carve-up of the dynamic shared memory (host and device agree)
@@ -86,8 +76,8 @@ struct DecSmem {  // carve-up of the dynamic shared memory (host and device agre
 __host__ __device__ inline DecSmem dec_smem(int q, int slots, int mt, int kpad, int nlrt_max) {
   DecSmem s;
   s.ring = 0;
-  s.bars = s.ring + static_cast<size_t>(slots) * kDecUPS * q * 512;
-  s.act = s.bars + static_cast<size_t>(2 * slots) * 8;
+  s.bars = static_cast<size_t>(slots) * kDecUPS * q * 512;
+  s.act = s.bars + static_cast<size_t>(2 * slots) * 8;  // full barriers + release counters
   s.accs = (s.act + static_cast<size_t>(mt) * kpad + 15) & ~size_t(15);
   s.csb = (s.accs + static_cast<size_t>(nlrt_max) * 16 * mt * 4 + 15) & ~size_t(15);
   s.czb = s.csb + static_cast<size_t>(nlrt_max) * 16 * 8;
@@ -95,8 +85,11 @@ __host__ __device__ inline DecSmem dec_smem(int q, int slots, int mt, int kpad, 
   s.total = s.ccs + static_cast<size_t>(nlrt_max) * 16 * 8;
   return s;
 }
-__host__ __device__ inline int dec_nlrt_max(int U, int grid, int kblocks) {
-  return (U + grid - 1) / grid / kblocks + 2;
+__host__ __device__ inline int dec_nlrt_max(int rowtiles, int grid) { return (rowtiles + grid - 1) / grid + 1; }
+
+__device__ __forceinline__ void l2_prefetch_bulk(const void* p, uint32_t bytes, uint64_t pol) {
+  asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(p), "r"(bytes), "l"(pol)
+               : "memory");
 }
 
 // non-finite inputs of one thread's vectors -> atomicMax(~flat index) (the
@@ -112,109 +105,115 @@ static __device__ __noinline__ void report_nonfinite_f16(const uint4* xr, int t,
   }
 }
 
-template <int QT, int MT, int MINB>
-__global__ void __launch_bounds__(kDecThreads, MINB) gemv_dec_kernel(const __grid_constant__ DecParams Pc) {
+template <int QT, int MT>
+__global__ void __launch_bounds__(kDecThreads, 1) gemv_dec_kernel(const __grid_constant__ DecParams Pc) {
   constexpr int NW = kDecWarps, UPS = kDecUPS, NG = NW / UPS;
   constexpr int unit_bytes = QT * 512;
   constexpr int slot_bytes = UPS * unit_bytes;
+  constexpr bool RAW = (QT & (QT - 1)) == 0;  // q in {1, 2, 4, 8}: raw masked fields
+  constexpr int NF = RAW ? 8 / QT : 1;         // fields (scales) per byte lane
+  constexpr int NA = NF >= 2 ? NF : 2;         // accumulator sets (>= 2 independent chains)
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ __align__(16) DecParams P;  // consumers' copy of the parameter block (below)
+  __shared__ __align__(16) DecParams P;
   __shared__ float r_lo[NW], r_hi[NW];
   __shared__ int r_sum[NW];
   __shared__ double s_sa[MT];
   __shared__ long long s_za[MT], s_ra[MT];
   __shared__ float s_inv[MT];
-  __shared__ int s_last;
   __shared__ long long s_wend;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   asm volatile("griddepcontrol.launch_dependents;");
 
-  // this CTA's unit range: whole row-tiles, or an even stream-K share
-  // Scalars of the parameter block go through a warp shuffle: left to itself
-  // ptxas re-reads them from the constant bank inside the loops (LDC on every
-  // iteration), and a constant-cache miss behind the weight stream costs a
-  // memory round trip.
-  const int G = gridDim.x, U = __shfl_sync(0xffffffffu, Pc.U, 0), kblocks = __shfl_sync(0xffffffffu, Pc.kblocks, 0);
-  const int S = __shfl_sync(0xffffffffu, Pc.slots, 0), rowsplit = __shfl_sync(0xffffffffu, Pc.rowsplit, 0);
-  const int rowtiles = __shfl_sync(0xffffffffu, Pc.rowtiles, 0);
-  const int kpad = kblocks * kKBlock;
-  int U0, U1;
-  if (rowsplit) {
-    U0 = static_cast<int>(static_cast<long long>(blockIdx.x) * rowtiles / G) * kblocks;
-    U1 = static_cast<int>(static_cast<long long>(blockIdx.x + 1) * rowtiles / G) * kblocks;
-  } else {
-    U0 = static_cast<int>(static_cast<long long>(blockIdx.x) * U / G);
-    U1 = static_cast<int>(static_cast<long long>(blockIdx.x + 1) * U / G);
-  }
+  // ---- 0. this CTA's row-tiles [rt_first, rt_end) = units [U0, U1)
+  const int G = gridDim.x;
+  const int rowtiles = Pc.rowtiles, kblocks = Pc.kblocks, S = Pc.slots;
+  // (blockIdx.x + 1) * rowtiles < 2^31 for any N the engine accepts: 32-bit math
+  const int rt_first = static_cast<int>((blockIdx.x * static_cast<unsigned>(rowtiles)) / G);
+  const int rt_end = static_cast<int>(((blockIdx.x + 1) * static_cast<unsigned>(rowtiles)) / G);
+  const int U0 = rt_first * kblocks, U1 = rt_end * kblocks;
+  const int nlrt = rt_end - rt_first;
   const int nsl = (U1 - U0 + UPS - 1) / UPS;
-  const DecSmem L = dec_smem(QT, S, MT, kpad, dec_nlrt_max(U, G, kblocks));
+  const int kpad = kblocks * kKBlock;
+  const DecSmem L = dec_smem(QT, S, MT, kpad, dec_nlrt_max(rowtiles, G));
   unsigned char* ring = smem + L.ring;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bars);
-  uint64_t* empty = full + S;
+  unsigned* relcnt = reinterpret_cast<unsigned*>(full + S);  // warps done with each slot
 
-  // ======================= producer warp: the weight stream ==================
-  // Starts at once, from the constant bank; the consumers meet it at named
-  // barrier 2 (its arrival publishes the mbarrier initialisation).
-  if (warp == NW) {
-    if (lane == 0) {
-      for (int s = 0; s < S; ++s) {
-        mbar_init_n(&full[s], 1);
-        mbar_init_n(&empty[s], UPS);
-      }
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  // ---- ring set-up by thread 0: full barriers, then (after the CTA barrier
+  // below) the L2 bulk prefetch of the CTA's weights and of the next layer's,
+  // and the first S slots.  Later slots are refilled by the last warp to
+  // release a slot (release() below): no producer warp, so 16 warps x 128
+  // registers fit the SM.
+  const unsigned char* wsrc = reinterpret_cast<const unsigned char*>(Pc.frag) + static_cast<size_t>(U0) * unit_bytes;
+  const uint64_t pol = l2_evict_first_policy();
+  auto issue_slot = [&](int i, int sl) {  // thread-level: TMA of slot index i into ring slot sl
+    const int nu = min(UPS, U1 - U0 - i * UPS);
+    const uint32_t bytes = static_cast<uint32_t>(nu * unit_bytes);
+    mbar_expect_tx(&full[sl], bytes);
+    tma_bulk_g2s_hint(ring + static_cast<size_t>(sl) * slot_bytes, wsrc + static_cast<size_t>(i) * slot_bytes, bytes,
+                      &full[sl], pol);
+  };
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init_n(&full[s], 1);
+      relcnt[s] = 0;
     }
-    __syncwarp();
-    asm volatile("bar.arrive 2, %0;" ::"n"(kDecThreads) : "memory");
-    if (lane == 0) {
-      const unsigned char* src = reinterpret_cast<const unsigned char*>(Pc.frag) + static_cast<size_t>(U0) * unit_bytes;
-      const uint64_t pol = l2_evict_first_policy();
-      int s = 0;
-      uint32_t ph = 0;
-      for (int i = 0; i < nsl; ++i) {
-        if (i >= S) mbar_wait_parity(&empty[s], ph ^ 1u);
-        const int nu = min(UPS, U1 - U0 - i * UPS);
-        const uint32_t bytes = static_cast<uint32_t>(nu * unit_bytes);
-        mbar_expect_tx(&full[s], bytes);
-        tma_bulk_g2s_hint(ring + static_cast<size_t>(s) * slot_bytes, src + static_cast<size_t>(i) * slot_bytes,
-                          bytes, &full[s], pol);
-        if (++s == S) {
-          s = 0;
-          ph ^= 1u;
-        }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int i = 0; i < S && i < nsl; ++i) issue_slot(i, i);
+    const size_t total = static_cast<size_t>(U1 - U0) * unit_bytes;
+    if (Pc.prefetch) {
+      for (size_t off = static_cast<size_t>(S) * slot_bytes; off < total; off += 32768)
+        l2_prefetch_bulk(wsrc + off, static_cast<uint32_t>(total - off < 32768 ? total - off : 32768), pol);
+      // the next layer's weights (input-independent) stream into L2 behind ours
+      if (Pc.next_frag) {
+        const size_t nb = Pc.next_bytes, lo = (nb * blockIdx.x / G) & ~size_t(15),
+                     hi = (nb * (blockIdx.x + 1) / G) & ~size_t(15);
+        for (size_t off = lo; off < hi; off += 32768)
+          l2_prefetch_bulk(Pc.next_frag + off, static_cast<uint32_t>(hi - off < 32768 ? hi - off : 32768), pol);
       }
     }
-    return;
   }
 
-  // consumers: the parameter block to shared memory, all threads at once (read
-  // lazily from the constant bank, each first touch of a constant-cache line
-  // would be a separate memory round trip behind the weight stream)
+  // ======================= consumer warps ====================================
+  // this thread's epilogue channel parameters (<= 1 channel per thread here;
+  // more are loaded below), requested first
+  const bool dequant = Pc.e.mode != EPI_ACC_I32 && Pc.e.mode != EPI_ACC_I64;
+  const int pj = rt_first * kRowTile + tid;
+  const bool has_p = dequant && tid < nlrt * 16 && pj < Pc.n;
+  double p_sb = 0.0;
+  long long p_zb = 0, p_cs = 0;
+  if (has_p) {
+    p_sb = Pc.e.s_b[static_cast<size_t>(pj) * Pc.e.sb_stride];
+    p_zb = Pc.e.z_b[static_cast<size_t>(pj) * Pc.e.zb_stride];
+    p_cs = Pc.e.colsum_b[pj];
+  }
+
+  // ---- 1. parameter block to shared memory (all threads at once; read lazily
+  // from the constant bank, every first touch of a line would be a separate
+  // round trip), epilogue parameters of this CTA's channels
   for (int i = tid; i < static_cast<int>(sizeof(DecParams) / 4); i += NW * 32)
     reinterpret_cast<uint32_t*>(&P)[i] = reinterpret_cast<const uint32_t*>(&Pc)[i];
-  asm volatile("bar.sync 2, %0;" ::"n"(kDecThreads) : "memory");
+  __syncthreads();  // parameter block and barrier initialisation visible
   unsigned long long* trace = P.trace ? P.trace + 64 * blockIdx.x : nullptr;
   if (trace && tid == 0) {
     trace[0] = clock64();
     trace[8] = gtimer();
     s_wend = 0;
   }
-  const int rt_first = U0 / kblocks;
-  const int rt_last = U1 > U0 ? (U1 - 1) / kblocks : rt_first - 1;
-  const int nlrt = rt_last - rt_first + 1;
   uint32_t* act = reinterpret_cast<uint32_t*>(smem + L.act);
   uint32_t* accs = reinterpret_cast<uint32_t*>(smem + L.accs);
   double* c_sb = reinterpret_cast<double*>(smem + L.csb);
   long long* c_zb = reinterpret_cast<long long*>(smem + L.czb);
   long long* c_cs = reinterpret_cast<long long*>(smem + L.ccs);
-
-  // ======================= consumer warps ===================================
-  const bool dequant = P.e.mode != EPI_ACC_I32 && P.e.mode != EPI_ACC_I64;
   const int tok_n = min(MT, P.m);
-  // ---- prologue loads, one batch: epilogue parameters of this CTA's channels
-  // (weight side: legal before the dependency wait) ...
   constexpr int kCT = NW * 32;
-  for (int idx = tid; dequant && idx < nlrt * 16; idx += kCT) {
+  if (has_p) {
+    c_sb[tid] = p_sb;
+    c_zb[tid] = p_zb;
+    c_cs[tid] = p_cs;
+  }
+  for (int idx = tid + kCT; dequant && idx < nlrt * 16; idx += kCT) {
     const int j = rt_first * kRowTile + idx;
     if (j < P.n) {
       c_sb[idx] = P.e.s_b[static_cast<size_t>(j) * P.e.sb_stride];
@@ -227,18 +226,20 @@ __global__ void __launch_bounds__(kDecThreads, MINB) gemv_dec_kernel(const __gri
     const int k4 = P.k >> 2, ntail = (kpad >> 2) - k4;
     for (int idx = tid; idx < ntail * MT; idx += kCT) act[act_frag_index(k4 + idx / MT, idx % MT, MT)] = 0u;
   }
-  // ... then the activations, which the previous kernel may still be producing
+  // ---- 2. the activations, which the previous kernel may still be producing
   asm volatile("griddepcontrol.wait;" ::: "memory");
   if (trace && tid == 0) trace[4] = clock64();
 
   if (P.x16) {
-    // Fused ReQuant, per token, fp16 rows (K % 8 == 0, K <= 64 * TPT: the
+    // Fused ReQuant, per token, fp16 rows (K % 8 == 0, K <= 32 * TPT: the
     // host routes longer rows through act_quant_kernel).  GT warps per token;
-    // each thread loads its (<= 8) 16-byte vectors of the row in one batch and
-    // keeps them in registers for both passes.
+    // each thread loads its (<= XR) 16-byte vectors of the row in one batch.
+    // One CTA barrier for the range; every warp then derives step / zero point
+    // itself (no second barrier), codes go to shared memory and the code sum to
+    // a shared atomic, and the barrier before the main loop publishes both.
     constexpr int GT = NW / MT;  // MT is a power of two <= NW
     constexpr int TPT = GT * 32;
-    constexpr int XR = 8;
+    constexpr int XR = 4;
     const int t = warp / GT;
     const int l = (warp % GT) * 32 + lane;
     const int nvec = P.k >> 3;
@@ -250,71 +251,74 @@ __global__ void __launch_bounds__(kDecThreads, MINB) gemv_dec_kernel(const __gri
       const int v = l + r * TPT;
       xv[r] = active && v < nvec ? __ldg(xr + v) : make_uint4(0u, 0u, 0u, 0u);
     }
-    float lo = CUDART_INF_F, hi = -CUDART_INF_F;
+    // min / max in the order-preserving integer image of fp32 (exact for fp16
+    // inputs): one REDUX per warp instead of a shuffle tree
+    auto ord = [](float f) {
+      const int b = __float_as_int(f);
+      return b >= 0 ? b : b ^ 0x7FFFFFFF;
+    };
+    auto unord = [](int o) { return __int_as_float(o >= 0 ? o : o ^ 0x7FFFFFFF); };
+    int lo = 0x7FFFFFFF, hi = static_cast<int>(0x80000000u);
     uint32_t bad = 0;
 #pragma unroll
     for (int r = 0; r < XR; ++r) {
       if (!active || l + r * TPT >= nvec) break;
       bad |= f16x8_nonfinite(xv[r]);
       const __half2* h2 = reinterpret_cast<const __half2*>(&xv[r]);
+      __half2 mn = h2[0], mx = h2[0];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float2 f = __half22float2(h2[e]);
-        lo = fminf(lo, fminf(f.x, f.y));
-        hi = fmaxf(hi, fmaxf(f.x, f.y));
+      for (int e = 1; e < 4; ++e) {
+        mn = __hmin2(mn, h2[e]);
+        mx = __hmax2(mx, h2[e]);
       }
+      lo = min(lo, min(ord(__low2float(mn)), ord(__high2float(mn))));
+      hi = max(hi, max(ord(__low2float(mx)), ord(__high2float(mx))));
     }
     const bool report = blockIdx.x == 0 && P.bad_out != nullptr;
     if (report && bad) report_nonfinite_f16(xr, t, l, TPT, nvec, P.k, P.bad_word);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-      hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-    }
+    lo = __reduce_min_sync(0xffffffffu, lo);
+    hi = __reduce_max_sync(0xffffffffu, hi);
     if (lane == 0) {
-      r_lo[warp] = lo;
-      r_hi[warp] = hi;
+      r_lo[warp] = __int_as_float(lo);  // raw bits: decoded below
+      r_hi[warp] = __int_as_float(hi);
+      if (warp % GT == 0) s_ra[t] = 0;
     }
-    consumers_sync();
+    cta_sync();
     if (trace && tid == 0) trace[5] = clock64();
-    if (active && warp % GT == 0 && lane == 0) {
-      float l2 = r_lo[warp], h2 = r_hi[warp];
-      for (int w = 1; w < GT; ++w) {
-        l2 = fminf(l2, r_lo[warp + w]);
-        h2 = fmaxf(h2, r_hi[warp + w]);
-      }
-      double step;
-      int z;
-      group_params(P.qp, l2, h2, &step, &z);
-      s_sa[t] = step;
-      s_za[t] = z;
-      s_inv[t] = f32_reciprocal(step);
-    }
-    consumers_sync();
-    if (trace && tid == 0) trace[6] = clock64();
     int rsum = 0;
     if (active) {
-      const double step = s_sa[t];
-      const float inv32 = s_inv[t];
-      const int zi = static_cast<int>(s_za[t]), topi = static_cast<int>(P.qp.levels - 1);
+      const int base = warp - warp % GT;  // first warp of this token
+      int l2 = lane < GT ? __float_as_int(r_lo[base + lane]) : 0x7FFFFFFF;
+      int h2 = lane < GT ? __float_as_int(r_hi[base + lane]) : static_cast<int>(0x80000000u);
+      l2 = __reduce_min_sync(0xffffffffu, l2);
+      h2 = __reduce_max_sync(0xffffffffu, h2);
+      // step / zero point in FP64 (quantizer.hpp:169-201) by lane 0 of every
+      // warp of the token (identical inputs, identical results), broadcast
+      double step = 0.0;
+      int z = 0;
+      float inv32 = 0.0f;
+      if (lane < 2) group_params(P.qp, unord(l2), unord(h2), &step, &z);
+      if (lane == 1) inv32 = f32_reciprocal(step);  // lane 0 finishes z meanwhile
+      step = __shfl_sync(0xffffffffu, step, 0);
+      z = __shfl_sync(0xffffffffu, z, 0);
+      inv32 = __shfl_sync(0xffffffffu, inv32, 1);
+      if (warp == base && lane == 0) {
+        s_sa[t] = step;
+        s_za[t] = z;
+      }
+      if (trace && tid == 0) trace[6] = clock64();
+      const int topi = static_cast<int>(P.qp.levels - 1);
 #pragma unroll
       for (int r = 0; r < XR; ++r) {
         const int v = l + r * TPT;
         if (v >= nvec) break;
         uint32_t w0, w1;
-        rsum += quant_codes8_f16(xv[r], step, inv32, zi, topi, &w0, &w1);
+        rsum += quant_codes8_f16(xv[r], step, inv32, z, topi, &w0, &w1);
         act[act_frag_index(2 * v, t, MT)] = w0;
         act[act_frag_index(2 * v + 1, t, MT)] = w1;
       }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) rsum += __shfl_xor_sync(0xffffffffu, rsum, o);
-    if (lane == 0) r_sum[warp] = rsum;
-    consumers_sync();
-    if (active && warp % GT == 0 && lane == 0) {
-      long long rr = 0;
-      for (int w = 0; w < GT; ++w) rr += r_sum[warp + w];
-      s_ra[t] = rr;
+      rsum = __reduce_add_sync(0xffffffffu, rsum);  // < 2^31: <= 255 * 65536
+      if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&s_ra[t]), static_cast<unsigned long long>(rsum));
     }
     if (report && tid == 0) {
       const unsigned long long w = atomicExch(P.bad_word, 0ull);
@@ -337,205 +341,207 @@ __global__ void __launch_bounds__(kDecThreads, MINB) gemv_dec_kernel(const __gri
       *P.bad_word = 0ull;
     }
   }
-  consumers_sync();
+  cta_sync();
   if (trace && tid == 0) trace[1] = clock64();
 
-  // ---- main loop.  Slot i holds units U0 + i*UPS .. +UPS-1; warp group
-  // grp = warp / UPS takes the slots i = grp (mod NG), warp w % UPS its unit.
-  // Two register buffers: the next slot's weights are requested before the
-  // current unit's IMMAs issue.  No parameter-block reads in here.
+  // ---- 3. main loop over the TMA ring.
+  // Warp group grp = warp / UPS takes the slots i = grp (mod NG), warp % UPS
+  // its unit of each.  Per unit: the weights come from shared memory into one
+  // of two register buffers (the next unit's are requested before this
+  // unit's IMMAs issue), the IMMAs accumulate into one of two accumulator
+  // sets, and the other set -- the previous unit's -- is folded into the
+  // row-tile sums AFTER these IMMAs are issued, so consecutive units' IMMA
+  // chains overlap instead of serialising on the flush.
   const int g = lane >> 2, tig = lane & 3;
-  const int grp = warp / UPS, wi = warp % UPS;
-  int acc[4][4];
-#pragma unroll
-  for (int c = 0; c < 4; ++c)
-#pragma unroll
-    for (int r = 0; r < 4; ++r) acc[c][r] = 0;
-  auto flush = [&](int r_t) {
-    const int lrt = r_t - rt_first;
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      // the true row-tile sum is < 2^32 (K <= 65536, codes <= 255): exact as unsigned
-      const uint32_t v = static_cast<uint32_t>(acc[0][r]) + static_cast<uint32_t>(acc[1][r]) +
-                         static_cast<uint32_t>(acc[2][r]) + static_cast<uint32_t>(acc[3][r]);
-      acc[0][r] = acc[1][r] = acc[2][r] = acc[3][r] = 0;
-      const int row = g + 8 * (r >> 1), tok = 2 * tig + (r & 1);
-      if (tok < tok_n) atomicAdd(&accs[(lrt * 16 + row) * MT + tok], v);
-    }
-  };
-  const uint32_t ring_lane = smem_addr(ring) + wi * unit_bytes + lane * 16;
   const uint32_t act_lane = smem_addr(act) + ((g * 4 + tig) * 8);  // B-fragment word pair of (g, tig)
   const bool has_b = g < MT;
-  auto wait_full = [&](int sl, uint32_t ph) { mbar_wait_parity(&full[sl], ph); };
-  auto lds_unit = [&](int sl, uint4 (&w)[QT]) {
-    const uint32_t a = ring_lane + sl * slot_bytes;
-#pragma unroll
-    for (int t = 0; t < QT; ++t)
-      asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
-                   : "=r"(w[t].x), "=r"(w[t].y), "=r"(w[t].z), "=r"(w[t].w) : "r"(a + t * 512));
-  };
-  int cur_rt = -1;
-  auto compute = [&](int r_t, int k_b, const uint4 (&w)[QT]) {
-    if (r_t != cur_rt) {
-      if (cur_rt >= 0) flush(cur_rt);
-      cur_rt = r_t;
-    }
-    uint2 b[8];
+  uint2 b[8];
+  int cur_kb = -1;
+  auto load_b = [&](int k_b) {  // B fragments of a k-block (kept while it repeats)
+    cur_kb = k_b;
     const uint32_t ab = act_lane + k_b * (8 * MT * 4 * 8);
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       b[c] = make_uint2(0u, 0u);
       if (has_b) asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(b[c].x), "=r"(b[c].y) : "r"(ab + c * MT * 32));
     }
+  };
+  auto mma_unit = [&](int (&acc)[NA][4], const uint4 (&w)[QT]) {
+    if constexpr (RAW) {
+      // quad Q = w[Q] holds A registers u = 0..3 of the chunks c = f*QT + Q in field f
+      constexpr uint32_t M = ((1u << QT) - 1u) * 0x01010101u;
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      uint32_t a[4];
+      for (int Q = 0; Q < QT; ++Q)
 #pragma unroll
-      for (int r = 0; r < 4; ++r) a[r] = widen_slices<QT>(w, 4 * c + r);
-      imma_16832(acc[c & 3], a[0], a[1], a[2], a[3], b[c].x, b[c].y);
+        for (int f = 0; f < NF; ++f) {
+          const uint32_t m = M << (QT * f);
+          const int c = f * QT + Q;
+          imma_16832(acc[NF >= 2 ? f : (Q & 1)], w[Q].x & m, w[Q].y & m, w[Q].z & m, w[Q].w & m, b[c].x, b[c].y);
+        }
+    } else {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        uint32_t a[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) a[r] = widen_slices<QT>(w, 4 * c + r);
+        imma_16832(acc[c & 1], a[0], a[1], a[2], a[3], b[c].x, b[c].y);
+      }
+    }
+  };
+  auto flush_set = [&](int (&acc)[NA][4], int r_t) {
+    const int lrt = r_t - rt_first;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      // field f holds 2^(QT f) * its partial sum, exactly (the true row-tile
+      // sum is < 2^32 for K <= 65536, and so is every scaled field sum)
+      uint32_t v = 0;
+#pragma unroll
+      for (int f = 0; f < NA; ++f) {
+        const int sh = RAW && NF >= 2 ? QT * f : 0;
+        v += static_cast<uint32_t>(acc[f][r]) >> sh;
+        acc[f][r] = 0;
+      }
+      const int row = g + 8 * (r >> 1), tok = 2 * tig + (r & 1);
+      if (tok < tok_n) atomicAdd(&accs[(lrt * 16 + row) * MT + tok], v);
     }
   };
   {
-    constexpr int STEP = NG * UPS;  // units between a warp's consecutive slots
-    int i = grp, s = grp;           // NG <= S (host plan)
-    uint32_t ph = 0;
-    int u = U0 + i * UPS + wi;
-    int rt = u / kblocks, kb = u - rt * kblocks;
-    auto advance = [&]() {
-      i += NG;
-      s += NG;
-      if (s >= S) {
-        s -= S;
-        ph ^= 1u;
-      }
-      u += STEP;
-      kb += STEP;
-      while (kb >= kblocks) {
-        kb -= kblocks;
-        ++rt;
-      }
+    // loop-invariant scalars re-read from the shared copy of the parameter
+    // block: left to ptxas they are re-fetched from the constant bank (LDC)
+    // inside the loop
+    const int S_ = *reinterpret_cast<volatile int*>(&P.slots);
+    const int kbl = *reinterpret_cast<volatile int*>(&P.kblocks);
+    const int grp = warp / UPS, off = grp * UPS + warp % UPS;
+    const int nw = U1 - U0 > off ? (U1 - U0 - off + NW - 1) / NW : 0;  // this warp's units
+    const uint32_t ring_lane = smem_addr(ring) + (warp % UPS) * unit_bytes + lane * 16;
+    auto lds_unit = [&](int sl, uint4 (&w)[QT]) {
+      const uint32_t a = ring_lane + sl * slot_bytes;
+#pragma unroll
+      for (int t = 0; t < QT; ++t)
+        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(w[t].x), "=r"(w[t].y), "=r"(w[t].z), "=r"(w[t].w) : "r"(a + t * 512));
     };
-    auto release = [&](int sl) {
+    auto wait_full = [&](int sl, uint32_t p) { mbar_wait_parity(&full[sl], p); };
+    // the last of the UPS warps done with ring slot sl refills it with slot
+    // index i + S (its data is in registers: the IMMAs reading it have issued)
+    const bool refill = nsl > S_;  // else every slot was loaded once, at kernel start
+    auto release = [&](int sl, int i) {
+      if (!refill) return;
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[sl]);
-    };
-    uint4 wa[QT], wb[QT];
-    if (i < nsl) {
-      wait_full(s, ph);
-      if (u < U1) lds_unit(s, wa);
-    }
-    while (i < nsl) {
-      // iteration A: compute wa, prefetch the next slot into wb
-      {
-        const int s0 = s, rt0 = rt, kb0 = kb;
-        const bool v0 = u < U1;
-        advance();
-        if (i < nsl) {
-          wait_full(s, ph);
-          if (u < U1) lds_unit(s, wb);
-        }
-        if (v0) compute(rt0, kb0, wa);
-        release(s0);
+      if (lane == 0 && i + S_ < nsl && atomicAdd(&relcnt[sl], 1u) == UPS - 1) {
+        relcnt[sl] = 0;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue_slot(i + S_, sl);
       }
-      if (i >= nsl) break;
-      // iteration B: compute wb, prefetch into wa
-      {
-        const int s0 = s, rt0 = rt, kb0 = kb;
-        const bool v0 = u < U1;
-        advance();
-        if (i < nsl) {
-          wait_full(s, ph);
-          if (u < U1) lds_unit(s, wa);
+    };
+    // fetch cursor: slot / parity / row-tile / k-block of the next unit to fetch
+    int fs = grp, fi = grp;  // ring slot / slot index of the next fetch (NG <= S)
+    uint32_t fph = 0;
+    int frt = (U0 + off) / kbl, fkb = U0 + off - frt * kbl;
+    auto fetch = [&](uint4 (&w)[QT], int& sl, int& idx, int& r_t, int& k_b) {
+      sl = fs;
+      idx = fi;
+      fi += NG;
+      r_t = frt;
+      k_b = fkb;
+      wait_full(fs, fph);
+      lds_unit(fs, w);
+      fs += NG;
+      if (fs >= S_) {
+        fs -= S_;
+        fph ^= 1u;
+      }
+      fkb += NW;
+      while (fkb >= kbl) {
+        fkb -= kbl;
+        ++frt;
+      }
+    };
+    int accA[NA][4], accB[NA][4];
+#pragma unroll
+    for (int f = 0; f < NA; ++f)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) accA[f][r] = accB[f][r] = 0;
+    if constexpr (QT <= 6) {
+      uint4 wA[QT], wB[QT];
+      int sA = 0, iA = 0, rtA = 0, kbA = 0, sB = 0, iB = 0, rtB = 0, kbB = 0;
+      if (nw > 0) fetch(wA, sA, iA, rtA, kbA);
+      for (int j = 0; j < nw; j += 2) {
+        // unit j (buffer A, accumulators A); unit j + 1 prefetched into B
+        const int rtB_prev = rtB;  // unit j - 1 (j > 0)
+        if (j + 1 < nw) fetch(wB, sB, iB, rtB, kbB);
+        if (kbA != cur_kb) load_b(kbA);
+        mma_unit(accA, wA);
+        if (j > 0) flush_set(accB, rtB_prev);
+        release(sA, iA);
+        if (j + 1 >= nw) {
+          flush_set(accA, rtA);
+          break;
         }
-        if (v0) compute(rt0, kb0, wb);
-        release(s0);
+        // unit j + 1 (buffer B, accumulators B); unit j + 2 prefetched into A
+        const int rtA_done = rtA;
+        if (j + 2 < nw) fetch(wA, sA, iA, rtA, kbA);
+        if (kbB != cur_kb) load_b(kbB);
+        mma_unit(accB, wB);
+        flush_set(accA, rtA_done);
+        release(sB, iB);
+        if (j + 2 >= nw) flush_set(accB, rtB);
+      }
+    } else {  // one register buffer (two would spill at this register budget)
+      uint4 wA[QT];
+      int sA = 0, iA = 0, rtA = 0, kbA = 0, rtP = -1;
+      for (int j = 0; j < nw; ++j) {
+        fetch(wA, sA, iA, rtA, kbA);
+        if (kbA != cur_kb) load_b(kbA);
+        if (j & 1) {
+          mma_unit(accB, wA);
+          flush_set(accA, rtP);
+        } else {
+          mma_unit(accA, wA);
+          if (j > 0) flush_set(accB, rtP);
+        }
+        release(sA, iA);
+        rtP = rtA;
+      }
+      if (nw > 0) {
+        if ((nw - 1) & 1) flush_set(accB, rtP);
+        else flush_set(accA, rtP);
       }
     }
   }
-  if (cur_rt >= 0) flush(cur_rt);
   if (trace && lane == 0) atomicMax(&s_wend, static_cast<long long>(clock64()));
-  consumers_sync();
+  cta_sync();
   if (trace && tid == 0) trace[2] = s_wend;
 
-  // ---- epilogue
-  const bool stream_k = P.gacc != nullptr;
-  auto owned = [&](int r) {
-    const int ufirst = r * kblocks;
-    return ufirst >= U0 && ufirst + kblocks <= U1;
-  };
+  // ---- 4. epilogue: zero-point correction + dequant of this CTA's channels
   const EpiParams& E = P.e;
-  auto store = [&](int lrt, int row, int i, long long a) {
+  for (int idx = tid; idx < nlrt * 16 * MT; idx += kCT) {
+    const int i = idx & (MT - 1), rc = idx / MT, lrt = rc >> 4, row = rc & 15;
     const int j = (rt_first + lrt) * kRowTile + row;
-    if (j >= P.n) return;
+    if (i >= tok_n || j >= P.n) continue;
+    const long long a = accs[idx];
     if (!dequant) {
       epi_store_v(E, i, j, a, 0.0, 0, 0);
-      return;
+      continue;
     }
-    const int c = lrt * 16 + row;
-    const long long za = s_za[i], zb = c_zb[c];
-    const long long corr = a - za * c_cs[c] - zb * s_ra[i] + E.k * za * zb;
+    const long long za = s_za[i], zb = c_zb[rc];
+    const long long corr = a - za * c_cs[rc] - zb * s_ra[i] + E.k * za * zb;
     const long long o = static_cast<long long>(i) * E.ldo + j;
     if (E.mode == EPI_CORR_I64) {
       static_cast<int64_t*>(E.out)[o] = corr;
-      return;
+      continue;
     }
-    const double y = __dmul_rn(__dmul_rn(s_sa[i], c_sb[c]), static_cast<double>(corr));
+    const double y = __dmul_rn(__dmul_rn(s_sa[i], c_sb[rc]), static_cast<double>(corr));
     if (E.mode == EPI_F64)
       static_cast<double*>(E.out)[o] = y;
     else if (E.mode == EPI_F16)
       static_cast<__half*>(E.out)[o] = __double2half(y);
     else
       static_cast<float*>(E.out)[o] = __double2float_rn(y);
-  };
-  for (int idx = tid; idx < nlrt * 16 * MT; idx += kCT) {
-    const int i = idx & (MT - 1), rc = idx / MT, lrt = rc >> 4;
-    if (i < tok_n && (!stream_k || owned(rt_first + lrt))) store(lrt, rc & 15, i, accs[idx]);
-  }
-  int nsplit = 0;
-  for (int lrt = 0; lrt < nlrt; ++lrt) {
-    if (!stream_k || owned(rt_first + lrt)) continue;
-    ++nsplit;
-    long long* gslot = P.gacc + static_cast<size_t>(rt_first + lrt) * 16 * 8;
-    for (int idx = tid; idx < 16 * tok_n; idx += kCT)
-      atomicAdd(reinterpret_cast<unsigned long long*>(&gslot[(idx / tok_n) * 8 + idx % tok_n]),
-                static_cast<unsigned long long>(accs[(lrt * 16 + idx / tok_n) * MT + idx % tok_n]));  // u32 partial
   }
   if (trace && tid == 0) {
     trace[3] = clock64();
     trace[9] = gtimer();
-  }
-  if (nsplit == 0) return;  // uniform across the consumer warps
-  consumers_sync();
-  // release: thread 0's gpu-scope fence after the barrier orders every consumer
-  // thread's partial-sum atomics before its arrival on the counter
-  if (tid == 0) {
-    asm volatile("fence.acq_rel.gpu;" ::: "memory");
-    int mask = 0;
-    for (int e = 0; e < 2; ++e) {  // only the first / last local row-tile can be shared
-      const int lrt = e == 0 ? 0 : nlrt - 1;
-      if (e == 1 && lrt == 0) break;
-      const int r = rt_first + lrt;
-      if (owned(r)) continue;
-      // contributing CTAs of row-tile r under the split floor(b*U/G)
-      const long long uf = static_cast<long long>(r) * kblocks, ul = uf + kblocks - 1;
-      const int c = static_cast<int>(((ul + 1) * G - 1) / U) - static_cast<int>(((uf + 1) * G - 1) / U) + 1;
-      if (c > 1 && atomicAdd(&P.gcnt[r], 1u) == static_cast<unsigned>(c - 1)) mask |= 1 << e;
-    }
-    if (mask) asm volatile("fence.acq_rel.gpu;" ::: "memory");  // acquire side for the slot reads below
-    s_last = mask;
-  }
-  consumers_sync();
-  const int mask = s_last;
-  for (int e = 0; e < 2; ++e) {
-    if (!(mask & (1 << e))) continue;
-    const int lrt = e == 0 ? 0 : nlrt - 1;
-    long long* gslot = P.gacc + static_cast<size_t>(rt_first + lrt) * 16 * 8;
-    for (int idx = tid; idx < 16 * tok_n; idx += kCT) {
-      const long long a = static_cast<long long>(
-          atomicExch(reinterpret_cast<unsigned long long*>(&gslot[(idx / tok_n) * 8 + idx % tok_n]), 0ull));
-      store(lrt, idx / tok_n, idx % tok_n, a);
-    }
-    if (tid == 0) P.gcnt[rt_first + lrt] = 0u;
   }
 }
 
@@ -544,39 +550,16 @@ __global__ void __launch_bounds__(kDecThreads, MINB) gemv_dec_kernel(const __gri
 // ============================================================================
 unsigned long long*& trace_buffer();
 
-struct DecPlan {
-  int grid, slots, minb;
-  size_t smem;
-};
-
-// Ring of ~80 KB in flight per CTA; two CTAs per SM when the plan fits in
-// half the shared memory (so the next launch can stream during this one's tail).
-static DecPlan plan_dec(int q, int mt, int kpad, int U, int kblocks, int grid) {
-  DecPlan p{};
-  p.grid = grid;
-  const int nl = dec_nlrt_max(U, p.grid, kblocks);
-  const int slot_bytes = kDecUPS * q * 512;
-  int target = 96 * 1024;
-  if (const char* env = std::getenv("ABQ_DEC_RING_KB")) target = std::atoi(env) * 1024;
-  const int min_slots = kDecWarps / kDecUPS;  // every warp group needs its own slot
-  int slots = std::max(min_slots, std::min(16, target / slot_bytes));
-  p.minb = 1;
-  while (slots > min_slots && dec_smem(q, slots, mt, kpad, nl).total > 220 * 1024) --slots;
-  p.slots = slots;
-  p.smem = dec_smem(q, slots, mt, kpad, nl).total;
-  return p;
-}
-
-template <int QT, int MT, int MINB>
-static int launch_dec3(const DecParams& P, const DecPlan& pl, bool pdl, cudaStream_t st) {
-  auto kern = gemv_dec_kernel<QT, MT, MINB>;
-  if (pl.smem > 220 * 1024) return fail(ABQ_ERR_VALUE, "gemv_dec: shared memory plan too large (%zu B)", pl.smem);
-  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(pl.smem));
+template <int QT, int MT>
+static int launch_dec2(const DecParams& P, int grid, size_t smem, bool pdl, cudaStream_t st) {
+  auto kern = gemv_dec_kernel<QT, MT>;
+  if (smem > 220 * 1024) return fail(ABQ_ERR_VALUE, "gemv_dec: shared memory plan too large (%zu B)", smem);
+  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (err != cudaSuccess) return fail(ABQ_ERR_CUDA, "gemv_dec: smem attribute: %s", cudaGetErrorString(err));
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(pl.grid);
+  cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kDecThreads);
-  cfg.dynamicSmemBytes = pl.smem;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -589,22 +572,17 @@ static int launch_dec3(const DecParams& P, const DecPlan& pl, bool pdl, cudaStre
   return ABQ_OK;
 }
 
-template <int QT, int MT>
-static int launch_dec2(const DecParams& P, const DecPlan& pl, bool pdl, cudaStream_t st) {
-  return launch_dec3<QT, MT, 1>(P, pl, pdl, st);
-}
-
 template <int MT>
-static int launch_dec1(const DecParams& P, const DecPlan& pl, bool pdl, cudaStream_t st) {
+static int launch_dec1(const DecParams& P, int grid, size_t smem, bool pdl, cudaStream_t st) {
   switch (P.q) {
-    case 1: return launch_dec2<1, MT>(P, pl, pdl, st);
-    case 2: return launch_dec2<2, MT>(P, pl, pdl, st);
-    case 3: return launch_dec2<3, MT>(P, pl, pdl, st);
-    case 4: return launch_dec2<4, MT>(P, pl, pdl, st);
-    case 5: return launch_dec2<5, MT>(P, pl, pdl, st);
-    case 6: return launch_dec2<6, MT>(P, pl, pdl, st);
-    case 7: return launch_dec2<7, MT>(P, pl, pdl, st);
-    default: return launch_dec2<8, MT>(P, pl, pdl, st);
+    case 1: return launch_dec2<1, MT>(P, grid, smem, pdl, st);
+    case 2: return launch_dec2<2, MT>(P, grid, smem, pdl, st);
+    case 3: return launch_dec2<3, MT>(P, grid, smem, pdl, st);
+    case 4: return launch_dec2<4, MT>(P, grid, smem, pdl, st);
+    case 5: return launch_dec2<5, MT>(P, grid, smem, pdl, st);
+    case 6: return launch_dec2<6, MT>(P, grid, smem, pdl, st);
+    case 7: return launch_dec2<7, MT>(P, grid, smem, pdl, st);
+    default: return launch_dec2<8, MT>(P, grid, smem, pdl, st);
   }
 }
 
@@ -620,7 +598,7 @@ int run_act_quant(const void* x, int x_dtype, size_t m, size_t k, int mt, const 
 // Every launch is itself PDL-enabled so consecutive layers overlap.
 int run_gemv_dec(const uint32_t* frag, unsigned q, size_t n, size_t k, size_t m, const void* x, int x_dtype,
                  const QuantParams& qp, const EpiParams& e, void* ws, unsigned long long* bad_out,
-                 cudaStream_t st) {
+                 cudaStream_t st, const void* next_frag, size_t next_bytes) {
   if (m == 0 || n == 0) return ABQ_OK;
   if (m > 8) return fail(ABQ_ERR_VALUE, "gemv_dec: m <= 8 only");
   DecParams P{};
@@ -635,12 +613,15 @@ int run_gemv_dec(const uint32_t* frag, unsigned q, size_t n, size_t k, size_t m,
   P.e = e;
   P.qp = qp;
   P.trace = trace_buffer();
+  P.prefetch = 1;
+  P.next_frag = static_cast<const unsigned char*>(next_frag);
+  P.next_bytes = next_frag ? next_bytes : 0;
+  if (const char* env = std::getenv("ABQ_DEC_PREFETCH")) P.prefetch = env[0] == '1';
   const int mt = m <= 1 ? 1 : m <= 2 ? 2 : m <= 4 ? 4 : 8;
   const int kpad = P.kblocks * kKBlock;
+  // workspace (imma_ws_bytes layout): [row-tile accumulators][counters][codes][stats][report word]
   char* w = static_cast<char*>(ws);
-  P.gacc = reinterpret_cast<long long*>(w);
   w += static_cast<size_t>(P.rowtiles) * 16 * 8 * 8;
-  P.gcnt = reinterpret_cast<unsigned*>(w);
   w += (static_cast<size_t>(P.rowtiles) * 4 + 255) & ~size_t(255);
   uint32_t* act_frag = reinterpret_cast<uint32_t*>(w);
   w += 8 * static_cast<size_t>(kpad);
@@ -649,9 +630,9 @@ int run_gemv_dec(const uint32_t* frag, unsigned q, size_t n, size_t k, size_t m,
   long long* rowsum = reinterpret_cast<long long*>(w + 128);
   P.bad_word = reinterpret_cast<unsigned long long*>(w + 192);
   P.bad_out = bad_out;
-  // fused ReQuant: each of the NW*32/mt threads of a token holds <= 8 vectors of 8
+  // fused ReQuant: each of the 32*kDecWarps/mt consumer threads of a token holds <= 4 vectors of 8
   const bool fused = x_dtype == ABQ_F16 && !qp.per_tensor && k % 8 == 0 &&
-                     k <= static_cast<size_t>(64 * kDecWarps * 32 / mt);
+                     k <= static_cast<size_t>(32 * kDecWarps * 32 / mt);
   if (fused) {
     P.x16 = static_cast<const __half*>(x);
   } else {
@@ -662,24 +643,28 @@ int run_gemv_dec(const uint32_t* frag, unsigned q, size_t n, size_t k, size_t m,
     P.z_a = z_a;
     P.rowsum = rowsum;
   }
-  // CTAs own whole row-tiles unless that leaves SMs idle (few row-tiles): the
-  // cross-CTA reduction of stream-K costs ~3 dependent global round trips
-  P.rowsplit = P.rowtiles >= num_sms() ? 1 : 0;
-  if (const char* env = std::getenv("ABQ_DEC_STREAMK")) P.rowsplit = env[0] == '1' ? 0 : 1;
-  if (P.rowsplit) {
-    P.gacc = nullptr;
-    P.gcnt = nullptr;
-  }
-  const int grid = P.rowsplit ? std::min(num_sms(), P.rowtiles) : std::max(1, std::min(num_sms(), P.U / kDecUPS));
-  const DecPlan pl = plan_dec(P.q, mt, kpad, P.U, P.kblocks, grid);
-  P.slots = pl.slots;
+  const int grid = std::min(num_sms(), P.rowtiles);
+  // Ring (one CTA per SM): as deep as the CTA's whole weight share when that
+  // fits in shared memory -- then every TMA copy is issued at kernel start and
+  // no refill latency is exposed at the tail of the main loop -- else ~208 KB.
+  const int nl = dec_nlrt_max(P.rowtiles, grid);
+  const size_t slot_bytes = static_cast<size_t>(kDecUPS) * q * 512;
+  const int max_units = ((P.rowtiles + grid - 1) / grid) * P.kblocks;
+  int slots = (max_units + kDecUPS - 1) / kDecUPS;
+  if (const char* env = std::getenv("ABQ_DEC_RING_KB")) slots = static_cast<int>(std::atoi(env) * 1024 / slot_bytes);
+  const int min_slots = kDecWarps / kDecUPS;
+  slots = std::max(min_slots, std::min(32, slots));
+  const size_t budget = 212 * 1024;
+  while (slots > min_slots && dec_smem(q, slots, mt, kpad, nl).total > budget) --slots;
+  P.slots = slots;
+  const size_t smem = dec_smem(q, slots, mt, kpad, nl).total;
   bool pdl = true;
   if (const char* env = std::getenv("ABQ_DEC_PDL")) pdl = env[0] == '1';
   switch (mt) {
-    case 1: return launch_dec1<1>(P, pl, pdl, st);
-    case 2: return launch_dec1<2>(P, pl, pdl, st);
-    case 4: return launch_dec1<4>(P, pl, pdl, st);
-    default: return launch_dec1<8>(P, pl, pdl, st);
+    case 1: return launch_dec1<1>(P, grid, smem, pdl, st);
+    case 2: return launch_dec1<2>(P, grid, smem, pdl, st);
+    case 4: return launch_dec1<4>(P, grid, smem, pdl, st);
+    default: return launch_dec1<8>(P, grid, smem, pdl, st);
   }
 }
 

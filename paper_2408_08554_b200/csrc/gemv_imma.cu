@@ -970,20 +970,21 @@ int run_act_quant(const void* x, int x_dtype, size_t m, size_t k, int mt, const 
 
 int run_gemv_dec(const uint32_t* frag, unsigned q, size_t n, size_t k, size_t m, const void* x, int x_dtype,
                  const QuantParams& qp, const EpiParams& e, void* ws, unsigned long long* bad_out,
-                 cudaStream_t st);
+                 cudaStream_t st, const void* next_frag, size_t next_bytes);
 
 // Serving path: act_quant_kernel (ReQuant into B-fragment codes) followed by the
 // stream-K GEMV with programmatic dependent launch.  `ws` must be
 // imma_ws_bytes(n, k) of zero-filled device memory (left zeroed).
 int run_gemv_imma_fused(const uint32_t* frag, unsigned q, size_t n, size_t k, size_t m, const void* x,
                         int x_dtype, const QuantParams& qp, const EpiParams& e, void* ws,
-                        unsigned long long* bad_out, cudaStream_t st) {
+                        unsigned long long* bad_out, cudaStream_t st, const void* next_frag,
+                        size_t next_bytes) {
   if (m == 0 || n == 0) return ABQ_OK;
   // the serving kernel is gemv_dec_kernel (gemv_dec.cu); ABQ_GEMV_KERNEL=imma
   // selects this earlier per-warp-ring kernel for comparison
   const char* kern_env = std::getenv("ABQ_GEMV_KERNEL");
   if (!(kern_env && std::strcmp(kern_env, "imma") == 0))
-    return run_gemv_dec(frag, q, n, k, m, x, x_dtype, qp, e, ws, bad_out, st);
+    return run_gemv_dec(frag, q, n, k, m, x, x_dtype, qp, e, ws, bad_out, st, next_frag, next_bytes);
   ImmaParams P = base_params(frag, q, n, k, m, e);
   const int mt = pick_imma_mt(static_cast<int>(m));
   const size_t rowtiles = P.rowtiles;

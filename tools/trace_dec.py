@@ -21,6 +21,9 @@ copies = int(sys.argv[3]) if len(sys.argv) > 3 else max(L, 2)
 x_np, wc, sb, zb, ws = bench.build_layer(abq, torch, m, n, k, wb, ab, copies)
 spec = abq.QuantSpec(bits=ab, granularity=abq.api.PER_TOKEN)
 lins = [abq.Linear(w, spec, max_m=m) for w in ws[:copies]]
+if os.environ.get("TRACE_NO_NEXT") != "1":
+    for i, lin in enumerate(lins):
+        lin.prefetch_next(lins[(i + 1) % len(lins)])
 x = torch.from_numpy(x_np).cuda()
 y = torch.empty((m, n), dtype=torch.float16, device="cuda")
 bufs = [torch.zeros(64 * 4096, dtype=torch.int64, device="cuda") for _ in range(L)]
@@ -58,6 +61,8 @@ for i, t in enumerate(rows):
     print("             prologue marks (us from start): wait done %.2f, min/max %.2f, step %.2f, codes %.2f" % tuple(ph))
     print(f"  launch {i:2d}: span {(e - a) / 1e3:6.2f} us{gap}   prologue {pro:5.2f}  main {main:5.2f}  epilogue {epi:5.2f} us"
           f"  (CTA start skew {(t[:, 8].max() - a) / 1e3:5.2f} us)")
+    tw = t[:, 24:40].astype(float) / ghz / 1e3
+    print("             main-loop slot waits per warp: median %.2f us, max %.2f us" % (np.median(tw), tw.max()))
     prev_end = e
 first, last = rows[0][:, 8].min(), rows[-1][:, 9].max()
 print(f"  first start -> last end {(last - first) / 1e3:.2f} us = {(last - first) / 1e3 / L:.3f} us per launch")
