@@ -40,7 +40,8 @@ unsigned long long*& trace_buffer();
 
 constexpr int kTcM = 128;
 constexpr int kTcK = 128;
-constexpr int kTcThreads = 256;
+constexpr int kTcThreads = 512;  // warps 8-15 only join the epilogue
+constexpr int kTcColGroups = kTcThreads / 128;  // epilogue: token-column groups per TMEM lane quarter
 
 // ---------------------------------------------------------------------------
 // prepack: ABQP [q][n][wpr] -> tc code slices
@@ -186,31 +187,43 @@ __device__ __forceinline__ uint32_t widen_row(const uint4 (&w)[Q], int o) {
 template <int MODE, int TT>
 __device__ __forceinline__ void tc_epilogue(const EpiParams& E, uint32_t taddr, int half, int tok0, int m, int ch,
                                             int n, const double* t_sa, const unsigned* t_za, const unsigned* t_kz,
-                                            const unsigned* t_ra, __half* stage, int lch) {
+                                            const unsigned* t_ra, __half* stage, int lch, const double* c_sb,
+                                            const int* c_zb, const int* c_cs, bool k32) {
   constexpr bool kRaw = MODE == EPI_ACC_I32 || MODE == EPI_ACC_I64;
   const bool chan_ok = ch < n;
+  // per-channel values, staged in shared memory during the k-loop (loaded here
+  // from global they cost two dependent memory round trips on the tail);
   // |colsum_b|, |u| <= 255 K < 2^31 for K <= 65536
-  double sb = 0.0;
-  int zb = 0, cs = 0;
-  if (!kRaw && chan_ok) {
-    sb = E.s_b[ch * E.sb_stride];
-    zb = E.z_b[ch * E.zb_stride];
-    cs = static_cast<int>(E.colsum_b[ch]);
-  }
+  const double sb = c_sb[lch];
+  const int zb = c_zb[lch], cs = c_cs[lch];
+  // up to 16 columns per tcgen05.ld; a thread covers TT / kTcColGroups columns
+  constexpr int TC = TT / kTcColGroups;
+  constexpr int CW = TC >= 16 ? 16 : TC;
 #pragma unroll 1
-  for (int c0 = half * (TT / 2); c0 < (half + 1) * (TT / 2); c0 += 8) {
-    uint32_t v[8];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
-        : "r"(taddr + static_cast<uint32_t>(c0)));
+  for (int c0 = half * TC; c0 < (half + 1) * TC; c0 += CW) {
+    uint32_t v[CW];
+    if constexpr (CW == 4)
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+                   : "r"(taddr + static_cast<uint32_t>(c0)));
+    else if constexpr (CW == 16)
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+          : "r"(taddr + static_cast<uint32_t>(c0)));
+    else
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+          : "r"(taddr + static_cast<uint32_t>(c0)));
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
     if (!chan_ok) continue;
-    const bool full = tok0 + c0 + 8 <= m;  // uniform: no per-token bound in the common case
+    const bool full = tok0 + c0 + CW <= m;  // uniform: no per-token bound in the common case
     const long long o0 = static_cast<long long>(tok0 + c0) * E.ldo + ch;
     if constexpr (kRaw) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
+      for (int i = 0; i < CW; ++i) {
         // the true sum is < 2^32 (K <= 65536, codes <= 255): exact as unsigned
         if (full || tok0 + c0 + i < m) {
           if constexpr (MODE == EPI_ACC_I32) static_cast<int32_t*>(E.out)[o0 + i * E.ldo] = static_cast<int32_t>(v[i]);
@@ -218,32 +231,44 @@ __device__ __forceinline__ void tc_epilogue(const EpiParams& E, uint32_t taddr, 
         }
       }
     } else {
-      // corrected = acc + (K z_a) z_b - z_a colsum_b - z_b rowsum_a: every factor
-      // is a non-negative 32-bit value, every product one IMAD.WIDE.U32
-      long long corr[8];
+      // corrected = acc + (K z_a - rowsum_a) z_b - z_a colsum_b.  With K <= 32768
+      // the true value is |corr| <= 255^2 K < 2^31, so the sum is computed in
+      // wrapping 32-bit arithmetic (two IMADs; exact modulo 2^32, hence exactly);
+      // larger K takes the 64-bit products.
+      long long corr[CW];
+      if (k32) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int ti = c0 + i;
-        const unsigned long long plus = static_cast<unsigned long long>(v[i]) +
-                                        static_cast<unsigned long long>(t_kz[ti]) * static_cast<unsigned>(zb);
-        const unsigned long long minus = static_cast<unsigned long long>(t_za[ti]) * static_cast<unsigned>(cs) +
-                                         static_cast<unsigned long long>(t_ra[ti]) * static_cast<unsigned>(zb);
-        corr[i] = static_cast<long long>(plus - minus);
+        for (int i = 0; i < CW; ++i) {
+          const int ti = c0 + i;
+          const uint32_t c = v[i] + (t_kz[ti] - t_ra[ti]) * static_cast<uint32_t>(zb) - t_za[ti] * static_cast<uint32_t>(cs);
+          corr[i] = static_cast<int>(c);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < CW; ++i) {
+          const int ti = c0 + i;
+          const unsigned long long plus = static_cast<unsigned long long>(v[i]) +
+                                          static_cast<unsigned long long>(t_kz[ti]) * static_cast<unsigned>(zb);
+          const unsigned long long minus = static_cast<unsigned long long>(t_za[ti]) * static_cast<unsigned>(cs) +
+                                           static_cast<unsigned long long>(t_ra[ti]) * static_cast<unsigned>(zb);
+          corr[i] = static_cast<long long>(plus - minus);
+        }
       }
       if constexpr (MODE == EPI_CORR_I64) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
+        for (int i = 0; i < CW; ++i)
           if (full || tok0 + c0 + i < m) static_cast<int64_t*>(E.out)[o0 + i * E.ldo] = corr[i];
       } else {
-        double y[8];
+        double y[CW];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
+        for (int i = 0; i < CW; ++i) {
           // exact int64 -> double (|corr| < 2^51) by the 1.5 * 2^52 magic add
           const double cd = __dsub_rn(__longlong_as_double(0x4338000000000000LL + corr[i]), 6755399441055744.0);
+          // (for k32 the compiler sees corr[i] as a sign-extended int32)
           y[i] = __dmul_rn(__dmul_rn(t_sa[c0 + i], sb), cd);
         }
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
+        for (int i = 0; i < CW; ++i) {
           if (full || tok0 + c0 + i < m) {
             const long long o = o0 + i * E.ldo;
             if constexpr (MODE == EPI_F64) static_cast<double*>(E.out)[o] = y[i];
@@ -266,15 +291,24 @@ struct TcParams {
   unsigned long long* trace;  // optional [grid][16] clock64 / globaltimer stamps (profiling)
 };
 
+// Shared memory: an input ring of kS stages -- the packed weights of a
+// 128-k block (or, q = 8, the A operand itself) + the activation tile -- that
+// the TMA producer keeps full, and (q < 8) a separate 2-deep ring of widened
+// u8 A operands.  Keeping the 16 KB widened operand out of the input stage
+// makes the input ring ~1.7x deeper for the same shared memory, which is what
+// bounds the k-loop (each stage's L2/HBM latency is covered by the stages in
+// flight behind it).
 template <int Q, int TT>
 struct TcShape {
   static constexpr bool kExpand = Q < 8;
   static constexpr int kA = kTcM * kTcK;          // u8 operand A (weights), 16 KB
   static constexpr int kB = TT * kTcK;            // u8 operand B (activations)
-  static constexpr int kW = kExpand ? Q * kTcM * 16 : 0;  // packed slices staging
-  static constexpr int kStage = kA + kB + kW;
-  static constexpr int kS = (200 * 1024) / kStage > 6 ? 6 : (200 * 1024) / kStage;
-  static constexpr int kSmem = kS * kStage + 1024;  // + alignment slack
+  static constexpr int kW = kExpand ? Q * kTcM * 16 : kA;  // packed slices (or A itself)
+  static constexpr int kStage = kW + kB;          // one input stage
+  static constexpr int kSA = kExpand ? 4 : 0;     // widened-A ring depth (2 k-blocks per widening pass)
+  static constexpr int kBudget = 208 * 1024 - kSA * kA;
+  static constexpr int kS = kBudget / kStage > 12 ? 12 : kBudget / kStage;
+  static constexpr int kSmem = kS * kStage + kSA * kA + 1024;  // + alignment slack
 };
 
 template <int Q, int TT>
@@ -284,34 +318,42 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_con
   constexpr int TMEM_COLS = TT <= 32 ? 32 : (TT <= 64 ? 64 : (TT <= 128 ? 128 : 256));
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ __align__(8) uint64_t wbar[S], abar[S], rbar[S], ebar[S], done_bar;
+  constexpr int SA = Sh::kSA > 0 ? Sh::kSA : 1;
+  // wbar/abar: stage s weights / activations landed; ebar: MMA done with input
+  // stage s; rbar/xbar: widened A slot a filled / free again
+  __shared__ __align__(8) uint64_t wbar[S], abar[S], ebar[S], rbar[SA], xbar[SA], done_bar;
   __shared__ uint32_t tmem_base_s;
   // per-token epilogue values, loaded by the otherwise idle warps 2-3:
   // s_a, z_a, K z_a, rowsum_a (all non-negative, < 2^32 for K <= 65536)
   __shared__ double t_sa[TT];
   __shared__ unsigned t_za[TT], t_kz[TT], t_ra[TT];
+  __shared__ double c_sb[kTcM];  // per-channel epilogue values (warps 8-11, during the k-loop)
+  __shared__ int c_zb[kTcM], c_cs[kTcM];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (warp == 7) warm_param_block(P, lane);
   const int rt = blockIdx.x, tok0 = blockIdx.y * TT;
   const int nkb = P.kblocks;
-  unsigned long long* trace = P.trace ? P.trace + 16 * (blockIdx.y * gridDim.x + blockIdx.x) : nullptr;
+  unsigned long long* trace = P.trace ? P.trace + 64 * (blockIdx.y * gridDim.x + blockIdx.x) : nullptr;
   if (trace && tid == 0) {
     unsigned long long g;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g));
     trace[0] = clock64();
     trace[8] = g;
   }
-  auto a_of = [&](int s) { return smem + s * Sh::kStage; };
-  auto b_of = [&](int s) { return smem + s * Sh::kStage + Sh::kA; };
-  auto w_of = [&](int s) { return smem + s * Sh::kStage + Sh::kA + Sh::kB; };
+  auto w_of = [&](int s) { return smem + s * Sh::kStage; };                  // packed W (q = 8: A)
+  auto b_of = [&](int s) { return smem + s * Sh::kStage + Sh::kW; };         // activations
+  auto x_of = [&](int a) { return smem + S * Sh::kStage + a * Sh::kA; };     // widened A (q < 8)
 
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&wbar[s], 1);
       mbar_init(&abar[s], 1);
-      mbar_init(&rbar[s], 128);
       mbar_init(&ebar[s], 1);
+    }
+    for (int a = 0; a < SA; ++a) {
+      mbar_init(&rbar[a], 4);  // one arrival per widening warp
+      mbar_init(&xbar[a], 1);
     }
     mbar_init(&done_bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -330,14 +372,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_con
   if (warp == 0) {
     if (lane == 0) {
       // ---- TMA producer
-      constexpr uint32_t WB = Sh::kExpand ? Sh::kW : Sh::kA;
+      constexpr uint32_t WB = Sh::kW;
       const unsigned char* wsrc = reinterpret_cast<const unsigned char*>(P.wtc) +
                                   static_cast<size_t>(rt) * nkb * WB;
       const unsigned char* asrc = P.act + static_cast<size_t>(tok0 / 8) * 1024;
       auto issue_w = [&](int kb) {
         const int s = kb % S;
         mbar_expect_tx(&wbar[s], WB);
-        bulk_g2s(Sh::kExpand ? w_of(s) : a_of(s), wsrc + static_cast<size_t>(kb) * WB, WB, &wbar[s]);
+        bulk_g2s(w_of(s), wsrc + static_cast<size_t>(kb) * WB, WB, &wbar[s]);
       };
       auto issue_a = [&](int kb) {
         const int s = kb % S;
@@ -346,6 +388,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_con
       };
       const int pre = nkb < S ? nkb : S;
       for (int kb = 0; kb < pre; ++kb) issue_w(kb);
+      {  // the rest of this CTA's weights: L2 bulk prefetch, so the ring's later
+         // weight copies hit L2 instead of waiting on HBM latency
+        uint64_t pol;
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+        const size_t total = static_cast<size_t>(nkb) * WB;
+        for (size_t off = static_cast<size_t>(pre) * WB; off < total; off += 32768)
+          asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(wsrc + off),
+                       "r"(static_cast<uint32_t>(total - off < 32768 ? total - off : 32768)), "l"(pol)
+                       : "memory");
+      }
       // the weights do not depend on the preceding ReQuant kernel; its codes do
       // (programmatic dependent launch; a no-op otherwise)
       asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -357,6 +409,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_con
       for (int kb = 0; kb < pre; ++kb) issue_a(kb);
       for (int kb = S; kb < nkb; ++kb) {
         mbar_wait(&ebar[kb % S], ((kb / S) - 1) & 1);  // MMA of kb - S done with the stage
+        if (trace && kb < S + 16) trace[48 + kb - S] = clock64();
         issue_w(kb);
         issue_a(kb);
       }
@@ -366,21 +419,36 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_con
       // ---- MMA issuer: D=s32, A=B=u8, both K-major, N=TT, M=128
       const uint32_t idesc = (2u << 4) | (static_cast<uint32_t>(TT >> 3) << 17) |
                              (static_cast<uint32_t>(kTcM >> 4) << 24);
+      // descriptors: the start-address field is the low 14 bits of (addr >> 4)
+      // and every operand lies below 256 KB, so a descriptor advances by a
+      // plain add of (byte offset >> 4) -- precomputed, the issue loop is a
+      // handful of uniform ops per UMMA
+      const uint64_t a_base = umma_desc(smem_u32(Sh::kExpand ? x_of(0) : w_of(0)), kTcM * 16, 128);
+      const uint64_t b_base = umma_desc(smem_u32(b_of(0)), 128, 1024);
+      constexpr uint64_t a_stride = (Sh::kExpand ? Sh::kA : Sh::kStage) >> 4;  // per ring slot
+      constexpr uint64_t b_stride = Sh::kStage >> 4;
+      constexpr uint64_t a_j = (2 * kTcM * 16) >> 4, b_j = (2 * 128) >> 4;  // per K = 32 step
+      int s = 0, a = 0;
+      uint32_t ph = 0, pha = 0;
       for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % S;
-        const uint32_t ph = static_cast<uint32_t>(kb / S) & 1u;
-        mbar_wait(Sh::kExpand ? &rbar[s] : &wbar[s], ph);
+        if (Sh::kExpand) mbar_wait(&rbar[a], pha);
+        else mbar_wait(&wbar[s], ph);
         mbar_wait(&abar[s], ph);
         tc_fence_after();
-        if (trace && (kb & 7) == 0 && kb < 64) trace[10 + (kb >> 3)] = clock64();
-        const uint32_t a_addr = smem_u32(a_of(s)), b_addr = smem_u32(b_of(s));
+        if (trace && kb < 16) trace[32 + kb] = clock64();
+        const uint64_t ad = a_base + (Sh::kExpand ? a : s) * a_stride, bd = b_base + s * b_stride;
 #pragma unroll
-        for (int j = 0; j < kTcK / 32; ++j) {
-          const uint64_t ad = umma_desc(a_addr + j * 2 * (kTcM * 16), kTcM * 16, 128);
-          const uint64_t bd = umma_desc(b_addr + j * 2 * 128, 128, 1024);
-          umma_i8(tmem_d, ad, bd, idesc, (kb | j) != 0 ? 1u : 0u);
-        }
+        for (int j = 0; j < kTcK / 32; ++j) umma_i8(tmem_d, ad + j * a_j, bd + j * b_j, idesc, (kb | j) != 0 ? 1u : 0u);
         tc_commit(&ebar[s]);
+        if (Sh::kExpand) tc_commit(&xbar[a]);
+        if (++s == S) {
+          s = 0;
+          ph ^= 1u;
+        }
+        if (++a == SA) {
+          a = 0;
+          pha ^= 1u;
+        }
       }
       tc_commit(&done_bar);
       if (trace) trace[3] = clock64();
@@ -400,26 +468,53 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_con
         }
       }
     }
-  } else if (Sh::kExpand && warp >= 4) {
-    // ---- widen packed code slices of row r into the A operand
+  } else if (Sh::kExpand && warp >= 4 && warp < 8) {
+    // ---- widen packed code slices of row r into the A operand, two k-blocks
+    // per pass (their loads, widening and stores interleave: one k-block per
+    // pass left each warp a ~600-cycle dependent chain per k-block, which
+    // paced the whole k-loop)
     const int r = tid - 128;
-    for (int kb = 0; kb < nkb; ++kb) {
-      const int s = kb % S;
-      mbar_wait(&wbar[s], static_cast<uint32_t>(kb / S) & 1u);
-      const uint4* wsl = reinterpret_cast<const uint4*>(w_of(s)) + r;
-      uint4 w[Q > 0 ? Q : 1];
-#pragma unroll
-      for (int t = 0; t < Q; ++t) w[t] = wsl[t * kTcM];
-      uint4* adst = reinterpret_cast<uint4*>(a_of(s)) + r;
+    auto widen_one = [&](int kb, const uint4 (&w)[Q > 0 ? Q : 1]) {
+      const int a = kb % SA;
+      if (kb >= SA) mbar_wait(&xbar[a], static_cast<uint32_t>(kb / SA - 1) & 1u);  // MMA of kb - SA done
+      uint4* adst = reinterpret_cast<uint4*>(x_of(a)) + r;
 #pragma unroll
       for (int kc = 0; kc < 8; ++kc)
         adst[kc * kTcM] = make_uint4(widen_row<Q>(w, 4 * kc), widen_row<Q>(w, 4 * kc + 1),
                                      widen_row<Q>(w, 4 * kc + 2), widen_row<Q>(w, 4 * kc + 3));
+    };
+    auto load_one = [&](int kb, uint4 (&w)[Q > 0 ? Q : 1]) {
+      const int s = kb % S;
+      mbar_wait(&wbar[s], static_cast<uint32_t>(kb / S) & 1u);
+      const uint4* wsl = reinterpret_cast<const uint4*>(w_of(s)) + r;
+#pragma unroll
+      for (int t = 0; t < Q; ++t) w[t] = wsl[t * kTcM];
+    };
+    for (int kb = 0; kb < nkb; kb += 2) {
+      const bool two = kb + 1 < nkb;
+      uint4 w0[Q > 0 ? Q : 1], w1[Q > 0 ? Q : 1];
+      load_one(kb, w0);
+      if (two) load_one(kb + 1, w1);
+      widen_one(kb, w0);
+      if (two) widen_one(kb + 1, w1);
       fence_async_smem();  // generic-proxy stores -> visible to the tensor core
-      mbar_arrive(&rbar[s]);
+      __syncwarp();
+      if (trace && tid == 128 && kb < 16) trace[16 + kb] = clock64();
+      if (lane == 0) {
+        mbar_arrive(&rbar[kb % SA]);
+        if (two) mbar_arrive(&rbar[(kb + 1) % SA]);
+      }
     }
   }
-  __syncthreads();  // per-token values in shared memory
+  if (warp >= 8 && warp < 12) {  // idle during the k-loop: this tile's channel parameters
+    const int c = tid - 256, j = rt * kTcM + c;
+    const EpiParams& E = P.e;
+    const bool ok = j < P.n && E.mode != EPI_ACC_I32 && E.mode != EPI_ACC_I64;
+    c_sb[c] = ok ? E.s_b[j * E.sb_stride] : 0.0;
+    c_zb[c] = ok ? E.z_b[j * E.zb_stride] : 0;
+    c_cs[c] = ok ? static_cast<int>(E.colsum_b[j]) : 0;
+  }
+  __syncthreads();  // per-token and per-channel values in shared memory
 
   // ---- epilogue: TMEM -> registers -> zero-point correction + dequant.  A
   // thread owns one output channel (TMEM lane) and half of the token columns,
@@ -432,16 +527,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_con
   __half* stage = reinterpret_cast<__half*>(smem);  // the operand ring is idle now
   const uint32_t taddr = tmem_d + (static_cast<uint32_t>(quarter * 32) << 16);
   switch (P.e.mode) {
-    case EPI_ACC_I32: tc_epilogue<EPI_ACC_I32, TT>(P.e, taddr, half, tok0, P.m, ch, P.n, t_sa, t_za, t_kz, t_ra, stage, lch); break;
-    case EPI_ACC_I64: tc_epilogue<EPI_ACC_I64, TT>(P.e, taddr, half, tok0, P.m, ch, P.n, t_sa, t_za, t_kz, t_ra, stage, lch); break;
-    case EPI_F64: tc_epilogue<EPI_F64, TT>(P.e, taddr, half, tok0, P.m, ch, P.n, t_sa, t_za, t_kz, t_ra, stage, lch); break;
-    case EPI_F16: tc_epilogue<EPI_F16, TT>(P.e, taddr, half, tok0, P.m, ch, P.n, t_sa, t_za, t_kz, t_ra, stage, lch); break;
-    case EPI_F32: tc_epilogue<EPI_F32, TT>(P.e, taddr, half, tok0, P.m, ch, P.n, t_sa, t_za, t_kz, t_ra, stage, lch); break;
-    default: tc_epilogue<EPI_CORR_I64, TT>(P.e, taddr, half, tok0, P.m, ch, P.n, t_sa, t_za, t_kz, t_ra, stage, lch); break;
+    case EPI_ACC_I32: tc_epilogue<EPI_ACC_I32, TT>(P.e, taddr, half, tok0, P.m, ch, P.n, t_sa, t_za, t_kz, t_ra, stage, lch, c_sb, c_zb, c_cs, P.k <= 32768); break;
+    case EPI_ACC_I64: tc_epilogue<EPI_ACC_I64, TT>(P.e, taddr, half, tok0, P.m, ch, P.n, t_sa, t_za, t_kz, t_ra, stage, lch, c_sb, c_zb, c_cs, P.k <= 32768); break;
+    case EPI_F64: tc_epilogue<EPI_F64, TT>(P.e, taddr, half, tok0, P.m, ch, P.n, t_sa, t_za, t_kz, t_ra, stage, lch, c_sb, c_zb, c_cs, P.k <= 32768); break;
+    case EPI_F16: tc_epilogue<EPI_F16, TT>(P.e, taddr, half, tok0, P.m, ch, P.n, t_sa, t_za, t_kz, t_ra, stage, lch, c_sb, c_zb, c_cs, P.k <= 32768); break;
+    case EPI_F32: tc_epilogue<EPI_F32, TT>(P.e, taddr, half, tok0, P.m, ch, P.n, t_sa, t_za, t_kz, t_ra, stage, lch, c_sb, c_zb, c_cs, P.k <= 32768); break;
+    default: tc_epilogue<EPI_CORR_I64, TT>(P.e, taddr, half, tok0, P.m, ch, P.n, t_sa, t_za, t_kz, t_ra, stage, lch, c_sb, c_zb, c_cs, P.k <= 32768); break;
   }
+  if (trace && tid == 0) trace[6] = clock64();
   if (P.e.mode == EPI_F16) {
     // staged fp16 tile -> global, 8 channels (16 B) per store where aligned
     __syncthreads();
+    if (trace && tid == 0) trace[7] = clock64();
     const int rows = min(TT, P.m - tok0), cols = min(kTcM, P.n - rt * kTcM);
     __half* out = static_cast<__half*>(P.e.out);
     const bool vec = (P.e.ldo & 7) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0;

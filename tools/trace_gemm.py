@@ -17,8 +17,9 @@ x_np, wc, sb, zb, ws = bench.build_layer(abq, torch, m, n, k, wb, ab, 2)
 spec = abq.QuantSpec(bits=ab, granularity=abq.api.PER_TOKEN)
 lins = [abq.Linear(w, spec, max_m=m) for w in ws]
 x = torch.from_numpy(x_np).cuda()
-y = torch.empty((m, n), dtype=torch.float16, device="cuda")
-buf = torch.zeros(16 * 4096, dtype=torch.int64, device="cuda")
+odt = {"f16": torch.float16, "f32": torch.float32, "f64": torch.float64}[sys.argv[2] if len(sys.argv) > 2 else "f16"]
+y = torch.empty((m, n), dtype=odt, device="cuda")
+buf = torch.zeros(64 * 4096, dtype=torch.int64, device="cuda")
 for _ in range(3):
     lins[0](x, out=y, check=False)
 torch.cuda.synchronize()
@@ -27,7 +28,7 @@ lib.abq_set_trace_buffer(buf.data_ptr())
 lins[1](x, out=y, check=False)
 torch.cuda.synchronize()
 lib.abq_set_trace_buffer(None)
-t = buf.view(-1, 16).cpu().numpy().astype(np.int64)
+t = buf.view(-1, 64).cpu().numpy().astype(np.int64)
 t = t[t[:, 0] > 0]
 ghz = 1.965
 
@@ -44,6 +45,14 @@ for j in range(6):
         print(f"  MMA of k-block {8 * j:3d} issued   median {np.median(us(c[ok] - t[ok, 0])):7.2f} us after CTA start")
 print(f"  last MMA issued          median {np.median(us(t[:, 3] - t[:, 0])):7.2f} us")
 print(f"  epilogue start (done)    median {np.median(us(t[:, 4] - t[:, 0])):7.2f} us")
+print(f"  tid0 epilogue math done median {np.median(us(t[:, 6] - t[:, 0])):7.2f} us; after barrier {np.median(us(t[:, 7] - t[:, 0])):7.2f}")
 print(f"  CTA end                  median {np.median(us(t[:, 5] - t[:, 0])):7.2f} us  max {us(t[:, 5] - t[:, 0]).max():7.2f}")
 print(f"  launch span (globaltimer) {(t[:, 9].max() - t[:, 8].min()) / 1e3:7.2f} us; CTA start skew "
       f"{(t[:, 8].max() - t[:, 8].min()) / 1e3:6.2f} us")
+
+c0 = t[0]
+print("  CTA 0 per k-block (us after start): widened / MMA issued / producer refill issued (stage kb+S)")
+for kb in range(16):
+    w, mm, pr = c0[16 + kb], c0[32 + kb], c0[48 + kb]
+    f = lambda v: "%6.2f" % us(v - c0[0]) if v > 0 else "   -  "
+    print("   kb %2d: %s %s %s" % (kb, f(w), f(mm), f(pr)))
