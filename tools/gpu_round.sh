@@ -1,6 +1,6 @@
 #!/bin/bash
-# One gpurun session: GPU parity tests, bench (both arms), sweep, ncu launch list + full capture.
-# usage (under gpurun): bash tools/gpu_round.sh [tag]
+# One gpurun session: GPU parity tests, smoke, bench (both arms), sweep, ncu launch list + full capture
+# of the decode GEMV.  usage (under gpurun): bash tools/gpu_round.sh [tag]
 TAG=${1:-r01}
 O=gpurun_out
 mkdir -p $O
@@ -9,9 +9,11 @@ timeout 900 python -m pytest tests -m gpu -x -q > $O/${TAG}_pytest_gpu.log 2>&1;
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/${TAG}_smoke.log 2>&1; echo "smoke rc=$?" >> $O/${TAG}_smoke.log
 timeout 600 python bench.py > $O/${TAG}_bench.json 2> $O/${TAG}_bench.err
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $O/${TAG}_bench_ref.json 2> $O/${TAG}_bench_ref.err
-timeout 900 python bench.py --sweep --no-cpu > $O/${TAG}_sweep.json 2> $O/${TAG}_sweep.err
+timeout 900 python bench.py --sweep --no-cpu --steps 5000 > $O/${TAG}_sweep.json 2> $O/${TAG}_sweep.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/${TAG}_launches.csv \
   python bench.py --steps 20 --warmup 3 --no-cpu --no-check > $O/${TAG}_launches.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemv -s 20 -c 3 -f -o $O/${TAG}_gemv \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemv_dec -s 20 -c 3 -f -o $O/${TAG}_gemv \
   python bench.py --steps 20 --warmup 3 --no-cpu --no-check > $O/${TAG}_ncu_full.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemm_tc -s 2 -c 1 -f -o $O/${TAG}_gemm \
+  python tools/trace_gemm.py cfg2_w4a4_m128 > $O/${TAG}_ncu_gemm.log 2>&1
 echo done
