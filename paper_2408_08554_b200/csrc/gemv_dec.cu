@@ -122,6 +122,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) gemv_dec_kernel(const __grid_c
   __shared__ float s_inv[MT];
   __shared__ long long s_wend;
 
+  const unsigned long long t_entry = gtimer();  // profiling: true CTA start
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   asm volatile("griddepcontrol.launch_dependents;");
 
@@ -154,24 +155,31 @@ __global__ void __launch_bounds__(kDecThreads, 1) gemv_dec_kernel(const __grid_c
     tma_bulk_g2s_hint(ring + static_cast<size_t>(sl) * slot_bytes, wsrc + static_cast<size_t>(i) * slot_bytes, bytes,
                       &full[sl], pol);
   };
-  if (tid == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init_n(&full[s], 1);
-      relcnt[s] = 0;
+  // Set-up spread over lanes (one thread doing it serially took ~2 us, all on
+  // the launch's critical path): warp 0 lane s initialises barrier s and, once
+  // the initialisation is fenced, issues slot s; warp 1's lanes issue the L2
+  // bulk prefetches (the CTA's range beyond the ring, then its share of the
+  // successor layer), one 32 KB chunk per lane per round.
+  if (warp == 0) {
+    if (lane < S) {
+      mbar_init_n(&full[lane], 1);
+      relcnt[lane] = 0;
     }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int i = 0; i < S && i < nsl; ++i) issue_slot(i, i);
+    __syncwarp();
+    if (lane == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+    for (int i = lane; i < S && i < nsl; i += 32) issue_slot(i, i);
+  } else if (warp == 1 && Pc.prefetch) {
     const size_t total = static_cast<size_t>(U1 - U0) * unit_bytes;
-    if (Pc.prefetch) {
-      for (size_t off = static_cast<size_t>(S) * slot_bytes; off < total; off += 32768)
-        l2_prefetch_bulk(wsrc + off, static_cast<uint32_t>(total - off < 32768 ? total - off : 32768), pol);
-      // the next layer's weights (input-independent) stream into L2 behind ours
-      if (Pc.next_frag) {
-        const size_t nb = Pc.next_bytes, lo = (nb * blockIdx.x / G) & ~size_t(15),
-                     hi = (nb * (blockIdx.x + 1) / G) & ~size_t(15);
-        for (size_t off = lo; off < hi; off += 32768)
-          l2_prefetch_bulk(Pc.next_frag + off, static_cast<uint32_t>(hi - off < 32768 ? hi - off : 32768), pol);
-      }
+    for (size_t off = static_cast<size_t>(S) * slot_bytes + static_cast<size_t>(lane) * 32768; off < total;
+         off += 32u * 32768)
+      l2_prefetch_bulk(wsrc + off, static_cast<uint32_t>(total - off < 32768 ? total - off : 32768), pol);
+    // the next layer's weights (input-independent) stream into L2 behind ours
+    if (Pc.next_frag) {
+      const size_t nb = Pc.next_bytes, lo = (nb * blockIdx.x / G) & ~size_t(15),
+                   hi = (nb * (blockIdx.x + 1) / G) & ~size_t(15);
+      for (size_t off = lo + static_cast<size_t>(lane) * 32768; off < hi; off += 32u * 32768)
+        l2_prefetch_bulk(Pc.next_frag + off, static_cast<uint32_t>(hi - off < 32768 ? hi - off : 32768), pol);
     }
   }
 
@@ -182,7 +190,8 @@ __global__ void __launch_bounds__(kDecThreads, 1) gemv_dec_kernel(const __grid_c
   const int pj = rt_first * kRowTile + tid;
   const bool has_p = dequant && tid < nlrt * 16 && pj < Pc.n;
   double p_sb = 0.0;
-  long long p_zb = 0, p_cs = 0;
+  int p_zb = 0;  // int32 as loaded: a conversion here would wait for the load before the barrier
+  long long p_cs = 0;
   if (has_p) {
     p_sb = Pc.e.s_b[static_cast<size_t>(pj) * Pc.e.sb_stride];
     p_zb = Pc.e.z_b[static_cast<size_t>(pj) * Pc.e.zb_stride];
@@ -199,12 +208,13 @@ __global__ void __launch_bounds__(kDecThreads, 1) gemv_dec_kernel(const __grid_c
   if (trace && tid == 0) {
     trace[0] = clock64();
     trace[8] = gtimer();
+    trace[12] = t_entry;
     s_wend = 0;
   }
   uint32_t* act = reinterpret_cast<uint32_t*>(smem + L.act);
   uint32_t* accs = reinterpret_cast<uint32_t*>(smem + L.accs);
   double* c_sb = reinterpret_cast<double*>(smem + L.csb);
-  long long* c_zb = reinterpret_cast<long long*>(smem + L.czb);
+  int* c_zb = reinterpret_cast<int*>(smem + L.czb);
   long long* c_cs = reinterpret_cast<long long*>(smem + L.ccs);
   const int tok_n = min(MT, P.m);
   constexpr int kCT = NW * 32;
@@ -524,7 +534,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) gemv_dec_kernel(const __grid_c
       epi_store_v(E, i, j, a, 0.0, 0, 0);
       continue;
     }
-    const long long za = s_za[i], zb = c_zb[rc];
+    const long long za = s_za[i], zb = static_cast<long long>(c_zb[rc]);
     const long long corr = a - za * c_cs[rc] - zb * s_ra[i] + E.k * za * zb;
     const long long o = static_cast<long long>(i) * E.ldo + j;
     if (E.mode == EPI_CORR_I64) {

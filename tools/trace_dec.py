@@ -63,6 +63,10 @@ for i, t in enumerate(rows):
           f"  (CTA start skew {(t[:, 8].max() - a) / 1e3:5.2f} us)")
     tw = t[:, 24:40].astype(float) / ghz / 1e3
     print("             main-loop slot waits per warp: median %.2f us, max %.2f us" % (np.median(tw), tw.max()))
+    en = t[:, 12]
+    print("             true CTA entry: first %.2f us, median %.2f, last %.2f us after previous end; entry->first stamp median %.2f us"
+          % (((en.min() - prev_end) / 1e3) if prev_end else 0, ((np.median(en) - prev_end) / 1e3) if prev_end else 0,
+             ((en.max() - prev_end) / 1e3) if prev_end else 0, np.median(t[:, 8] - en) / 1e3))
     prev_end = e
 first, last = rows[0][:, 8].min(), rows[-1][:, 9].max()
 print(f"  first start -> last end {(last - first) / 1e3:.2f} us = {(last - first) / 1e3 / L:.3f} us per launch")
