@@ -97,6 +97,19 @@ __global__ void prepack_frag_kernel(const uint64_t* __restrict__ planes, int q, 
 // ---------------------------------------------------------------------------
 constexpr int kActThreads = 256;
 
+// non-finite fp16 inputs of one thread's vectors -> atomicMax(~flat index);
+// out of line: it only runs when one was seen
+static __device__ __noinline__ void act_report_nonfinite(const __half* row, int tok, int k, int tid, int nvec,
+                                                         unsigned long long* bad_word) {
+  for (int v = tid; v < nvec; v += kActThreads) {
+    const uint4 q = reinterpret_cast<const uint4*>(row)[v];
+    const __half* h = reinterpret_cast<const __half*>(&q);
+    for (int e = 0; e < 8; ++e)
+      if (!isfinite(__half2float(h[e])))
+        atomicMax(bad_word, ~(static_cast<unsigned long long>(tok) * k + static_cast<unsigned long long>(v) * 8 + e));
+  }
+}
+
 // ROW: write the tcgen05 GEMM's tiled u8 operand (tc_act_offset, `row_ld` =
 // token groups) instead of the GEMV's B-fragment order.
 template <typename T, bool ROW>
@@ -129,83 +142,80 @@ __global__ void __launch_bounds__(kActThreads) act_quant_kernel(const T* __restr
     if (!qp.per_tensor && (k & 7) == 0 && k <= 8 * 4 * kActThreads) {
       const int nvec = k >> 3;
       uint4 v[4];
-      float flo = CUDART_INF_F, fhi = -CUDART_INF_F;
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
         const int idx = tid + r * kActThreads;
-        v[r] = make_uint4(0u, 0u, 0u, 0u);
-        if (idx < nvec) {
-          v[r] = __ldg(reinterpret_cast<const uint4*>(row) + idx);
-          const __half2* h2 = reinterpret_cast<const __half2*>(&v[r]);
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float2 f = __half22float2(h2[e]);
-            if (!isfinite(f.x)) atomicMax(bad_word, ~(static_cast<unsigned long long>(tok) * k + idx * 8 + 2 * e));
-            if (!isfinite(f.y)) atomicMax(bad_word, ~(static_cast<unsigned long long>(tok) * k + idx * 8 + 2 * e + 1));
-            flo = fminf(flo, fminf(f.x, f.y));
-            fhi = fmaxf(fhi, fmaxf(f.x, f.y));
-          }
-        }
+        v[r] = idx < nvec ? __ldg(reinterpret_cast<const uint4*>(row) + idx) : make_uint4(0u, 0u, 0u, 0u);
       }
       // the row is requested: let the dependent GEMV / GEMM start streaming its
       // weights now (issued after our loads, so they do not queue behind them)
       griddep_launch();
+      // range in the order-preserving integer image of fp32 (exact for fp16):
+      // one REDUX per warp; non-finite inputs by exponent test, reported out of line
+      auto ord = [](float f) {
+        const int b = __float_as_int(f);
+        return b >= 0 ? b : b ^ 0x7FFFFFFF;
+      };
+      auto unord = [](int o) { return __int_as_float(o >= 0 ? o : o ^ 0x7FFFFFFF); };
+      int lo = 0x7FFFFFFF, hi = static_cast<int>(0x80000000u);
+      uint32_t bad = 0;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        flo = fminf(flo, __shfl_xor_sync(0xffffffffu, flo, o));
-        fhi = fmaxf(fhi, __shfl_xor_sync(0xffffffffu, fhi, o));
-      }
-      if (lane == 0) {
-        s_lo[warp] = flo;
-        s_hi[warp] = fhi;
-      }
-      __syncthreads();
-      if (tid == 0) {
-        double l = s_lo[0], h = s_hi[0];
-        for (int w = 1; w < kActThreads / 32; ++w) {
-          l = fmin(l, s_lo[w]);
-          h = fmax(h, s_hi[w]);
+      for (int r = 0; r < 4; ++r) {
+        if (tid + r * kActThreads >= nvec) break;
+        bad |= f16x8_nonfinite(v[r]);
+        const __half2* h2 = reinterpret_cast<const __half2*>(&v[r]);
+        __half2 mn = h2[0], mx = h2[0];
+#pragma unroll
+        for (int e = 1; e < 4; ++e) {
+          mn = __hmin2(mn, h2[e]);
+          mx = __hmax2(mx, h2[e]);
         }
-        double step;
-        int z;
-        group_params(qp, l, h, &step, &z);
-        s_step = step;
-        s_z = z;
+        lo = min(lo, min(ord(__low2float(mn)), ord(__high2float(mn))));
+        hi = max(hi, max(ord(__low2float(mx)), ord(__high2float(mx))));
+      }
+      if (bad) act_report_nonfinite(row, tok, k, tid, nvec, bad_word);
+      lo = __reduce_min_sync(0xffffffffu, lo);
+      hi = __reduce_max_sync(0xffffffffu, hi);
+      if (lane == 0) {
+        s_lo[warp] = __int_as_float(lo);  // raw bits, decoded below
+        s_hi[warp] = __int_as_float(hi);
+      }
+      if (tid == 0) s_sum[0] = 0;
+      __syncthreads();
+      // every warp derives step / zero point itself (lanes 0 and 1 in parallel)
+      int l2 = lane < kActThreads / 32 ? __float_as_int(s_lo[lane]) : 0x7FFFFFFF;
+      int h2 = lane < kActThreads / 32 ? __float_as_int(s_hi[lane]) : static_cast<int>(0x80000000u);
+      l2 = __reduce_min_sync(0xffffffffu, l2);
+      h2 = __reduce_max_sync(0xffffffffu, h2);
+      double step = 0.0;
+      int z = 0;
+      float inv32 = 0.0f;
+      if (lane < 2) group_params(qp, unord(l2), unord(h2), &step, &z);
+      if (lane == 1) inv32 = f32_reciprocal(step);
+      step = __shfl_sync(0xffffffffu, step, 0);
+      z = __shfl_sync(0xffffffffu, z, 0);
+      inv32 = __shfl_sync(0xffffffffu, inv32, 1);
+      if (tid == 0) {
         s_a[tok] = step;
         z_a[tok] = z;
       }
-      __syncthreads();
-      const double step = s_step;
-      const float inv32 = f32_reciprocal(step);
-      const int zi = s_z, topi = static_cast<int>(qp.levels - 1);
-      long long rsum = 0;
+      const int topi = static_cast<int>(qp.levels - 1);
+      int rsum = 0;
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
         const int idx = tid + r * kActThreads;
-        if (idx < nvec) {
-          const __half* hv = reinterpret_cast<const __half*>(&v[r]);
-          uint32_t w0 = 0, w1 = 0;
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const unsigned c = quant_code_f32(__half2float(hv[e]), step, inv32, zi, topi);
-            rsum += c;
-            if (e < 4) w0 |= c << (8 * e);
-            else w1 |= c << (8 * (e - 4));
-          }
-          dst[slot_of(2 * idx)] = w0;
-          dst[slot_of(2 * idx + 1)] = w1;
-        }
+        if (idx >= nvec) break;
+        uint32_t w0, w1;
+        rsum += quant_codes8_f16(v[r], step, inv32, z, topi, &w0, &w1);
+        dst[slot_of(2 * idx)] = w0;
+        dst[slot_of(2 * idx + 1)] = w1;
       }
       // zero codes in the k padding of the last block
       for (int v4 = k / 4 + tid; v4 < kzero / 4; v4 += kActThreads) dst[slot_of(v4)] = 0u;
-      rsum = warp_sum(rsum);
-      if (lane == 0) s_sum[warp] = rsum;
+      rsum = __reduce_add_sync(0xffffffffu, rsum);  // < 2^31: <= 255 * 65536
+      if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&s_sum[0]), static_cast<unsigned long long>(rsum));
       __syncthreads();
-      if (tid == 0) {
-        long long rr = 0;
-        for (int w = 0; w < kActThreads / 32; ++w) rr += s_sum[w];
-        rowsum[tok] = rr;
-      }
+      if (tid == 0) rowsum[tok] = s_sum[0];
       return;
     }
   }
