@@ -107,3 +107,48 @@ def test_repeated_calls_are_deterministic(abq, variant):
     first = lin(xd, out_dtype=torch.float64).clone()
     for _ in range(20):
         assert torch.equal(lin(xd, out_dtype=torch.float64, check=False), first)
+
+
+def test_prefetch_next_hint_is_transparent(abq, orc):
+    """abq_weights.prefetch_next only moves the successor's weight traffic into
+    L2 earlier: results with the hint (chained, cyclic) equal those without and
+    the oracle, for every layer of the chain."""
+    rng = np.random.default_rng(11)
+    m, k = 2, 1024
+    layers = []
+    for n, wb, ab in ((700, 4, 4), (300, 2, 8), (513, 8, 3)):
+        x, wc, sb, zb = _case(rng, m, n, k, wb, ab)
+        w = abq.PackedWeights.from_planes(abq.bitpack(wc, wb), sb, zb)
+        layers.append((x, wc, sb, zb, wb, ab, w))
+    plain = [abq.Linear(L[6], abq.QuantSpec(bits=L[5], granularity=abq.api.PER_TOKEN), max_m=m) for L in layers]
+    hinted = [abq.Linear(L[6], abq.QuantSpec(bits=L[5], granularity=abq.api.PER_TOKEN), max_m=m) for L in layers]
+    for i, lin in enumerate(hinted):
+        lin.prefetch_next(hinted[(i + 1) % len(hinted)])
+    for rep in range(3):
+        for (x, wc, sb, zb, wb, ab, _), lp, lh in zip(layers, plain, hinted):
+            xt = torch.from_numpy(x).cuda()
+            y0 = lp(xt, out_dtype=torch.float64).cpu().numpy()
+            y1 = lh(xt, out_dtype=torch.float64).cpu().numpy()
+            ac, sa, za = orc.quantize(x.astype(np.float64), ab, 0, 2)
+            want = orc.quantized_linear(ac, ab, sa, za, wc, wb, sb, zb)
+            assert np.array_equal(y0, want) and np.array_equal(y1, want), (rep, wb, ab)
+
+
+@pytest.mark.parametrize("m,n,k,wb,ab", [
+    (1, 4096, 11008, 2, 8),   # LLaMA-7B down_proj, W2A8 decode (fused ReQuant, K not a 4096 multiple)
+    (3, 5120, 5120, 4, 4),    # LLaMA-13B q_proj, 3 tokens
+    (8, 2048, 4096, 4, 4),    # 8 tokens: ReQuant kernel + GEMV (PDL pair)
+    (1, 1024, 13824, 6, 6),   # LLaMA-13B down_proj K, W6A6 (non power-of-two slices)
+])
+def test_serving_gemv_llama_shapes(abq, orc, m, n, k, wb, ab):
+    rng = np.random.default_rng(m * 131 + k)
+    x, wc, sb, zb = _case(rng, m, n, k, wb, ab)
+    w = abq.PackedWeights.from_planes(abq.bitpack(wc, wb), sb, zb)
+    lin = abq.Linear(w, abq.QuantSpec(bits=ab, granularity=abq.api.PER_TOKEN), max_m=m)
+    xt = torch.from_numpy(x).cuda()
+    y64 = lin(xt, out_dtype=torch.float64).cpu().numpy()
+    y16 = lin(xt, out_dtype=torch.float16).cpu().numpy()
+    ac, sa, za = orc.quantize(x.astype(np.float64), ab, 0, 2)
+    want = orc.quantized_linear(ac, ab, sa, za, wc, wb, sb, zb)
+    assert np.array_equal(y64, want)
+    assert np.array_equal(y16, want.astype(np.float16))
