@@ -14,6 +14,9 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
   python bench.py --steps 20 --warmup 3 --no-cpu --no-check > $O/${TAG}_launches.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemv_dec -s 20 -c 3 -f -o $O/${TAG}_gemv \
   python bench.py --steps 20 --warmup 3 --no-cpu --no-check > $O/${TAG}_ncu_full.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemv_dec -s 20 -c 2 -f -o $O/${TAG}_gemv_nonext \
+  python bench.py --steps 20 --warmup 3 --no-cpu --no-check --no-prefetch-next > $O/${TAG}_ncu_full_nonext.log 2>&1
+timeout 600 python bench.py --no-cpu --no-prefetch-next --steps 20000 > $O/${TAG}_bench_nonext.json 2> $O/${TAG}_bench_nonext.err
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemm_tc -s 2 -c 1 -f -o $O/${TAG}_gemm \
   python tools/trace_gemm.py cfg2_w4a4_m128 > $O/${TAG}_ncu_gemm.log 2>&1
 echo done
