@@ -431,7 +431,16 @@ __global__ void __launch_bounds__(kDecThreads, 1) gemv_dec_kernel(const __grid_c
         asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
                      : "=r"(w[t].x), "=r"(w[t].y), "=r"(w[t].z), "=r"(w[t].w) : "r"(a + t * 512));
     };
-    auto wait_full = [&](int sl, uint32_t p) { mbar_wait_parity(&full[sl], p); };
+    long long t_wait = 0;  // profiling (trace mode only)
+    auto wait_full = [&](int sl, uint32_t p) {
+      if (trace) {
+        const long long t0 = clock64();
+        mbar_wait_parity(&full[sl], p);
+        t_wait += clock64() - t0;
+      } else {
+        mbar_wait_parity(&full[sl], p);
+      }
+    };
     // the last of the UPS warps done with ring slot sl refills it with slot
     // index i + S (its data is in registers: the IMMAs reading it have issued)
     const bool refill = nsl > S_;  // else every slot was loaded once, at kernel start
@@ -467,12 +476,69 @@ __global__ void __launch_bounds__(kDecThreads, 1) gemv_dec_kernel(const __grid_c
         ++frt;
       }
     };
+    // Fast path, layers with 16 k-blocks (K in (3840, 4096]: LLaMA q/k/v/o/
+    // gate/up): warp w owns k-block w of every row-tile of the CTA, so its j-th
+    // unit is row-tile rt_first + j.  Each row-tile gets its own accumulator set
+    // in registers (fully unrolled, static indices): the IMMA chains of all
+    // units are independent and nothing is flushed until the loop is done.
+    constexpr int RTMAX = (QT == 4 || QT == 8) ? 6 : (QT == 2 ? 3 : 0);
+    bool fast_done = false;
+    if constexpr (RTMAX > 0 && NG == 2) {
+      if (kbl == NW && nw <= RTMAX) {
+        constexpr bool DB = QT <= 4;  // two register buffers where they fit
+        if (nw > 0 && cur_kb != warp) load_b(warp);
+        int acc[RTMAX][NA][4];
+#pragma unroll
+        for (int j = 0; j < RTMAX; ++j)
+#pragma unroll
+          for (int f = 0; f < NA; ++f)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) acc[j][f][r] = 0;
+        uint4 wbuf[DB ? 2 : 1][QT];
+        int s0 = grp;  // ring slot of the warp's j-th unit (slot index grp + 2 j)
+        uint32_t p0 = 0;
+        if (DB && nw > 0) {
+          wait_full(s0, p0);
+          lds_unit(s0, wbuf[0]);
+        }
+#pragma unroll
+        for (int j = 0; j < RTMAX; ++j) {
+          if (j < nw) {
+            int s1 = s0 + NG;
+            uint32_t p1 = p0;
+            if (s1 >= S_) {
+              s1 -= S_;
+              p1 ^= 1u;
+            }
+            if constexpr (DB) {
+              if (j + 1 < nw) {
+                wait_full(s1, p1);
+                lds_unit(s1, wbuf[(j + 1) & 1]);
+              }
+            } else {
+              wait_full(s0, p0);
+              lds_unit(s0, wbuf[0]);
+            }
+            mma_unit(acc[j], wbuf[DB ? (j & 1) : 0]);
+            release(s0, grp + NG * j);
+            s0 = s1;
+            p0 = p1;
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < RTMAX; ++j)
+          if (j < nw) flush_set(acc[j], rt_first + j);
+        fast_done = true;
+      }
+    }
+    if (trace && lane == 0) trace[24 + warp] = t_wait;
     int accA[NA][4], accB[NA][4];
 #pragma unroll
     for (int f = 0; f < NA; ++f)
 #pragma unroll
       for (int r = 0; r < 4; ++r) accA[f][r] = accB[f][r] = 0;
-    if constexpr (QT <= 6) {
+    if (fast_done) {
+    } else if constexpr (QT <= 6) {
       uint4 wA[QT], wB[QT];
       int sA = 0, iA = 0, rtA = 0, kbA = 0, sB = 0, iB = 0, rtB = 0, kbB = 0;
       if (nw > 0) fetch(wA, sA, iA, rtA, kbA);
