@@ -32,6 +32,8 @@
 // byte b, stored to the operand at (kc * 128 + r) * 16 (core matrices 8 rows x
 // 16 B: LBO 2048 B along K, SBO 128 B along M).  For q = 8 the packed words
 // ARE that operand.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace abq_dev {
@@ -288,7 +290,8 @@ struct TcParams {
   EpiParams e;
   unsigned long long* bad_word;  // ReQuant status (~index, 0 = none), published to bad_out
   unsigned long long* bad_out;
-  unsigned long long* trace;  // optional [grid][16] clock64 / globaltimer stamps (profiling)
+  unsigned long long* trace;  // optional [grid][64] clock64 / globaltimer stamps (profiling)
+  int dbg;                    // experiments (ABQ_TC_DBG): 2 MMA skips the A wait, 4 no UMMA
 };
 
 // Shared memory: an input ring of kS stages -- the packed weights of a
@@ -431,14 +434,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_con
       int s = 0, a = 0;
       uint32_t ph = 0, pha = 0;
       for (int kb = 0; kb < nkb; ++kb) {
-        if (Sh::kExpand) mbar_wait(&rbar[a], pha);
-        else mbar_wait(&wbar[s], ph);
+        if (!(P.dbg & 2)) {
+          if (Sh::kExpand) mbar_wait(&rbar[a], pha);
+          else mbar_wait(&wbar[s], ph);
+        }
         mbar_wait(&abar[s], ph);
         tc_fence_after();
         if (trace && kb < 16) trace[32 + kb] = clock64();
         const uint64_t ad = a_base + (Sh::kExpand ? a : s) * a_stride, bd = b_base + s * b_stride;
 #pragma unroll
-        for (int j = 0; j < kTcK / 32; ++j) umma_i8(tmem_d, ad + j * a_j, bd + j * b_j, idesc, (kb | j) != 0 ? 1u : 0u);
+        for (int j = 0; j < kTcK / 32; ++j)
+          if (!(P.dbg & 4)) umma_i8(tmem_d, ad + j * a_j, bd + j * b_j, idesc, (kb | j) != 0 ? 1u : 0u);
         tc_commit(&ebar[s]);
         if (Sh::kExpand) tc_commit(&xbar[a]);
         if (++s == S) {
@@ -653,6 +659,7 @@ int run_gemm_tc(const uint32_t* wtc, unsigned q, size_t n, size_t k, const uint8
   P.kblocks = static_cast<int>((k + kTcK - 1) / kTcK);
   P.e = e;
   P.trace = trace_buffer();
+  if (const char* env = std::getenv("ABQ_TC_DBG")) P.dbg = std::atoi(env);
   switch (q) {
     case 1: return launch_tt<1>(P, pdl, st);
     case 2: return launch_tt<2>(P, pdl, st);

@@ -129,9 +129,14 @@ __global__ void __launch_bounds__(kDecThreads, 1) gemv_dec_kernel(const __grid_c
   // ---- 0. this CTA's row-tiles [rt_first, rt_end) = units [U0, U1)
   const int G = gridDim.x;
   const int rowtiles = Pc.rowtiles, kblocks = Pc.kblocks, S = Pc.slots;
-  // (blockIdx.x + 1) * rowtiles < 2^31 for any N the engine accepts: 32-bit math
-  const int rt_first = static_cast<int>((blockIdx.x * static_cast<unsigned>(rowtiles)) / G);
-  const int rt_end = static_cast<int>(((blockIdx.x + 1) * static_cast<unsigned>(rowtiles)) / G);
+  // The rowtiles % G CTAs with one row-tile more come FIRST: the next layer's
+  // CTAs are launched in blockIdx order onto SMs as this layer's CTAs retire,
+  // so its heavy CTAs land on the SMs freed first (by this layer's light ones)
+  // and the late starters are light.
+  const int rt_base = rowtiles / G, rt_heavy = rowtiles - rt_base * G;
+  auto rt_start = [&](int b) { return b < rt_heavy ? b * (rt_base + 1) : rt_heavy + b * rt_base; };
+  const int rt_first = rt_start(blockIdx.x);
+  const int rt_end = rt_start(blockIdx.x + 1);
   const int U0 = rt_first * kblocks, U1 = rt_end * kblocks;
   const int nlrt = rt_end - rt_first;
   const int nsl = (U1 - U0 + UPS - 1) / UPS;
