@@ -102,7 +102,10 @@ int run_prepack_tc(const uint64_t* planes, unsigned q, size_t n, size_t k, uint3
 bool gemm_tc_supported(size_t k);
 int run_gemm_tc(const uint32_t* wtc, unsigned q, size_t n, size_t k, const uint8_t* act, size_t m,
                 const EpiParams& e, cudaStream_t st, unsigned long long* bad_word = nullptr,
-                unsigned long long* bad_out = nullptr, bool pdl = false);
+                unsigned long long* bad_out = nullptr, bool pdl = false, unsigned* sk_flags = nullptr,
+                uint32_t* sk_part = nullptr);
+size_t tc_sk_flag_bytes(size_t n);
+size_t tc_sk_part_bytes(size_t m, size_t n);
 int run_tile_codes(const uint8_t* src, size_t m, size_t k, uint8_t* dst, cudaStream_t st);
 int run_act_quant(const void* x, int x_dtype, size_t m, size_t k, int mt, const QuantParams& qp,
                   uint32_t* out, int row_ld, double* s_a, int32_t* z_a, long long* rowsum,
@@ -533,11 +536,13 @@ int abq_linear_planes(const abq_act* act, const abq_weights* w, void* y, int out
 static size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 
 size_t abq_linear_workspace_bytes(size_t m, size_t n, size_t k, unsigned act_planes) {
-  // [gacc + gcnt for the stream-K decode GEMV][act planes][s_a][z_a][rowsum_a][range 256 B]
-  // [tiled u8 act codes for the tcgen05 GEMM][row-major u8 codes m x k]
-  return align256(imma_ws_bytes(n, k)) + align256(size_t(act_planes) * m * wpr_of(k) * 8) +
-         align256(m * 8) + align256(m * 4) + align256(m * 8) + 256 + align256(tc_act_bytes(m, k)) +
-         align256(m * k);
+  // [gacc + gcnt for the stream-K decode GEMV][stream-K GEMM flags][ReQuant report word, 256 B][act planes][s_a][z_a]
+  // [rowsum_a][range 256 B][tiled u8 act codes for the tcgen05 GEMM][row-major u8 codes m x k]
+  // [stream-K GEMM partial tiles]; everything before the act planes depends on n, k only
+  return align256(imma_ws_bytes(n, k)) + align256(tc_sk_flag_bytes(n)) + 256 +
+         align256(size_t(act_planes) * m * wpr_of(k) * 8) + align256(m * 8) + align256(m * 4) +
+         align256(m * 8) + 256 + align256(tc_act_bytes(m, k)) + align256(m * k) +
+         align256(tc_sk_part_bytes(m, n));
 }
 
 int abq_linear(const void* x, int x_dtype, size_t m, size_t k, const abq_quant_spec* act_spec,
@@ -557,6 +562,12 @@ int abq_linear(const void* x, int x_dtype, size_t m, size_t k, const abq_quant_s
   char* ws = static_cast<char*>(workspace);
   void* ws_imma = ws;
   ws += align256(imma_ws_bytes(w->n, k));
+  unsigned* sk_flags = reinterpret_cast<unsigned*>(ws);
+  ws += align256(tc_sk_flag_bytes(w->n));
+  // zero between calls; at an offset independent of m (the regions after it
+  // move with m and hold data of earlier calls)
+  unsigned long long* bad_word = reinterpret_cast<unsigned long long*>(ws);
+  ws += 256;
   uint64_t* planes = reinterpret_cast<uint64_t*>(ws);
   ws += align256(size_t(p) * m * wpr_of(k) * 8);
   double* sa = reinterpret_cast<double*>(ws);
@@ -593,7 +604,7 @@ int abq_linear(const void* x, int x_dtype, size_t m, size_t k, const abq_quant_s
     // ReQuant straight to u8 codes (K1), then the tcgen05 GEMM with the fused epilogue
     uint8_t* codes = reinterpret_cast<uint8_t*>(range + 32);  // tiled operand
     uint8_t* rowmajor = codes + align256(tc_act_bytes(m, k));
-    unsigned long long* bad_word = range + 2;  // zero-filled workspace word
+    uint32_t* sk_part = reinterpret_cast<uint32_t*>(rowmajor + align256(m * k));
     // per-token (or few-token per-tensor) ReQuant: one CTA per token, PDL into the GEMM
     const bool fast_k1 = act_spec->granularity != ABQ_PER_TENSOR || m <= 8;
     if (fast_k1) {
@@ -622,7 +633,7 @@ int abq_linear(const void* x, int x_dtype, size_t m, size_t k, const abq_quant_s
     e.colsum_b = w->colsums;
     e.k = static_cast<long long>(k);
     st = run_gemm_tc(w->tc, w->q, w->n, k, codes, m, e, s, fast_k1 ? bad_word : nullptr,
-                     fast_k1 ? bad : nullptr, fast_k1);
+                     fast_k1 ? bad : nullptr, fast_k1, sk_flags, sk_part);
     if (st) return st;
   } else {
     st = run_quantize(x, x_dtype, m, k, params_of(*act_spec), nullptr, nullptr, nullptr, planes, p, sa,

@@ -32,6 +32,7 @@
 // byte b, stored to the operand at (kc * 128 + r) * 16 (core matrices 8 rows x
 // 16 B: LBO 2048 B along K, SBO 128 B along M).  For q = 8 the packed words
 // ARE that operand.
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -43,7 +44,10 @@ unsigned long long*& trace_buffer();
 constexpr int kTcM = 128;
 constexpr int kTcK = 128;
 constexpr int kTcThreads = 512;  // warps 8-15 only join the epilogue
-constexpr int kTcColGroups = kTcThreads / 128;  // epilogue: token-column groups per TMEM lane quarter
+constexpr int kTcColGroups = kTcThreads / 128;
+constexpr int kTcIssuers = 3;  // MMA-issuing threads (lane 0 of warps 1 .. kTcIssuers)
+// stream-K schedule by default (ABQ_TC_SK=0/1 overrides)
+constexpr bool kTcStreamKDefault = false;  // epilogue: token-column groups per TMEM lane quarter
 
 // ---------------------------------------------------------------------------
 // prepack: ABQP [q][n][wpr] -> tc code slices
@@ -160,6 +164,18 @@ __device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t adesc, uint64_
       "r"(mask3));
 }
 
+// same with A in tensor memory ([a_tmem]: 128 lanes = rows, K = 32 u8 in 8 columns)
+__device__ __forceinline__ void umma_i8_tmem_a(uint32_t tmem_d, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                               uint32_t accumulate) {
+  const uint32_t mask0 = 0, mask1 = 0, mask2 = 0, mask3 = 0;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, {%5, %6, %7, %8}, p;\n\t}" ::"r"(tmem_d),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(mask0), "r"(mask1), "r"(mask2),
+      "r"(mask3));
+}
+
 // u8 code register o (k = 16 (o >> 2) + 4 (o & 3) + b in byte b) of one row
 // from its 4Q code-slice words: one shift + one mask-merge per slice.
 template <int Q>
@@ -190,7 +206,8 @@ template <int MODE, int TT>
 __device__ __forceinline__ void tc_epilogue(const EpiParams& E, uint32_t taddr, int half, int tok0, int m, int ch,
                                             int n, const double* t_sa, const unsigned* t_za, const unsigned* t_kz,
                                             const unsigned* t_ra, __half* stage, int lch, const double* c_sb,
-                                            const int* c_zb, const int* c_cs, bool k32) {
+                                            const int* c_zb, const int* c_cs, bool k32, const uint32_t* part,
+                                            int npart) {
   constexpr bool kRaw = MODE == EPI_ACC_I32 || MODE == EPI_ACC_I64;
   const bool chan_ok = ch < n;
   // per-channel values, staged in shared memory during the k-loop (loaded here
@@ -220,6 +237,11 @@ __device__ __forceinline__ void tc_epilogue(const EpiParams& E, uint32_t taddr, 
           : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
           : "r"(taddr + static_cast<uint32_t>(c0)));
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    // stream-K: the k-ranges of this tile other CTAs accumulated (exact
+    // modulo 2^32 like the accumulator itself)
+    for (int c = 0; c < npart; ++c)
+#pragma unroll
+      for (int i = 0; i < CW; ++i) v[i] += __ldcg(part + (c * TT + c0 + i) * kTcM + lch);
     if (!chan_ok) continue;
     const bool full = tok0 + c0 + CW <= m;  // uniform: no per-token bound in the common case
     const long long o0 = static_cast<long long>(tok0 + c0) * E.ldo + ch;
@@ -283,6 +305,37 @@ __device__ __forceinline__ void tc_epilogue(const EpiParams& E, uint32_t taddr, 
   }
 }
 
+// stream-K contributor: this CTA's partial accumulator of a tile -> global
+// [column][channel] (coalesced along the TMEM lanes), read back by the tile's
+// finisher CTA.
+template <int TT>
+__device__ __forceinline__ void tc_store_partial(uint32_t taddr, int half, int lch, uint32_t* part) {
+  constexpr int TC = TT / kTcColGroups;
+  constexpr int CW = TC >= 16 ? 16 : (TC >= 8 ? 8 : 4);
+#pragma unroll 1
+  for (int c0 = half * TC; c0 < (half + 1) * TC; c0 += CW) {
+    uint32_t v[CW];
+    if constexpr (CW == 4)
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+                   : "r"(taddr + static_cast<uint32_t>(c0)));
+    else if constexpr (CW == 16)
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+          : "r"(taddr + static_cast<uint32_t>(c0)));
+    else
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+          : "r"(taddr + static_cast<uint32_t>(c0)));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < CW; ++i) __stcg(part + (c0 + i) * kTcM + lch, v[i]);
+  }
+}
+
 struct TcParams {
   const uint32_t* wtc;  // tc code slices
   const uint8_t* act;   // tiled u8 activation codes (tc_act_offset)
@@ -291,8 +344,26 @@ struct TcParams {
   unsigned long long* bad_word;  // ReQuant status (~index, 0 = none), published to bad_out
   unsigned long long* bad_out;
   unsigned long long* trace;  // optional [grid][64] clock64 / globaltimer stamps (profiling)
-  int dbg;                    // experiments (ABQ_TC_DBG): 2 MMA skips the A wait, 4 no UMMA
+  int dbg;                    // experiments (ABQ_TC_DBG): 2 MMA skips the A wait, 4 no UMMA,
+                              // 8 no activation TMA, 16 no weight TMA, 32 no widening (results invalid)
+  // stream-K (one token tile, grid < rowtiles x kblocks units): CTA b owns the
+  // units [b T / G, (b + 1) T / G) of the (row-tile, k-block) sequence; a
+  // tile's finisher is the CTA holding its last k-block, its contributors
+  // (at most 2) publish partial accumulators + a flag.  Flags are zero
+  // between launches (the finisher resets them).
+  int sk;
+  unsigned* sk_flags;  // [rowtiles][2]
+  uint32_t* sk_part;   // [rowtiles][2][TT][128]
 };
+
+// stream-K workspace: flags (zero-filled once by the caller, at an offset that
+// does not depend on m) and partial tiles (no initial value needed)
+size_t tc_sk_flag_bytes(size_t n) { return (n + kTcM - 1) / kTcM * 2 * 4; }
+size_t tc_sk_part_bytes(size_t m, size_t n) {
+  if (m == 0 || m > 256) return 0;
+  const size_t tt = m <= 16 ? 16 : m <= 32 ? 32 : m <= 64 ? 64 : m <= 128 ? 128 : 256;
+  return (n + kTcM - 1) / kTcM * 2 * tt * kTcM * 4;
+}
 
 // Shared memory: an input ring of kS stages -- the packed weights of a
 // 128-k block (or, q = 8, the A operand itself) + the activation tile -- that
@@ -308,7 +379,14 @@ struct TcShape {
   static constexpr int kB = TT * kTcK;            // u8 operand B (activations)
   static constexpr int kW = kExpand ? Q * kTcM * 16 : kA;  // packed slices (or A itself)
   static constexpr int kStage = kW + kB;          // one input stage
-  static constexpr int kSA = kExpand ? 4 : 0;     // widened-A ring depth (2 k-blocks per widening pass)
+  // widened A in tensor memory (tcgen05.st from the widening warps, UMMA
+  // reads A from TMEM): takes the 16 KB store + 16 KB UMMA read per k-block
+  // off the 128 B/clk shared-memory port that bounds the k-loop.  Needs
+  // 2 TT accumulator + 4 x 32 operand columns <= 512.
+  static constexpr bool kTmemA = kExpand && TT <= 128;
+  static constexpr int kXA = kExpand ? (kTmemA ? 8 : 4) : 0;  // widened-A ring depth (2 k-blocks per widening pass)
+  static constexpr int kWG = kTmemA ? 2 : 1;                  // widening warp groups (4 warps = 128 rows each)
+  static constexpr int kSA = kTmemA ? 0 : kXA;               // ... of it in shared memory
   static constexpr int kBudget = 208 * 1024 - kSA * kA;
   static constexpr int kS = kBudget / kStage > 12 ? 12 : kBudget / kStage;
   static constexpr int kSmem = kS * kStage + kSA * kA + 1024;  // + alignment slack
@@ -318,15 +396,18 @@ template <int Q, int TT>
 __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_constant__ TcParams P) {
   using Sh = TcShape<Q, TT>;
   constexpr int S = Sh::kS;
-  constexpr int TMEM_COLS = TT <= 32 ? 32 : (TT <= 64 ? 64 : (TT <= 128 ? 128 : 256));
+  // two accumulators (a stream-K CTA's range touches at most two tiles)
+  constexpr int TMEM_NEED = 2 * TT + (Sh::kTmemA ? Sh::kXA * 32 : 0);
+  constexpr int TMEM_COLS = TMEM_NEED <= 32 ? 32 : (TMEM_NEED <= 64 ? 64 : (TMEM_NEED <= 128 ? 128 : (TMEM_NEED <= 256 ? 256 : 512)));
+  constexpr uint32_t TMEM_A = 2 * TT;  // first column of the widened-A ring (kTmemA)
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  constexpr int SA = Sh::kSA > 0 ? Sh::kSA : 1;
+  constexpr int SA = Sh::kXA > 0 ? Sh::kXA : 1;
   // wbar/abar: stage s weights / activations landed; ebar: MMA done with input
   // stage s; rbar/xbar: widened A slot a filled / free again
   __shared__ __align__(8) uint64_t wbar[S], abar[S], ebar[S], rbar[SA], xbar[SA], done_bar;
   __shared__ uint32_t tmem_base_s;
-  // per-token epilogue values, loaded by the otherwise idle warps 2-3:
+  // per-token epilogue values, loaded by the otherwise idle warps 12-15:
   // s_a, z_a, K z_a, rowsum_a (all non-negative, < 2^32 for K <= 65536)
   __shared__ double t_sa[TT];
   __shared__ unsigned t_za[TT], t_kz[TT], t_ra[TT];
@@ -335,8 +416,24 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_con
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (warp == 7) warm_param_block(P, lane);
-  const int rt = blockIdx.x, tok0 = blockIdx.y * TT;
+  const int tok0 = blockIdx.y * TT;
   const int nkb = P.kblocks;
+  // this CTA's units u = row-tile x nkb + k-block: [U0, U0 + nU), split into
+  // <= 2 segments at a row-tile boundary (seg0 = [U0, U0 + n0))
+  int U0, nU;
+  if (P.sk) {
+    const long long T = static_cast<long long>(P.rowtiles) * nkb, G = gridDim.x;
+    U0 = static_cast<int>(blockIdx.x * T / G);
+    nU = static_cast<int>((blockIdx.x + 1) * T / G) - U0;
+  } else {
+    U0 = blockIdx.x * nkb;
+    nU = nkb;
+  }
+  const int t0 = U0 / nkb, n0 = min(nU, (t0 + 1) * nkb - U0);
+  const int nseg = n0 < nU ? 2 : 1;
+  // the (single) tile this CTA finishes, -1 if none
+  const int fin_seg = U0 + n0 == (t0 + 1) * nkb ? 0 : (nseg == 2 && U0 + nU == (t0 + 2) * nkb ? 1 : -1);
+  const int rt = fin_seg < 0 ? -1 : t0 + fin_seg;
   unsigned long long* trace = P.trace ? P.trace + 64 * (blockIdx.y * gridDim.x + blockIdx.x) : nullptr;
   if (trace && tid == 0) {
     unsigned long long g;
@@ -358,7 +455,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_con
       mbar_init(&rbar[a], 4);  // one arrival per widening warp
       mbar_init(&xbar[a], 1);
     }
-    mbar_init(&done_bar, 1);
+    mbar_init(&done_bar, kTcIssuers);  // one commit per MMA-issuing thread
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -371,31 +468,55 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_con
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_d = tmem_base_s;
+  if (warp >= 12) {
+    // zero both accumulators (the two MMA-issuing threads always accumulate,
+    // so neither has to go first)
+    const uint32_t tz = tmem_d + (static_cast<uint32_t>((warp & 3) * 32) << 16);
+    const uint32_t z = 0u;
+#pragma unroll 1
+    for (int c = 0; c < 2 * TT; c += 16)
+      asm volatile(
+          "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(tz + c),
+          "r"(z)
+          : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
 
   if (warp == 0) {
     if (lane == 0) {
       // ---- TMA producer
       constexpr uint32_t WB = Sh::kW;
       const unsigned char* wsrc = reinterpret_cast<const unsigned char*>(P.wtc) +
-                                  static_cast<size_t>(rt) * nkb * WB;
+                                  static_cast<size_t>(U0) * WB;
       const unsigned char* asrc = P.act + static_cast<size_t>(tok0 / 8) * 1024;
       auto issue_w = [&](int kb) {
         const int s = kb % S;
+        if (P.dbg & 16) {
+          mbar_arrive(&wbar[s]);
+          return;
+        }
         mbar_expect_tx(&wbar[s], WB);
         bulk_g2s(w_of(s), wsrc + static_cast<size_t>(kb) * WB, WB, &wbar[s]);
       };
       auto issue_a = [&](int kb) {
-        const int s = kb % S;
+        const int s = kb % S, kk = (U0 + kb) % nkb;
+        if (P.dbg & 8) {
+          mbar_arrive(&abar[s]);
+          return;
+        }
         mbar_expect_tx(&abar[s], Sh::kB);
-        bulk_g2s(b_of(s), asrc + static_cast<size_t>(kb) * P.groups * 1024, Sh::kB, &abar[s]);
+        bulk_g2s(b_of(s), asrc + static_cast<size_t>(kk) * P.groups * 1024, Sh::kB, &abar[s]);
       };
-      const int pre = nkb < S ? nkb : S;
+      const int pre = nU < S ? nU : S;
       for (int kb = 0; kb < pre; ++kb) issue_w(kb);
       {  // the rest of this CTA's weights: L2 bulk prefetch, so the ring's later
          // weight copies hit L2 instead of waiting on HBM latency
         uint64_t pol;
         asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-        const size_t total = static_cast<size_t>(nkb) * WB;
+        const size_t total = static_cast<size_t>(nU) * WB;
         for (size_t off = static_cast<size_t>(pre) * WB; off < total; off += 32768)
           asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(wsrc + off),
                        "r"(static_cast<uint32_t>(total - off < 32768 ? total - off : 32768)), "l"(pol)
@@ -410,30 +531,38 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_con
         *P.bad_word = 0ull;
       }
       for (int kb = 0; kb < pre; ++kb) issue_a(kb);
-      for (int kb = S; kb < nkb; ++kb) {
+      for (int kb = S; kb < nU; ++kb) {
         mbar_wait(&ebar[kb % S], ((kb / S) - 1) & 1);  // MMA of kb - S done with the stage
         if (trace && kb < S + 16) trace[48 + kb - S] = clock64();
         issue_w(kb);
         issue_a(kb);
       }
     }
-  } else if (warp == 1) {
+  } else if (warp >= 1 && warp <= kTcIssuers) {
     if (lane == 0) {
-      // ---- MMA issuer: D=s32, A=B=u8, both K-major, N=TT, M=128
+      // ---- MMA issuers: D=s32, A=B=u8, both K-major, N=TT, M=128.
+      // kTcIssuers threads (lane 0 of warps 1..) take k-blocks round robin: an mbarrier wait in
+      // the issuing thread stalls that thread's instruction stream for ~40
+      // cycles per UMMA in flight (microbench_umma_mix), so while one waits
+      // the other's UMMAs keep the tensor pipe busy.  Both accumulate into
+      // the (pre-zeroed) accumulator; integer sums commute.
+      const int t = warp - 1;
       const uint32_t idesc = (2u << 4) | (static_cast<uint32_t>(TT >> 3) << 17) |
                              (static_cast<uint32_t>(kTcM >> 4) << 24);
       // descriptors: the start-address field is the low 14 bits of (addr >> 4)
       // and every operand lies below 256 KB, so a descriptor advances by a
       // plain add of (byte offset >> 4) -- precomputed, the issue loop is a
       // handful of uniform ops per UMMA
-      const uint64_t a_base = umma_desc(smem_u32(Sh::kExpand ? x_of(0) : w_of(0)), kTcM * 16, 128);
+      const uint64_t a_base = umma_desc(smem_u32(Sh::kTmemA ? smem : (Sh::kExpand ? x_of(0) : w_of(0))), kTcM * 16, 128);
       const uint64_t b_base = umma_desc(smem_u32(b_of(0)), 128, 1024);
       constexpr uint64_t a_stride = (Sh::kExpand ? Sh::kA : Sh::kStage) >> 4;  // per ring slot
       constexpr uint64_t b_stride = Sh::kStage >> 4;
       constexpr uint64_t a_j = (2 * kTcM * 16) >> 4, b_j = (2 * 128) >> 4;  // per K = 32 step
-      int s = 0, a = 0;
-      uint32_t ph = 0, pha = 0;
-      for (int kb = 0; kb < nkb; ++kb) {
+      for (int kb = t; kb < nU; kb += kTcIssuers) {
+        const int s = kb % S, a = kb % SA;
+        const uint32_t ph = static_cast<uint32_t>(kb / S) & 1u, pha = static_cast<uint32_t>(kb / SA) & 1u;
+        // a new segment (row tile) accumulates into the second TMEM buffer
+        const uint32_t td = tmem_d + (kb >= n0 ? static_cast<uint32_t>(TT) : 0u);
         if (!(P.dbg & 2)) {
           if (Sh::kExpand) mbar_wait(&rbar[a], pha);
           else mbar_wait(&wbar[s], ph);
@@ -443,27 +572,88 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_con
         if (trace && kb < 16) trace[32 + kb] = clock64();
         const uint64_t ad = a_base + (Sh::kExpand ? a : s) * a_stride, bd = b_base + s * b_stride;
 #pragma unroll
-        for (int j = 0; j < kTcK / 32; ++j)
-          if (!(P.dbg & 4)) umma_i8(tmem_d, ad + j * a_j, bd + j * b_j, idesc, (kb | j) != 0 ? 1u : 0u);
+        for (int j = 0; j < kTcK / 32; ++j) {
+          if (P.dbg & 4) continue;
+          if constexpr (Sh::kTmemA) umma_i8_tmem_a(td, tmem_d + TMEM_A + a * 32 + j * 8, bd + j * b_j, idesc, 1u);
+          else umma_i8(td, ad + j * a_j, bd + j * b_j, idesc, 1u);
+        }
         tc_commit(&ebar[s]);
         if (Sh::kExpand) tc_commit(&xbar[a]);
-        if (++s == S) {
-          s = 0;
-          ph ^= 1u;
-        }
-        if (++a == SA) {
-          a = 0;
-          pha ^= 1u;
-        }
       }
       tc_commit(&done_bar);
       if (trace) trace[3] = clock64();
     }
-  } else if (warp == 2 || warp == 3) {
+  } else if (Sh::kExpand && warp >= 4 && warp < 4 + 4 * Sh::kWG) {
+    // ---- widen packed code slices of row r into the A operand, two k-blocks
+    // per pass (their loads, widening and stores interleave: one k-block per
+    // pass left each warp a ~600-cycle dependent chain per k-block, which
+    // paced the whole k-loop)
+    // kWG groups of 4 warps take alternate k-block pairs (TMEM lane quarter = warp % 4)
+    const int r = (tid - 128) & (kTcM - 1), grp = (warp - 4) >> 2;
+    auto widen_one = [&](int kb, const uint4 (&w)[Q > 0 ? Q : 1]) {
+      const int a = kb % SA;
+      if (kb >= SA) mbar_wait(&xbar[a], static_cast<uint32_t>(kb / SA - 1) & 1u);  // MMA of kb - SA done
+      if constexpr (Sh::kTmemA) {
+        // row r = TMEM lane r (warp w owns lanes 32 (w % 4) ..), register o -> column o
+        tc_fence_after();
+        uint32_t v[32];
+#pragma unroll
+        for (int o = 0; o < 32; ++o) v[o] = widen_row<Q>(w, o);
+        const uint32_t ta = tmem_d + (static_cast<uint32_t>((warp & 3) * 32) << 16) + TMEM_A + a * 32;
+        asm volatile(
+            "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+            "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(ta),
+            "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+            "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]),
+            "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]),
+            "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+            : "memory");
+      } else {
+        uint4* adst = reinterpret_cast<uint4*>(x_of(a)) + r;
+#pragma unroll
+        for (int kc = 0; kc < 8; ++kc)
+          adst[kc * kTcM] = make_uint4(widen_row<Q>(w, 4 * kc), widen_row<Q>(w, 4 * kc + 1),
+                                       widen_row<Q>(w, 4 * kc + 2), widen_row<Q>(w, 4 * kc + 3));
+      }
+    };
+    auto load_one = [&](int kb, uint4 (&w)[Q > 0 ? Q : 1]) {
+      const int s = kb % S;
+      mbar_wait(&wbar[s], static_cast<uint32_t>(kb / S) & 1u);
+      const uint32_t wsl = smem_u32(w_of(s)) + r * 16;
+#pragma unroll
+      for (int t = 0; t < Q; ++t)
+        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(w[t].x), "=r"(w[t].y), "=r"(w[t].z), "=r"(w[t].w)
+                     : "r"(wsl + t * kTcM * 16));
+    };
+    for (int kb = 2 * grp; kb < nU; kb += 2 * Sh::kWG) {
+      const bool two = kb + 1 < nU;
+      uint4 w0[Q > 0 ? Q : 1], w1[Q > 0 ? Q : 1];
+      if (!(P.dbg & 32)) {
+        load_one(kb, w0);
+        if (two) load_one(kb + 1, w1);
+        widen_one(kb, w0);
+        if (two) widen_one(kb + 1, w1);
+      }
+      if constexpr (Sh::kTmemA) {
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc_fence_before();
+      } else {
+        fence_async_smem();  // generic-proxy stores -> visible to the tensor core
+      }
+      __syncwarp();
+      if (trace && tid == 128 && kb < 16) trace[16 + kb] = clock64();
+      if (lane == 0) {
+        mbar_arrive(&rbar[kb % SA]);
+        if (two) mbar_arrive(&rbar[(kb + 1) % SA]);
+      }
+    }
+  }
+  if (warp >= 12) {  // idle during the k-loop: per-token epilogue values (after the ReQuant kernel)
     const EpiParams& E = P.e;
     if (E.mode != EPI_ACC_I32 && E.mode != EPI_ACC_I64) {
       asm volatile("griddepcontrol.wait;" ::: "memory");  // ReQuant results visible
-      for (int i = tid - 64; i < TT; i += 64) {
+      for (int i = tid - 384; i < TT; i += 128) {
         const int tk = tok0 + i;
         if (tk < P.m) {
           const int za = E.z_a[tk * E.za_stride];
@@ -474,46 +664,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_con
         }
       }
     }
-  } else if (Sh::kExpand && warp >= 4 && warp < 8) {
-    // ---- widen packed code slices of row r into the A operand, two k-blocks
-    // per pass (their loads, widening and stores interleave: one k-block per
-    // pass left each warp a ~600-cycle dependent chain per k-block, which
-    // paced the whole k-loop)
-    const int r = tid - 128;
-    auto widen_one = [&](int kb, const uint4 (&w)[Q > 0 ? Q : 1]) {
-      const int a = kb % SA;
-      if (kb >= SA) mbar_wait(&xbar[a], static_cast<uint32_t>(kb / SA - 1) & 1u);  // MMA of kb - SA done
-      uint4* adst = reinterpret_cast<uint4*>(x_of(a)) + r;
-#pragma unroll
-      for (int kc = 0; kc < 8; ++kc)
-        adst[kc * kTcM] = make_uint4(widen_row<Q>(w, 4 * kc), widen_row<Q>(w, 4 * kc + 1),
-                                     widen_row<Q>(w, 4 * kc + 2), widen_row<Q>(w, 4 * kc + 3));
-    };
-    auto load_one = [&](int kb, uint4 (&w)[Q > 0 ? Q : 1]) {
-      const int s = kb % S;
-      mbar_wait(&wbar[s], static_cast<uint32_t>(kb / S) & 1u);
-      const uint4* wsl = reinterpret_cast<const uint4*>(w_of(s)) + r;
-#pragma unroll
-      for (int t = 0; t < Q; ++t) w[t] = wsl[t * kTcM];
-    };
-    for (int kb = 0; kb < nkb; kb += 2) {
-      const bool two = kb + 1 < nkb;
-      uint4 w0[Q > 0 ? Q : 1], w1[Q > 0 ? Q : 1];
-      load_one(kb, w0);
-      if (two) load_one(kb + 1, w1);
-      widen_one(kb, w0);
-      if (two) widen_one(kb + 1, w1);
-      fence_async_smem();  // generic-proxy stores -> visible to the tensor core
-      __syncwarp();
-      if (trace && tid == 128 && kb < 16) trace[16 + kb] = clock64();
-      if (lane == 0) {
-        mbar_arrive(&rbar[kb % SA]);
-        if (two) mbar_arrive(&rbar[(kb + 1) % SA]);
-      }
-    }
   }
-  if (warp >= 8 && warp < 12) {  // idle during the k-loop: this tile's channel parameters
-    const int c = tid - 256, j = rt * kTcM + c;
+  if (warp >= 12 && rt >= 0) {  // ... and the finished tile's channel parameters
+    const int c = tid - 384, j = rt * kTcM + c;
     const EpiParams& E = P.e;
     const bool ok = j < P.n && E.mode != EPI_ACC_I32 && E.mode != EPI_ACC_I64;
     c_sb[c] = ok ? E.s_b[j * E.sb_stride] : 0.0;
@@ -529,34 +682,81 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_con
   tc_fence_after();
   if (trace && tid == 0) trace[4] = clock64();
   const int quarter = warp & 3, half = warp >> 2;
-  const int lch = quarter * 32 + lane, ch = rt * kTcM + lch;
-  __half* stage = reinterpret_cast<__half*>(smem);  // the operand ring is idle now
-  const uint32_t taddr = tmem_d + (static_cast<uint32_t>(quarter * 32) << 16);
-  switch (P.e.mode) {
-    case EPI_ACC_I32: tc_epilogue<EPI_ACC_I32, TT>(P.e, taddr, half, tok0, P.m, ch, P.n, t_sa, t_za, t_kz, t_ra, stage, lch, c_sb, c_zb, c_cs, P.k <= 32768); break;
-    case EPI_ACC_I64: tc_epilogue<EPI_ACC_I64, TT>(P.e, taddr, half, tok0, P.m, ch, P.n, t_sa, t_za, t_kz, t_ra, stage, lch, c_sb, c_zb, c_cs, P.k <= 32768); break;
-    case EPI_F64: tc_epilogue<EPI_F64, TT>(P.e, taddr, half, tok0, P.m, ch, P.n, t_sa, t_za, t_kz, t_ra, stage, lch, c_sb, c_zb, c_cs, P.k <= 32768); break;
-    case EPI_F16: tc_epilogue<EPI_F16, TT>(P.e, taddr, half, tok0, P.m, ch, P.n, t_sa, t_za, t_kz, t_ra, stage, lch, c_sb, c_zb, c_cs, P.k <= 32768); break;
-    case EPI_F32: tc_epilogue<EPI_F32, TT>(P.e, taddr, half, tok0, P.m, ch, P.n, t_sa, t_za, t_kz, t_ra, stage, lch, c_sb, c_zb, c_cs, P.k <= 32768); break;
-    default: tc_epilogue<EPI_CORR_I64, TT>(P.e, taddr, half, tok0, P.m, ch, P.n, t_sa, t_za, t_kz, t_ra, stage, lch, c_sb, c_zb, c_cs, P.k <= 32768); break;
+  const int lch = quarter * 32 + lane;
+  const uint32_t tlane = tmem_d + (static_cast<uint32_t>(quarter * 32) << 16);
+  const uint32_t* part = nullptr;
+  int npart = 0;
+  if (P.sk) {
+    // stream-K hand-off.  Contributions are published before any finisher
+    // waits (a CTA's contributed segment is always its last one, its finished
+    // segment its first), so no chain of CTAs serialises.
+    const long long T = static_cast<long long>(P.rowtiles) * nkb, G = gridDim.x;
+    auto cta_of = [&](long long u) { return static_cast<int>(((u + 1) * G - 1) / T); };
+    const int con_seg = nseg == 2 ? 1 : (fin_seg < 0 ? 0 : -1);
+    if (con_seg >= 0) {
+      const int tcon = t0 + con_seg, slot = static_cast<int>(blockIdx.x) - cta_of(static_cast<long long>(tcon) * nkb);
+      tc_store_partial<TT>(tlane + (con_seg ? static_cast<uint32_t>(TT) : 0u), half, lch,
+                           P.sk_part + (static_cast<size_t>(tcon) * 2 + slot) * TT * kTcM);
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence();
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(P.sk_flags + tcon * 2 + slot), "r"(1u) : "memory");
+        if (trace) trace[10] = clock64();
+      }
+    }
+    if (rt >= 0) {
+      npart = static_cast<int>(blockIdx.x) - cta_of(static_cast<long long>(rt) * nkb);
+      part = P.sk_part + static_cast<size_t>(rt) * 2 * TT * kTcM;
+      if (tid == 0) {
+        for (int c = 0; c < npart; ++c) {
+          unsigned f = 0;
+          for (;;) {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(P.sk_flags + rt * 2 + c) : "memory");
+            if (f) break;
+            __nanosleep(64);
+          }
+          P.sk_flags[rt * 2 + c] = 0u;  // consumed: zero for the next launch
+        }
+        if (trace) {
+          trace[11] = clock64();
+          trace[12] = (static_cast<unsigned long long>(nU) << 32) | (static_cast<unsigned>(npart) << 8) |
+                      static_cast<unsigned>(nseg);
+        }
+      }
+      __syncthreads();
+    }
   }
-  if (trace && tid == 0) trace[6] = clock64();
-  if (P.e.mode == EPI_F16) {
-    // staged fp16 tile -> global, 8 channels (16 B) per store where aligned
-    __syncthreads();
-    if (trace && tid == 0) trace[7] = clock64();
-    const int rows = min(TT, P.m - tok0), cols = min(kTcM, P.n - rt * kTcM);
-    __half* out = static_cast<__half*>(P.e.out);
-    const bool vec = (P.e.ldo & 7) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
-    for (int idx = tid; idx < rows * (kTcM / 8); idx += kTcThreads) {
-      const int r = idx / (kTcM / 8), c8 = (idx % (kTcM / 8)) * 8;
-      if (c8 >= cols) continue;
-      const __half* src = stage + r * kTcM + c8;
-      __half* dst = out + static_cast<long long>(tok0 + r) * P.e.ldo + rt * kTcM + c8;
-      if (vec && c8 + 8 <= cols) {
-        *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(src);
-      } else {
-        for (int j = 0; j < 8 && c8 + j < cols; ++j) dst[j] = src[j];
+  if (rt >= 0) {
+    const int ch = rt * kTcM + lch;
+    __half* stage = reinterpret_cast<__half*>(smem);  // the operand ring is idle now
+    const uint32_t taddr = tlane + (fin_seg == 1 ? static_cast<uint32_t>(TT) : 0u);
+    const bool k32 = P.k <= 32768;
+    switch (P.e.mode) {
+      case EPI_ACC_I32: tc_epilogue<EPI_ACC_I32, TT>(P.e, taddr, half, tok0, P.m, ch, P.n, t_sa, t_za, t_kz, t_ra, stage, lch, c_sb, c_zb, c_cs, k32, part, npart); break;
+      case EPI_ACC_I64: tc_epilogue<EPI_ACC_I64, TT>(P.e, taddr, half, tok0, P.m, ch, P.n, t_sa, t_za, t_kz, t_ra, stage, lch, c_sb, c_zb, c_cs, k32, part, npart); break;
+      case EPI_F64: tc_epilogue<EPI_F64, TT>(P.e, taddr, half, tok0, P.m, ch, P.n, t_sa, t_za, t_kz, t_ra, stage, lch, c_sb, c_zb, c_cs, k32, part, npart); break;
+      case EPI_F16: tc_epilogue<EPI_F16, TT>(P.e, taddr, half, tok0, P.m, ch, P.n, t_sa, t_za, t_kz, t_ra, stage, lch, c_sb, c_zb, c_cs, k32, part, npart); break;
+      case EPI_F32: tc_epilogue<EPI_F32, TT>(P.e, taddr, half, tok0, P.m, ch, P.n, t_sa, t_za, t_kz, t_ra, stage, lch, c_sb, c_zb, c_cs, k32, part, npart); break;
+      default: tc_epilogue<EPI_CORR_I64, TT>(P.e, taddr, half, tok0, P.m, ch, P.n, t_sa, t_za, t_kz, t_ra, stage, lch, c_sb, c_zb, c_cs, k32, part, npart); break;
+    }
+    if (trace && tid == 0) trace[6] = clock64();
+    if (P.e.mode == EPI_F16) {
+      // staged fp16 tile -> global, 8 channels (16 B) per store where aligned
+      __syncthreads();
+      if (trace && tid == 0) trace[7] = clock64();
+      const int rows = min(TT, P.m - tok0), cols = min(kTcM, P.n - rt * kTcM);
+      __half* out = static_cast<__half*>(P.e.out);
+      const bool vec = (P.e.ldo & 7) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+      for (int idx = tid; idx < rows * (kTcM / 8); idx += kTcThreads) {
+        const int r = idx / (kTcM / 8), c8 = (idx % (kTcM / 8)) * 8;
+        if (c8 >= cols) continue;
+        const __half* src = stage + r * kTcM + c8;
+        __half* dst = out + static_cast<long long>(tok0 + r) * P.e.ldo + rt * kTcM + c8;
+        if (vec && c8 + 8 <= cols) {
+          *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(src);
+        } else {
+          for (int j = 0; j < 8 && c8 + j < cols; ++j) dst[j] = src[j];
+        }
       }
     }
   }
@@ -611,7 +811,19 @@ static int launch_tc(const TcParams& P, bool pdl, cudaStream_t st) {
   auto kern = gemm_tc_kernel<Q, TT>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Sh::kSmem);
   if (err != cudaSuccess) return fail(ABQ_ERR_CUDA, "gemm_tc: smem attribute: %s", cudaGetErrorString(err));
-  dim3 grid(static_cast<unsigned>(P.rowtiles), static_cast<unsigned>((P.m + TT - 1) / TT));
+  TcParams L = P;
+  const int gy = (P.m + TT - 1) / TT;
+  int gx = P.rowtiles;
+  // stream-K when one token tile leaves SMs idle: G = min(SMs, 2 x row-tiles)
+  // CTAs share the (row-tile, k-block) units; G <= 2 rowtiles keeps every
+  // range >= kblocks / 2 (<= 2 contributors per tile), G > rowtiles keeps it
+  // <= kblocks (<= 2 segments per CTA)
+  if (L.sk && gy == 1 && P.kblocks >= 2 && P.rowtiles < num_sms()) {
+    gx = std::min(num_sms(), 2 * P.rowtiles);
+  } else {
+    L.sk = 0;
+  }
+  dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(gy));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(kTcThreads);
@@ -622,7 +834,7 @@ static int launch_tc(const TcParams& P, bool pdl, cudaStream_t st) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  err = cudaLaunchKernelEx(&cfg, kern, P);
+  err = cudaLaunchKernelEx(&cfg, kern, L);
   if (err != cudaSuccess) return fail(ABQ_ERR_CUDA, "gemm_tc: launch: %s", cudaGetErrorString(err));
   ABQ_LAUNCHED();
   return ABQ_OK;
@@ -643,7 +855,7 @@ bool gemm_tc_supported(size_t k) { return k > 0 && k <= 65536 && k % 16 == 0; }
 // act: tiled u8 codes (tc_act_offset, groups = tc_act_groups(m)), 16-B aligned
 int run_gemm_tc(const uint32_t* wtc, unsigned q, size_t n, size_t k, const uint8_t* act, size_t m,
                 const EpiParams& e, cudaStream_t st, unsigned long long* bad_word,
-                unsigned long long* bad_out, bool pdl) {
+                unsigned long long* bad_out, bool pdl, unsigned* sk_flags, uint32_t* sk_part) {
   if (m == 0 || n == 0) return ABQ_OK;
   TcParams P{};
   P.bad_word = bad_word;
@@ -660,6 +872,13 @@ int run_gemm_tc(const uint32_t* wtc, unsigned q, size_t n, size_t k, const uint8
   P.e = e;
   P.trace = trace_buffer();
   if (const char* env = std::getenv("ABQ_TC_DBG")) P.dbg = std::atoi(env);
+  const char* sk_env = std::getenv("ABQ_TC_SK");
+  const bool sk_on = sk_env ? std::atoi(sk_env) != 0 : kTcStreamKDefault;
+  if (sk_flags && sk_part && m <= 256 && sk_on) {
+    P.sk = 1;
+    P.sk_flags = sk_flags;
+    P.sk_part = sk_part;
+  }
   switch (q) {
     case 1: return launch_tt<1>(P, pdl, st);
     case 2: return launch_tt<2>(P, pdl, st);

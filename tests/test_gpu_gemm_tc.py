@@ -78,3 +78,37 @@ def test_btc_gemm_matches_oracle(abq, orc, m, n, k, p, q):
     b = rng.integers(0, 1 << q, (n, k), dtype=np.uint8)
     got = abq.gemm_btc(abq.bitpack(a, p), abq.bitpack(b, q)).cpu().numpy()
     assert np.array_equal(got, orc.gemm_codes(a, p, b, q))
+
+
+@pytest.mark.parametrize("m,n,k,wbits,abits", [
+    (128, 11008, 4096, 4, 4),   # LLaMA-7B up: 86 row-tiles -> 148 CTAs, <= 2 contributors per tile
+    (9, 128, 32, 3, 5),         # one row-tile, two k-blocks -> 2 CTAs
+    (200, 300, 48 * 16, 2, 8),  # 3 row-tiles, 6 k-blocks, token tile 256
+    (64, 5000, 3 * 128, 8, 8),  # odd k-block count
+    (33, 19000, 1024, 5, 3),    # row-tiles (149) >= SMs: no stream-K
+    (100, 640, 11008, 6, 6),    # long K, 5 row-tiles -> 10 CTAs of ~43 k-blocks
+])
+def test_tc_stream_k(abq, orc, m, n, k, wbits, abits, monkeypatch):
+    """stream-K prefill GEMM (one token tile, row-tiles < SMs): bit-exact against
+    the oracle, repeated calls (the hand-off flags reset themselves), a
+    smaller m through the same workspace, and equal to the one-CTA-per-tile
+    schedule (ABQ_TC_SK=0)."""
+    monkeypatch.setenv("ABQ_TC_SK", "1")
+    rng = np.random.default_rng(m + n + k)
+    wc = rng.integers(0, 1 << wbits, (n, k), dtype=np.uint8)
+    sb = rng.uniform(1e-3, 1e-2, n)
+    zb = rng.integers(0, 1 << wbits, n).astype(np.int32)
+    w = abq.PackedWeights.from_planes(abq.bitpack(wc, wbits), sb, zb)
+    lin = abq.Linear(w, abq.QuantSpec(bits=abits, granularity=abq.api.PER_TOKEN), max_m=m)
+    for mm in (m, max(9, m // 2 + 1), m):
+        x = (rng.standard_normal((mm, k)) * 2).astype(np.float16)
+        xd = torch.from_numpy(x).cuda()
+        ac, sa, za = orc.quantize(x.astype(np.float64), abits, 0, 2)
+        want = orc.quantized_linear(ac, abits, sa, za, wc, wbits, sb, zb)
+        for rep in range(2):
+            y = lin(xd, out_dtype=torch.float64).cpu().numpy()
+            assert np.array_equal(y, want), (mm, rep)
+        y16 = lin(xd, out_dtype=torch.float16).cpu().numpy()
+        assert np.array_equal(y16, want.astype(np.float16)), mm
+    monkeypatch.setenv("ABQ_TC_SK", "0")
+    assert np.array_equal(lin(xd, out_dtype=torch.float64).cpu().numpy(), want)

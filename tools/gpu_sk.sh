@@ -1,0 +1,4 @@
+O=gpurun_out; T=${1:-sk}
+timeout 900 python -m pytest tests/test_gpu_gemm_tc.py -m gpu -x -q > $O/${T}_pytest.log 2>&1; echo "rc=$?" >> $O/${T}_pytest.log
+for w in cfg2_w4a4_m128 cfg2_w8a8_m128; do timeout 120 python tools/trace_gemm.py $w; ABQ_TC_SK=1 timeout 120 python tools/trace_gemm.py $w; done > $O/${T}_trace.txt 2>&1
+for w in cfg2_w4a4_m128 cfg2_w8a8_m128 cfg2_w4a4_m16; do timeout 300 python bench.py --steps 3000 --warmup 50 --no-cpu --no-check --workload $w; ABQ_TC_SK=1 timeout 300 python bench.py --steps 3000 --warmup 50 --no-cpu --no-check --workload $w; done > $O/${T}_bench.json 2>&1

@@ -38,13 +38,14 @@ def us(a):
 
 
 print(f"{name}: {len(t)} CTAs")
-for j in range(6):
-    c = t[:, 10 + j]
-    ok = c > 0
-    if ok.any():
-        print(f"  MMA of k-block {8 * j:3d} issued   median {np.median(us(c[ok] - t[ok, 0])):7.2f} us after CTA start")
+print(f"  first MMA issued         median {np.median(us(t[:, 32] - t[:, 0])):7.2f} us after CTA start")
 print(f"  last MMA issued          median {np.median(us(t[:, 3] - t[:, 0])):7.2f} us")
 print(f"  epilogue start (done)    median {np.median(us(t[:, 4] - t[:, 0])):7.2f} us")
+con, fin = t[:, 10] > 0, t[:, 11] > 0
+if con.any():  # stream-K
+    print(f"  stream-K: units/CTA {np.unique(t[:, 12] >> 32)}, contributors/finish {np.unique((t[fin, 12] >> 8) & 255)}")
+    print(f"  partial published        median {np.median(us(t[con, 10] - t[con, 0])):7.2f} us")
+    print(f"  finisher wait done       median {np.median(us(t[fin, 11] - t[fin, 0])):7.2f} us  max {us(t[fin, 11] - t[fin, 0]).max():7.2f}")
 print(f"  tid0 epilogue math done median {np.median(us(t[:, 6] - t[:, 0])):7.2f} us; after barrier {np.median(us(t[:, 7] - t[:, 0])):7.2f}")
 print(f"  CTA end                  median {np.median(us(t[:, 5] - t[:, 0])):7.2f} us  max {us(t[:, 5] - t[:, 0]).max():7.2f}")
 print(f"  launch span (globaltimer) {(t[:, 9].max() - t[:, 8].min()) / 1e3:7.2f} us; CTA start skew "
