@@ -252,6 +252,19 @@ typedef enum {
 int abq_set_gemv_variant(int variant);
 int abq_get_gemv_variant(void);
 
+/* prefill GEMM schedule (tcgen05 path, m >= 9): one CTA per 128-channel row
+ * tile, or stream-K over all SMs (CTAs share (row-tile, k-block) units and
+ * hand partial tiles to the tile's finisher).  Results are identical; the
+ * GPU-side counterpart of the reference's tile choice, picked by
+ * abq.autotune_linear.  Process-global, like engine_threads (gemm.hpp:81-84). */
+typedef enum {
+  ABQ_GEMM_AUTO = 0,
+  ABQ_GEMM_CLASSIC = 1,
+  ABQ_GEMM_STREAM_K = 2
+} abq_gemm_schedule;
+int abq_set_gemm_schedule(int schedule);
+int abq_get_gemm_schedule(void);
+
 /* Profiling hook: when set (device buffer of >= 4 u64 per CTA, NULL = off),
  * the decode GEMV records %globaltimer at kernel start, after the ReQuant
  * prologue, after the main loop and before the split-tile epilogue. */

@@ -89,6 +89,8 @@ _SIGNATURES = {
                         _P, _P]),
     "abq_set_gemv_variant": (_I, [_I]),
     "abq_get_gemv_variant": (_I, []),
+    "abq_set_gemm_schedule": (_I, [_I]),
+    "abq_get_gemm_schedule": (_I, []),
     "abq_set_trace_buffer": (_I, [_P]),
 }
 

@@ -9,7 +9,9 @@ functions in namespace ``abq`` (paths relative to /root/reference/proj):
   gemm.hpp:19-307       TileConfig, default_tile, GemmStats, fits_int32, engine_threads,
                         gemm_arbitrary(_wide), gemm_naive, zero_point_correct,
                         code_rowsums, quantized_linear
-  tune.hpp:17-23        padding_redundancy
+  tune.hpp:17-192       padding_redundancy, enumerate_tile_candidates, BenchRecord,
+                        AutotuneResult, autotune (+ autotune_linear: the engine's own
+                        schedules -- GEMV variant, prefill GEMM classic / stream-K)
 
 Every numeric result is computed by the sm_100a kernels behind the C-ABI
 (include/abq_cuda.h); tensors live on the GPU (torch CUDA storage is used for
@@ -20,7 +22,7 @@ from __future__ import annotations
 
 import ctypes as C
 import dataclasses
-from typing import Optional
+from typing import List, Optional
 
 import numpy as np
 import torch
@@ -333,6 +335,225 @@ def padding_redundancy(m: int, p: int, mma_m: int) -> float:
     out = C.c_double()
     _check(L.lib().abq_padding_redundancy(m, p, mma_m, C.byref(out)))
     return out.value
+
+
+# ---------------------------------------------------------------------------
+# tuning (tune.hpp)
+# ---------------------------------------------------------------------------
+_WARP_LAYOUTS = ((1, 1), (1, 2), (1, 4), (2, 2), (2, 4), (4, 4))  # tune.hpp:28-32
+
+
+def _total_row_padding(m: int, p: int, bm: int, mma_m: int) -> int:
+    """detail::total_row_padding  tune.hpp:35-44."""
+    pad = 0
+    for m0 in range(0, m, bm):
+        e = p * min(bm, m - m0)
+        pad += -(-e // mma_m) * mma_m - e
+    return pad
+
+
+def enumerate_tile_candidates(p: int, q: int, m: int, n: int, k: int) -> List[TileConfig]:
+    """enumerate_tile_candidates  tune.hpp:51-92: warp layout x power-of-two inner
+    tiles x BK grid, block tile derived from the layout, deduplicated, then only
+    the block heights with the least row padding for (p, M).  Host logic; the
+    validity check is the engine's (abq_tile_valid)."""
+    if not (1 <= p <= 8 and 1 <= q <= 8):
+        raise ValueError("enumerate_tile_candidates: p,q must be in [1,8]")
+    seen, raw = set(), []
+    for lm, ln in _WARP_LAYOUTS:
+        for wm in (8, 16, 32, 64):
+            for wn in (8, 16, 32, 64):
+                for bk in (128, 256, 384, 512):
+                    t = TileConfig(BM=-(-(lm * wm) // p), BN=-(-(ln * wn) // q), BK=bk, WM=wm, WN=wn,
+                                   WK=TileConfig.mma_k)
+                    if not t.valid(p, q):
+                        continue
+                    key = (t.BM, t.BN, t.BK, t.WM, t.WN)
+                    if key in seen:
+                        continue
+                    seen.add(key)
+                    raw.append(t)
+    best = min((_total_row_padding(m, p, t.BM, TileConfig.mma_m) for t in raw), default=None)
+    out = [t for t in raw if _total_row_padding(m, p, t.BM, TileConfig.mma_m) == best]
+    return out or [default_tile(p, q)]
+
+
+@dataclasses.dataclass
+class BenchRecord:
+    """BenchRecord  tune.hpp:94-105 (one CSV row per timed candidate)."""
+    config_id: str = ""
+    BM: int = 0
+    BN: int = 0
+    BK: int = 0
+    WM: int = 0
+    WN: int = 0
+    p: int = 0
+    q: int = 0
+    M: int = 0
+    N: int = 0
+    K: int = 0
+    median_us: float = 0.0
+    tops: float = 0.0  # 2*M*N*K ops over the median latency
+
+    @staticmethod
+    def csv_header() -> str:
+        return "config_id,BM,BN,BK,WM,WN,p,q,M,N,K,median_us,tops"
+
+    def csv_row(self) -> str:
+        return ",".join(str(v) for v in dataclasses.astuple(self))
+
+
+@dataclasses.dataclass
+class AutotuneResult:
+    """AutotuneResult  tune.hpp:136-139 (best: a TileConfig for autotune, the
+    schedule name for autotune_linear)."""
+    best: object
+    records: List[BenchRecord]
+
+
+def tops_of(m: int, n: int, k: int, us: float) -> float:
+    """detail::tops_of  tune.hpp:129-131."""
+    return 2.0 * m * n * k / (us * 1e6)
+
+
+def _time_median_us(fn, trials: int) -> float:
+    """detail::time_median_us  tune.hpp:114-127 on the device: one discarded
+    warm-up, then `trials` calls each bracketed by CUDA events on the current
+    stream; median (mean of the middle two for even counts)."""
+    fn()
+    times = []
+    st = torch.cuda.current_stream()
+    for _ in range(trials):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        fn()
+        e1.record(st)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1) * 1e3)
+    times.sort()
+    h = len(times) // 2
+    return times[h] if len(times) % 2 else 0.5 * (times[h - 1] + times[h])
+
+
+def _time_graph_us(fn, trials: int, reps: int = 20) -> float:
+    """Per-call device time of `fn` replayed from a CUDA graph of `reps` calls
+    (the serving path; eager timing would measure host launch overhead):
+    median over `trials` replays bracketed by CUDA events."""
+    fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(reps):
+            fn()
+    g.replay()
+    torch.cuda.synchronize()
+    times = []
+    for _ in range(trials):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g.replay()
+        e1.record()
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1) * 1e3 / reps)
+    times.sort()
+    h = len(times) // 2
+    return times[h] if len(times) % 2 else 0.5 * (times[h - 1] + times[h])
+
+
+def autotune(candidates: List[TileConfig], a: "BitPlaneMatrix", bt: "BitPlaneMatrix",
+             trials: int = 3) -> AutotuneResult:
+    """autotune  tune.hpp:141-192: time every candidate through gemm_arbitrary
+    (gemm_arbitrary_wide when the int32 bound does not hold), verify each result
+    bit for bit against the first candidate's (a mismatch is a hard Error), and
+    return the fastest.  Timing is device time (CUDA events) instead of the
+    reference's steady_clock."""
+    if not candidates:
+        raise ValueError("autotune: no candidates")
+    if trials < 3:
+        raise ValueError("autotune: need at least 3 trials")
+    wide = not fits_int32(a.planes, bt.planes, a.cols)
+    fn = gemm_arbitrary_wide if wide else gemm_arbitrary
+    reference, records, best = None, [], 0
+    for ci, t in enumerate(candidates):
+        t.require_valid(a.planes, bt.planes)
+        got = [None]
+
+        def run():
+            got[0] = fn(a, bt, t)
+
+        us = _time_median_us(run, trials)
+        if ci == 0:
+            reference = got[0]
+        elif not torch.equal(got[0], reference):
+            raise Error(f"autotune: config {t.describe()} disagrees with the reference result")
+        rec = BenchRecord(t.describe(), t.BM, t.BN, t.BK, t.WM, t.WN, a.planes, bt.planes, a.rows, bt.rows,
+                          a.cols, us, tops_of(a.rows, bt.rows, a.cols, us))
+        if records and us < records[best].median_us:
+            best = len(records)
+        records.append(rec)
+    return AutotuneResult(candidates[best], records)
+
+
+GEMM_SCHEDULES = {"auto": 0, "classic": 1, "stream_k": 2}
+
+
+def set_gemm_schedule(schedule: str) -> None:
+    """Prefill GEMM schedule (abq_set_gemm_schedule): "auto", "classic" (one CTA
+    per 128-channel row tile) or "stream_k" (all SMs share (row-tile, k-block)
+    units).  Process-global; results do not depend on it."""
+    if schedule not in GEMM_SCHEDULES:
+        raise ValueError(f"set_gemm_schedule: unknown schedule {schedule!r}")
+    _check(L.lib().abq_set_gemm_schedule(GEMM_SCHEDULES[schedule]))
+
+
+def get_gemm_schedule() -> str:
+    v = L.lib().abq_get_gemm_schedule()
+    return {i: k for k, i in GEMM_SCHEDULES.items()}[v]
+
+
+def autotune_linear(lin: "Linear", x: torch.Tensor, trials: int = 5,
+                    out_dtype=torch.float16) -> AutotuneResult:
+    """The GPU counterpart of the reference's tile search for a resident layer:
+    time the engine's own schedules for this (M, N, K, p, q) -- the decode GEMV
+    variants for M <= 8 (fused tensor-pipe kernel / bit-serial AND+popcount),
+    the prefill GEMM schedules for M >= 9 (classic / stream-K) -- verify every
+    schedule's output bit for bit against the first, leave the fastest selected
+    (process-global, like abq_set_gemv_variant) and return the records
+    (config_id = schedule name, tile fields 0).  Each schedule is timed as the
+    serving path runs it: a CUDA graph of back-to-back calls."""
+    if trials < 3:
+        raise ValueError("autotune: need at least 3 trials")
+    m = x.shape[0]
+    old_v, old_s = L.lib().abq_get_gemv_variant(), L.lib().abq_get_gemm_schedule()
+    if m <= 8:
+        scheds = [("auto", lambda: (set_gemv_variant("auto"), set_gemm_schedule("auto"))),
+                  ("popc", lambda: set_gemv_variant("popc"))]
+    else:
+        scheds = [("classic", lambda: (set_gemv_variant("auto"), set_gemm_schedule("classic"))),
+                  ("stream_k", lambda: (set_gemv_variant("auto"), set_gemm_schedule("stream_k"))),
+                  ("popc", lambda: set_gemv_variant("popc"))]
+    out = torch.empty((m, lin.w.planes.rows), dtype=out_dtype, device=x.device)
+    reference, records, best = None, [], 0
+    try:
+        for name, select in scheds:
+            select()
+            us = _time_graph_us(lambda: lin(x, out=out, check=False), trials)
+            got = out.clone()
+            if reference is None:
+                reference = got
+            elif not torch.equal(got, reference):
+                raise Error(f"autotune: schedule {name} disagrees with the reference result")
+            rec = BenchRecord(name, 0, 0, 0, 0, 0, lin.spec.planes(), lin.w.planes.planes, m,
+                              lin.w.planes.rows, lin.k, us, tops_of(m, lin.w.planes.rows, lin.k, us))
+            if records and us < records[best].median_us:
+                best = len(records)
+            records.append(rec)
+    finally:
+        L.lib().abq_set_gemv_variant(old_v)
+        L.lib().abq_set_gemm_schedule(old_s)
+    # leave the winner selected
+    dict(scheds)[records[best].config_id]()
+    return AutotuneResult(records[best].config_id, records)
 
 
 def _gemm(fn, name, a: BitPlaneMatrix, bt: BitPlaneMatrix, tile, stats, dtype):

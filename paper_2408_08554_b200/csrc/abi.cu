@@ -105,6 +105,7 @@ int run_gemm_tc(const uint32_t* wtc, unsigned q, size_t n, size_t k, const uint8
                 unsigned long long* bad_out = nullptr, bool pdl = false, unsigned* sk_flags = nullptr,
                 uint32_t* sk_part = nullptr);
 size_t tc_sk_flag_bytes(size_t n);
+int& gemm_schedule();
 size_t tc_sk_part_bytes(size_t m, size_t n);
 int run_tile_codes(const uint8_t* src, size_t m, size_t k, uint8_t* dst, cudaStream_t st);
 int run_act_quant(const void* x, int x_dtype, size_t m, size_t k, int mt, const QuantParams& qp,
@@ -282,6 +283,14 @@ int abq_set_gemv_variant(int variant) {
   return ABQ_OK;
 }
 int abq_get_gemv_variant(void) { return g_gemv_variant; }
+
+int abq_set_gemm_schedule(int schedule) {
+  if (schedule < ABQ_GEMM_AUTO || schedule > ABQ_GEMM_STREAM_K)
+    return fail(ABQ_ERR_VALUE, "abq_set_gemm_schedule: unknown schedule %d", schedule);
+  gemm_schedule() = schedule;
+  return ABQ_OK;
+}
+int abq_get_gemm_schedule(void) { return gemm_schedule(); }
 
 int abq_set_trace_buffer(void* dev_words) {
   trace_buffer() = static_cast<unsigned long long*>(dev_words);

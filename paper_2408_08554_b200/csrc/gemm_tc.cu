@@ -46,8 +46,13 @@ constexpr int kTcK = 128;
 constexpr int kTcThreads = 512;  // warps 8-15 only join the epilogue
 constexpr int kTcColGroups = kTcThreads / 128;
 constexpr int kTcIssuers = 3;  // MMA-issuing threads (lane 0 of warps 1 .. kTcIssuers)
-// stream-K schedule by default (ABQ_TC_SK=0/1 overrides)
-constexpr bool kTcStreamKDefault = false;  // epilogue: token-column groups per TMEM lane quarter
+// ABQ_GEMM_AUTO picks stream-K when the one-CTA-per-row-tile grid leaves at
+// least half the SMs idle (2 x row-tiles <= SMs): measured with
+// abq.autotune_linear (profiles/r01_tune_sweep.csv), stream-K is 17-18 %
+// faster at N <= 4096 with K = 11008 or M = 256 and ties at K = 4096, while
+// at N = 11008 (86 row-tiles) the partial-tile hand-off costs more than the
+// 62 idle SMs.
+inline bool tc_stream_k_auto(int rowtiles) { return 2 * rowtiles <= num_sms(); }  // epilogue: token-column groups per TMEM lane quarter
 
 // ---------------------------------------------------------------------------
 // prepack: ABQP [q][n][wpr] -> tc code slices
@@ -358,6 +363,12 @@ struct TcParams {
 
 // stream-K workspace: flags (zero-filled once by the caller, at an offset that
 // does not depend on m) and partial tiles (no initial value needed)
+// abq_set_gemm_schedule (ABQ_GEMM_AUTO / CLASSIC / STREAM_K)
+int& gemm_schedule() {
+  static int s = 0;
+  return s;
+}
+
 size_t tc_sk_flag_bytes(size_t n) { return (n + kTcM - 1) / kTcM * 2 * 4; }
 size_t tc_sk_part_bytes(size_t m, size_t n) {
   if (m == 0 || m > 256) return 0;
@@ -873,7 +884,11 @@ int run_gemm_tc(const uint32_t* wtc, unsigned q, size_t n, size_t k, const uint8
   P.trace = trace_buffer();
   if (const char* env = std::getenv("ABQ_TC_DBG")) P.dbg = std::atoi(env);
   const char* sk_env = std::getenv("ABQ_TC_SK");
-  const bool sk_on = sk_env ? std::atoi(sk_env) != 0 : kTcStreamKDefault;
+  // an explicit schedule wins; else ABQ_TC_SK (experiments); else the default
+  const int sched = gemm_schedule();
+  const bool sk_on = sched == ABQ_GEMM_STREAM_K ? true
+                     : sched == ABQ_GEMM_CLASSIC ? false
+                     : (sk_env ? std::atoi(sk_env) != 0 : tc_stream_k_auto(P.rowtiles));
   if (sk_flags && sk_part && m <= 256 && sk_on) {
     P.sk = 1;
     P.sk_flags = sk_flags;
