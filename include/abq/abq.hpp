@@ -8,6 +8,8 @@
 //   quantizer.hpp:14-224      Scheme, Granularity, QuantSpec, CompensationPair,
 //                             QuantizedTensor, quantize, quantize_balanced
 //   bitplane.hpp:15-96        BitPlaneMatrix, bitpack, unpack, bmma
+//   tune.hpp:51-192           enumerate_tile_candidates, BenchRecord, AutotuneResult,
+//                             autotune (device engine timed with steady_clock, as the reference)
 //   gemm.hpp:19-307           TileConfig, default_tile, GemmStats, fits_int32,
 //                             engine_threads, gemm_arbitrary(_wide), gemm_naive,
 //                             zero_point_correct, code_rowsums, quantized_linear
@@ -21,7 +23,12 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <chrono>
+#include <iterator>
 #include <cstdint>
+#include <set>
+#include <tuple>
 #include <optional>
 #include <random>
 #include <sstream>
@@ -351,6 +358,125 @@ inline Matrix<std::int32_t> gemm_naive(const BitPlaneMatrix& a, const BitPlaneMa
                                bt.cols, dout.get(), nullptr));
   dout.to_host(out.data.data());
   return out;
+}
+
+// ---- tuning (tune.hpp:51-192) --------------------------------------------------
+namespace detail {
+/// padded rows summed over the BM-row blocks covering m rows (tune.hpp:35-44)
+inline std::size_t row_padding_total(std::size_t m, unsigned p, std::size_t bm, std::size_t mma_m) {
+  std::size_t total = 0;
+  for (std::size_t start = 0; start < m; start += bm) {
+    const std::size_t rows = p * std::min(bm, m - start);
+    total += (rows + mma_m - 1) / mma_m * mma_m - rows;
+  }
+  return total;
+}
+}  // namespace detail
+
+/// enumerate_tile_candidates  tune.hpp:51-92: warp layouts {1x1,1x2,1x4,2x2,2x4,4x4}
+/// x inner tiles {8..64}^2 x BK {128..512}; block tile = ceil(layout x inner / bits);
+/// valid + first occurrence only; then the block heights with the least row padding.
+inline std::vector<TileConfig> enumerate_tile_candidates(unsigned p, unsigned q, std::size_t m, std::size_t,
+                                                         std::size_t) {
+  if (p < 1 || p > 8 || q < 1 || q > 8) throw ValueError("enumerate_tile_candidates: p,q must be in [1,8]");
+  constexpr unsigned layouts[6][2] = {{1, 1}, {1, 2}, {1, 4}, {2, 2}, {2, 4}, {4, 4}};
+  constexpr std::size_t inner[4] = {8, 16, 32, 64}, depth[4] = {128, 256, 384, 512};
+  std::set<std::tuple<std::size_t, std::size_t, std::size_t, std::size_t, std::size_t>> seen;
+  std::vector<TileConfig> all;
+  for (const auto& l : layouts)
+    for (std::size_t wm : inner)
+      for (std::size_t wn : inner)
+        for (std::size_t bk : depth) {
+          TileConfig t{(l[0] * wm + p - 1) / p, (l[1] * wn + q - 1) / q, bk, wm, wn, TileConfig::mma_k};
+          if (t.valid(p, q) && seen.emplace(t.BM, t.BN, t.BK, t.WM, t.WN).second) all.push_back(t);
+        }
+  std::size_t least = ~std::size_t(0);
+  for (const auto& t : all) least = std::min(least, detail::row_padding_total(m, p, t.BM, TileConfig::mma_m));
+  std::vector<TileConfig> out;
+  std::copy_if(all.begin(), all.end(), std::back_inserter(out), [&](const TileConfig& t) {
+    return detail::row_padding_total(m, p, t.BM, TileConfig::mma_m) == least;
+  });
+  if (out.empty()) out.push_back(default_tile(p, q));
+  return out;
+}
+
+/// BenchRecord  tune.hpp:94-105
+struct BenchRecord {
+  std::string config_id;
+  std::size_t BM = 0, BN = 0, BK = 0, WM = 0, WN = 0;
+  unsigned p = 0, q = 0;
+  std::size_t M = 0, N = 0, K = 0;
+  double median_us = 0.0;
+  double tops = 0.0;
+  static std::string csv_header() { return "config_id,BM,BN,BK,WM,WN,p,q,M,N,K,median_us,tops"; }
+};
+
+namespace detail {
+/// tops_of  tune.hpp:129-131
+inline double tops_of(std::size_t m, std::size_t n, std::size_t k, double us) {
+  return 2.0 * double(m) * double(n) * double(k) / (us * 1e6);
+}
+/// time_median_us  tune.hpp:114-127 (one discarded warm-up, steady_clock
+/// around each synchronous call, median)
+template <typename Fn>
+inline double time_median_us(Fn&& fn, unsigned trials) {
+  fn();
+  std::vector<double> us;
+  for (unsigned i = 0; i < trials; ++i) {
+    const auto t0 = std::chrono::steady_clock::now();
+    fn();
+    us.push_back(std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count());
+  }
+  std::sort(us.begin(), us.end());
+  const std::size_t h = us.size() / 2;
+  return us.size() % 2 ? us[h] : 0.5 * (us[h - 1] + us[h]);
+}
+}  // namespace detail
+
+struct AutotuneResult {
+  TileConfig best;
+  std::vector<BenchRecord> records;
+};
+
+/// autotune  tune.hpp:141-192: every candidate is timed through the engine's
+/// gemm_arbitrary (_wide past the int32 bound) and must reproduce the first
+/// candidate's result exactly (else abq::Error); the fastest wins.
+inline AutotuneResult autotune(const std::vector<TileConfig>& candidates, const BitPlaneMatrix& a,
+                               const BitPlaneMatrix& bt, unsigned trials = 3) {
+  if (candidates.empty()) throw ValueError("autotune: no candidates");
+  if (trials < 3) throw ValueError("autotune: need at least 3 trials");
+  const bool wide = !fits_int32(a.planes, bt.planes, a.cols);
+  AutotuneResult res;
+  Matrix<std::int64_t> first;
+  std::size_t best = 0;
+  for (std::size_t i = 0; i < candidates.size(); ++i) {
+    const TileConfig& t = candidates[i];
+    t.require_valid(a.planes, bt.planes);
+    Matrix<std::int64_t> got;
+    const double us = detail::time_median_us(
+        [&] {
+          if (wide) {
+            got = gemm_arbitrary_wide(a, bt, t);
+          } else {
+            const Matrix<std::int32_t> r = gemm_arbitrary(a, bt, t);
+            got = Matrix<std::int64_t>(r.rows, r.cols);
+            std::copy(r.data.begin(), r.data.end(), got.data.begin());
+          }
+        },
+        trials);
+    if (i == 0) first = got;
+    else if (!(got == first)) throw Error("autotune: config " + t.describe() + " disagrees with the reference result");
+    BenchRecord r;
+    r.config_id = t.describe();
+    r.BM = t.BM, r.BN = t.BN, r.BK = t.BK, r.WM = t.WM, r.WN = t.WN;
+    r.p = a.planes, r.q = bt.planes, r.M = a.rows, r.N = bt.rows, r.K = a.cols;
+    r.median_us = us;
+    r.tops = detail::tops_of(r.M, r.N, r.K, us);
+    if (!res.records.empty() && us < res.records[best].median_us) best = res.records.size();
+    res.records.push_back(r);
+  }
+  res.best = candidates[best];
+  return res;
 }
 
 template <typename Acc>

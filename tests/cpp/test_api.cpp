@@ -6,7 +6,7 @@
 // same independent in-test oracles (plain int64 loops), so a user switching
 // their #include to this engine sees the same contract hold:
 //   test_bitkernel.cpp:36-180, acceptance.cpp:29-104, test_quantizer.cpp:94-128,
-//   test_tune.cpp:10-23.
+//   test_tune.cpp:10-70.
 // Prints one PASS/FAIL line per case; exit status = number of failures.
 #include <cstdio>
 #include <set>
@@ -246,6 +246,51 @@ static void case_quantizer_and_padding() {
   report(ok, "balanced 2-bit level set, degenerate range, padding figures");
 }
 
+static void case_tune() {
+  // test_tune.cpp:25-70 + the reference's own candidate list for (p=4, q=4, M=1)
+  // (tests/golden/tune/candidates.json, written by the unmodified
+  // enumerate_tile_candidates): 384 candidates, first/last as below
+  bool ok = true;
+  const auto c = enumerate_tile_candidates(4, 4, 1, 4096, 4096);
+  CHECK(c.size() == 384);
+  CHECK(c.front().BM == 2 && c.front().BN == 2 && c.front().BK == 128 && c.front().WM == 8 && c.front().WN == 8);
+  CHECK(c.back().BM == 64 && c.back().BN == 64 && c.back().BK == 512 && c.back().WM == 64 && c.back().WN == 64);
+  std::set<std::string> ids;
+  for (const auto& t : c) {
+    CHECK(t.valid(4, 4));
+    ids.insert(t.describe());
+  }
+  CHECK(ids.size() == c.size());
+  bool threw = false;
+  try {
+    enumerate_tile_candidates(0, 4, 1, 64, 64);
+  } catch (const ValueError&) {
+    threw = true;
+  }
+  CHECK(threw);
+  threw = false;
+  try {
+    autotune({}, BitPlaneMatrix(), BitPlaneMatrix());
+  } catch (const ValueError&) {
+    threw = true;
+  }
+  CHECK(threw);
+  Rng rng(11);
+  const CodeMat a = rng.code_matrix(24, 200, 3), b = rng.code_matrix(30, 200, 5);
+  const auto pa = bitpack(a, 3), pb = bitpack(b, 5);
+  const auto cands = enumerate_tile_candidates(3, 5, 24, 30, 200);
+  const std::vector<TileConfig> tried(cands.begin(), cands.begin() + std::min<std::size_t>(4, cands.size()));
+  const AutotuneResult r = autotune(tried, pa, pb, 3);
+  CHECK(r.records.size() == tried.size());
+  for (const auto& rec : r.records) CHECK(rec.median_us > 0.0 && rec.tops > 0.0 && rec.M == 24 && rec.N == 30);
+  const auto got = gemm_arbitrary(pa, pb, r.best);
+  const IntMat want = naive_codes(a, b);
+  for (std::size_t i = 0; i < 24; ++i)
+    for (std::size_t j = 0; j < 30; ++j) CHECK(std::int64_t(got(i, j)) == want(i, j));
+  CHECK(BenchRecord::csv_header() == "config_id,BM,BN,BK,WM,WN,p,q,M,N,K,median_us,tops");
+  report(ok, "tune: reference candidate list, validity, errors, verified autotune");
+}
+
 int main() {
   case_bitpack();
   case_bmma();
@@ -255,6 +300,7 @@ int main() {
   case_quantized_linear_and_stats();
   case_acceptance_1000();
   case_quantizer_and_padding();
+  case_tune();
   std::printf("%d failure(s)\n", failures);
   return failures;
 }
