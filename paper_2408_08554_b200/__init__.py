@@ -12,3 +12,4 @@ from .api import (BitPlaneMatrix, Error, GemmStats, IoError, Linear, OverflowErr
                   bitpack, bmma, code_rowsums, default_tile, dequantize, fits_int32, gemm_arbitrary, gemm_btc,
                   gemm_arbitrary_wide, gemm_naive, linear_planes, padding_redundancy, plane_rowsums,
                   quantize, quantize_balanced, quantized_linear, unpack, zero_point_correct)
+from . import io, model  # noqa: F401,E402  (weight files; toy block)
