@@ -370,8 +370,11 @@ int& gemm_schedule() {
 }
 
 size_t tc_sk_flag_bytes(size_t n) { return (n + kTcM - 1) / kTcM * 2 * 4; }
+// stream-K only runs with fewer row-tiles than SMs; layers wider than this
+// never need partial tiles (keeps the per-layer workspace small)
+constexpr size_t kSkMaxRowtiles = 160;
 size_t tc_sk_part_bytes(size_t m, size_t n) {
-  if (m == 0 || m > 256) return 0;
+  if (m == 0 || m > 256 || (n + kTcM - 1) / kTcM > kSkMaxRowtiles) return 0;
   const size_t tt = m <= 16 ? 16 : m <= 32 ? 32 : m <= 64 ? 64 : m <= 128 ? 128 : 256;
   return (n + kTcM - 1) / kTcM * 2 * tt * kTcM * 4;
 }
@@ -829,7 +832,8 @@ static int launch_tc(const TcParams& P, bool pdl, cudaStream_t st) {
   // CTAs share the (row-tile, k-block) units; G <= 2 rowtiles keeps every
   // range >= kblocks / 2 (<= 2 contributors per tile), G > rowtiles keeps it
   // <= kblocks (<= 2 segments per CTA)
-  if (L.sk && gy == 1 && P.kblocks >= 2 && P.rowtiles < num_sms()) {
+  if (L.sk && gy == 1 && P.kblocks >= 2 && P.rowtiles < num_sms() &&
+      static_cast<size_t>(P.rowtiles) <= kSkMaxRowtiles) {
     gx = std::min(num_sms(), 2 * P.rowtiles);
   } else {
     L.sk = 0;
