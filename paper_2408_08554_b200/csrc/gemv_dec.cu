@@ -57,6 +57,7 @@ struct DecParams {
   unsigned long long* trace;     // optional [grid][64] stamps (tools/trace_dec.py)
   int prefetch;                  // L2 bulk prefetch of the CTA's weights (default 1)
   int slots;                     // TMA ring slots of kDecUPS units
+  int preslots;                  // ring slots issued before the activations are awaited
   const unsigned char* next_frag;  // L2 prefetch hint: the next layer's weights (or null)
   size_t next_bytes;
 };
@@ -173,10 +174,13 @@ __global__ void __launch_bounds__(kDecThreads, 1) gemv_dec_kernel(const __grid_c
     __syncwarp();
     if (lane == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncwarp();
-    for (int i = lane; i < S && i < nsl; i += 32) issue_slot(i, i);
+    for (int i = lane; i < min(S, Pc.preslots) && i < nsl; i += 32) issue_slot(i, i);
   } else if (warp == 1 && Pc.prefetch) {
+    // (the ring slots issued after the activation load are prefetched too, so
+    // their copies hit L2)
     const size_t total = static_cast<size_t>(U1 - U0) * unit_bytes;
-    for (size_t off = static_cast<size_t>(S) * slot_bytes + static_cast<size_t>(lane) * 32768; off < total;
+    for (size_t off = static_cast<size_t>(min(S, Pc.preslots)) * slot_bytes + static_cast<size_t>(lane) * 32768;
+         off < total;
          off += 32u * 32768)
       l2_prefetch_bulk(wsrc + off, static_cast<uint32_t>(total - off < 32768 ? total - off : 32768), pol);
     // the next layer's weights (input-independent) stream into L2 behind ours
@@ -266,6 +270,10 @@ __global__ void __launch_bounds__(kDecThreads, 1) gemv_dec_kernel(const __grid_c
       const int v = l + r * TPT;
       xv[r] = active && v < nvec ? __ldg(xr + v) : make_uint4(0u, 0u, 0u, 0u);
     }
+    // the rest of the ring only now: shared-memory-bound TMA traffic into this
+    // SM ahead of the activation loads delayed them (~0.2 us on the critical path)
+    if (warp == 0)
+      for (int i = P.preslots + lane; i < P.slots && i < nsl; i += 32) issue_slot(i, i);
     // min / max in the order-preserving integer image of fp32 (exact for fp16
     // inputs): one REDUX per warp instead of a shuffle tree
     auto ord = [](float f) {
@@ -340,7 +348,8 @@ __global__ void __launch_bounds__(kDecThreads, 1) gemv_dec_kernel(const __grid_c
       *P.bad_out = w ? ~w : ~0ull;
     }
   } else {
-    // codes + stats from act_quant_kernel
+    // codes + stats from act_quant_kernel (the host issues the whole ring up
+    // front on this path: preslots == slots)
     const uint4* src = reinterpret_cast<const uint4*>(P.act_frag);
     uint4* dst = reinterpret_cast<uint4*>(act);
     const int nv = MT * kpad / 16;  // act_quant_kernel zero-fills codes past K
@@ -738,6 +747,11 @@ int run_gemv_dec(const uint32_t* frag, unsigned q, size_t n, size_t k, size_t m,
   const size_t budget = 212 * 1024;
   while (slots > min_slots && dec_smem(q, slots, mt, kpad, nl).total > budget) --slots;
   P.slots = slots;
+  // slots in flight before the activations are awaited: ~64 KB (the rest is
+  // L2-prefetched and copied once the activation loads are issued)
+  int pre_kb = 64;
+  if (const char* env = std::getenv("ABQ_DEC_PRE_KB")) pre_kb = std::atoi(env);
+  P.preslots = fused ? std::max(1, std::min(slots, static_cast<int>(pre_kb * 1024 / slot_bytes))) : slots;
   const size_t smem = dec_smem(q, slots, mt, kpad, nl).total;
   bool pdl = true;
   if (const char* env = std::getenv("ABQ_DEC_PDL")) pdl = env[0] == '1';
