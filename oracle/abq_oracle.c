@@ -106,7 +106,7 @@ int orc_quantize(const double* x, size_t rows, size_t cols, unsigned bits, int s
       if (bad) *bad = (int64_t)i;
       return ORC_VALUE;
     }
-  v = (double*)malloc(sizeof(double) * (rows * cols ? rows * cols : 1));
+  v = (double*)malloc(sizeof(double) * (rows * cols != 0 ? rows * cols : 1));
   memcpy(v, x, sizeof(double) * rows * cols);
   if (comp_a && comp_b)
     for (i = 0; i < rows; ++i)
@@ -264,7 +264,7 @@ int orc_gemm_arbitrary_i32(const uint64_t* a, unsigned p, size_t m, const uint64
   size_t i;
   int64_t* tmp;
   if (!orc_fits_int32(p, q, k)) return ORC_OVERFLOW;
-  tmp = (int64_t*)malloc(sizeof(int64_t) * (m * n ? m * n : 1));
+  tmp = (int64_t*)malloc(sizeof(int64_t) * (m * n != 0 ? m * n : 1));
   orc_gemm_planes(a, p, m, bt, q, n, k, tmp);
   for (i = 0; i < m * n; ++i) out[i] = (int32_t)tmp[i];
   free(tmp);
