@@ -31,17 +31,25 @@ METRICS = [
 def raw_rows(path):
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    return rows[0], rows[2:]
+    return rows[0], rows[2:], rows[1]
+
+
+_BYTE_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
+
+
+def to_bytes(value, unit):
+    """ncu picks a unit per metric per report (row 2 of the raw CSV); normalise to bytes."""
+    return float(value.replace(",", "")) * _BYTE_SCALE[unit.strip()]
 
 
 def summary(path):
-    h, rows = raw_rows(path)
+    h, rows, units = raw_rows(path)
     for r in rows:
         name = r[h.index("Kernel Name")] if "Kernel Name" in h else "?"
         print(f"kernel: {name}")
         for m in METRICS:
             if m in h:
-                print(f"  {m:70s} {r[h.index(m)]}")
+                print(f"  {m:70s} {r[h.index(m)]} {units[h.index(m)]}")
         stalls = [(c, r[i]) for i, c in enumerate(h) if "pcsamp_warps_issue_stalled" in c and not c.endswith("not_issued")]
         stalls = sorted(stalls, key=lambda x: -float(x[1] or 0))[:6]
         if stalls:
@@ -64,11 +72,11 @@ def launches(path):
 
 
 def traffic(path, key, json_path):
-    h, rows = raw_rows(path)
+    h, rows, units = raw_rows(path)
     r = rows[0]
-    b = float(r[h.index("dram__bytes_read.sum")]) + float(r[h.index("dram__bytes_write.sum")])
-    unit = "MB"  # ncu reports these in the unit printed in row 1; convert MB -> bytes
-    rec = {"dram_bytes_per_launch": int(b * 1e6), "source": path, "unit_assumed": unit}
+    b = sum(to_bytes(r[h.index(m)], units[h.index(m)]) for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+    rec = {"dram_bytes_per_launch": int(b), "source": path,
+           "units": [units[h.index(m)] for m in ("dram__bytes_read.sum", "dram__bytes_write.sum")]}
     data = {}
     if json_path:
         try:
