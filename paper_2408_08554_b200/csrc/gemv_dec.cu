@@ -55,7 +55,7 @@ struct DecParams {
   unsigned long long* bad_word;  // non-finite input report (see run_gemv_dec)
   unsigned long long* bad_out;
   unsigned long long* trace;     // optional [grid][64] stamps (tools/trace_dec.py)
-  int prefetch;                  // L2 bulk prefetch of the CTA's weights (default 1)
+  int prefetch;                  // L2 bulk prefetch of the CTA's weights (default 0)
   int slots;                     // TMA ring slots of kDecUPS units
   int preslots;                  // ring slots issued before the activations are awaited
   const unsigned char* next_frag;  // L2 prefetch hint: the next layer's weights (or null)
@@ -703,7 +703,11 @@ int run_gemv_dec(const uint32_t* frag, unsigned q, size_t n, size_t k, size_t m,
   P.e = e;
   P.qp = qp;
   P.trace = trace_buffer();
-  P.prefetch = 1;
+  // L2 bulk prefetch of the CTA's range beyond the pre-issued ring slots and of
+  // the successor layer: off by default -- measured slower on every decode
+  // shape (profiles/r01_dec_prefetch_sweep.txt: W4A4 M=1 7.56 -> 7.32 us, W8A8
+  // M=1 10.0 -> 8.4 us, W4A4 M=8 11.3 -> 9.9 us); ABQ_DEC_PREFETCH=1 restores it.
+  P.prefetch = 0;
   P.next_frag = static_cast<const unsigned char*>(next_frag);
   P.next_bytes = next_frag ? next_bytes : 0;
   if (const char* env = std::getenv("ABQ_DEC_PREFETCH")) P.prefetch = env[0] == '1';
