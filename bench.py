@@ -4,18 +4,27 @@
 One step = one pass of the hot path over one batch:
     fp16 activations (resident in HBM)
       -> K1 ReQuant + BitPacking (per-token asymmetric, FP64, round-half-away)
-      -> K2 plane GEMV: sum_{s,t} 2^(s+t) popc(A_s & W_t) over the packed weights
+      -> K2/K3 exact code product sum_{s,t} 2^(s+t) popc(A_s & W_t) over the packed weights
       -> K4 fused zero-point correction + dequant -> fp16 output
-on the BASELINE.json configs[1] workload (LLaMA-7B up_proj, K=4096 N=11008,
-W4A4, M=1 decode).  value = packed weight bytes / step time (GB/s, the
-metric's HBM GB/s on packed weight bytes), whole job over all ranks.
+The default workload is BASELINE.json configs[1] (LLaMA-7B up_proj, K=4096
+N=11008, W4A4, M=1 decode); value = packed weight bytes / step time (GB/s, the
+metric's "HBM GB/s on packed weight bytes"), whole job over all ranks.  The
+other two parts of the metric -- W2A8 M=1 GEMV at LLaMA-7B shapes and the
+M=128 GEMM in TOPS against a cuBLAS fp16 GEMM of the same shape -- are
+measured in the same run and reported under "parts" (N=1).
 
-    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--workload NAME] [--sweep]
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--workload NAME]
+
+--gpus N without a torchrun environment re-launches itself under
+torch.distributed.run with N ranks (one per GPU).  Single-linear workloads
+scale weakly (each rank owns N output channels of a world x N layer); the
+cfg4 / cfg5 layer workloads scale strongly (one fixed LLaMA layer, its 7
+linears column-sharded over the ranks, plus the NCCL all-gather leg).
 
 L2 hygiene: each step reads a different copy of the packed weights, rotating
-over enough copies to exceed 4x the L2 size, so every step streams its
-weights from HBM.  Steps are replayed from a CUDA graph (launch overhead is
-not part of a serving step), timed with CUDA events on the launching stream,
+over copies totalling > 4x the L2 size, so every step streams its weights
+from HBM.  Steps are replayed from CUDA graphs (every graph replayed during
+warm-up before it is timed), timed with CUDA events on the launching stream,
 max over ranks.
 """
 from __future__ import annotations
@@ -24,6 +33,7 @@ import argparse
 import json
 import math
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -36,20 +46,52 @@ sys.path.insert(0, ROOT)
 
 METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
 
-# name -> (m, n, k, w_bits, a_bits, description)
+# single-linear workloads: name -> (m, n, k, w_bits, a_bits, description)
 WORKLOADS = {
     "cfg2_w4a4_m1": (1, 11008, 4096, 4, 4, "cfg2 W4A4 GEMV M=1 K=4096 N=11008 (LLaMA-7B up_proj)"),
     "cfg2_w8a8_m1": (1, 11008, 4096, 8, 8, "cfg2 W8A8 GEMV M=1 K=4096 N=11008 (LLaMA-7B up_proj)"),
     "cfg1_w2a8": (1, 4096, 4096, 2, 8, "cfg1 W2A8 GEMV M=1 K=N=4096 (LLaMA-7B q_proj)"),
+    "w2a8_m1_gate_up": (1, 11008, 4096, 2, 8, "W2A8 GEMV M=1 K=4096 N=11008 (LLaMA-7B gate/up_proj)"),
+    "w2a8_m1_down": (1, 4096, 11008, 2, 8, "W2A8 GEMV M=1 K=11008 N=4096 (LLaMA-7B down_proj)"),
 }
 for _m in (4, 8, 16, 128):
     for _w in (4, 8):
         WORKLOADS[f"cfg2_w{_w}a{_w}_m{_m}"] = (
             _m, 11008, 4096, _w, _w, f"cfg2 W{_w}A{_w} M={_m} K=4096 N=11008 (LLaMA-7B up_proj)")
 
+# layer workloads (strong scaling): name -> (m, w_bits, a_bits, [(proj, n, k)], unit, description)
+LAYERS = {
+    "cfg4_w2a8_13b_decode": (
+        1, 2, 8, [("q", 5120, 5120), ("k", 5120, 5120), ("v", 5120, 5120), ("o", 5120, 5120),
+                  ("gate", 13824, 5120), ("up", 13824, 5120), ("down", 5120, 13824)], "GB/s",
+        "cfg4 LLaMA-13B W2A8 decode layer (q,k,v,o,gate,up,down), M=1, N-sharded over the ranks"),
+    "cfg5_w4a4_70b_prefill": (
+        2048, 4, 4, [("q", 8192, 8192), ("k", 1024, 8192), ("v", 1024, 8192), ("o", 8192, 8192),
+                     ("gate", 28672, 8192), ("up", 28672, 8192), ("down", 8192, 28672)], "TOPS",
+        "cfg5 LLaMA-70B W4A4 prefill layer (q,k,v,o,gate,up,down), M=2048, N-sharded over the ranks"),
+}
+
+# the parts of the headline metric measured beside the headline (N=1)
+PARTS = ["cfg1_w2a8", "w2a8_m1_gate_up", "w2a8_m1_down", "cfg2_w8a8_m1", "cfg2_w4a4_m128", "cfg2_w8a8_m128"]
+
 
 def packed_bytes(n, k, w_bits):
     return w_bits * n * ((k + 63) // 64) * 8
+
+
+def config_of(workload: str, world: int) -> dict:
+    """The workload's config dict -- identical in both arms."""
+    if workload in LAYERS:
+        m, wb, ab, projs, unit, desc = LAYERS[workload]
+        return {"workload": desc, "m": m, "w_bits": wb, "a_bits": ab,
+                "linears": [f"{p} N={n} K={k}" for p, n, k in projs],
+                "parallelism": f"column-parallel x{world} (N-sharded, NCCL all-gather leg reported)" if world > 1
+                else "single", "l2": "rotating packed-weight copies (> 4x L2 per rotation)"}
+    m, n, k, wb, ab, desc = WORKLOADS[workload]
+    return {"workload": desc, "m": m, "n": n * world, "k": k, "w_bits": wb, "a_bits": ab,
+            "parallelism": f"column-parallel x{world} (N-sharded, weak: {n} channels per rank)" if world > 1
+            else "single", "l2": "rotating packed-weight copies (> 4x L2 per rotation)",
+            "step": "fp16 x -> ReQuant+BitPack -> plane GEMV/GEMM -> zero-point+dequant -> fp16 y"}
 
 
 # ---------------------------------------------------------------------------
@@ -113,8 +155,9 @@ def measured_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
         d = json.load(open(path))
-        return d.get("hbm_gbs", 6650.0), "measured", d
-    return 6650.0, "fallback", {}
+        return d, "measured (MEASURED_PEAKS.json)"
+    # fallback figures of /opt/skills/guides/B200_PROFILING.md (an earlier measurement on this pool)
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1590.0}, "of fallback"
 
 
 def ncu_traffic(kernel_key: str):
@@ -122,12 +165,11 @@ def ncu_traffic(kernel_key: str):
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(path):
         return None
-    d = json.load(open(path))
-    v = d.get(kernel_key)
+    v = json.load(open(path)).get(kernel_key)
     return None if v is None else v.get("dram_bytes_per_launch")
 
 
-def dist_setup(args):
+def dist_setup():
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -157,91 +199,11 @@ def barrier(world):
         dist.barrier()
 
 
-# ---------------------------------------------------------------------------
-# reference arm: the reference's CPU implementation on the host cores
-# ---------------------------------------------------------------------------
-def run_reference(args, world, rank):
-    if rank != 0:
-        return
-    from oracle.oracle import RefOracle
-    m, n, k, wb, ab, desc = WORKLOADS[args.workload]
-    rng = np.random.default_rng(42)
-    x = rng.standard_normal((m, k)).astype(np.float16).astype(np.float64)
-    wc = rng.integers(0, 1 << wb, (n, k), dtype=np.uint8)
-    sb = rng.uniform(1e-3, 1e-2, n)
-    zb = rng.integers(0, 1 << wb, n).astype(np.int32)
-    cores = os.cpu_count() or 1
-    kind = "reference" if RefOracle.available() else None
-    if kind is None:
-        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
-        return
-    ref = RefOracle()
-    run = ref.linear(wc, wb, sb, zb, threads=cores)
-    out = np.zeros((m, n))
-    for _ in range(max(1, args.warmup)):
-        run(x, ab, out)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        run(x, ab, out)
-    dt = (time.perf_counter() - t0) / args.steps
-    gbs = packed_bytes(n, k, wb) / dt / 1e9
-    print(json.dumps({
-        "impl": "reference", "metric": METRIC, "value": round(gbs, 3), "unit": "GB/s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
-        "data": "synthetic",
-        "config": {"workload": desc, "m": m, "n": n, "k": k, "w_bits": wb, "a_bits": ab},
-        "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": cores, "kind": kind,
-                         "sample": f"full workload per step: reference quantize+bitpack+code_rowsums+"
-                                   f"gemm_arbitrary(default_tile)+zero_point_correct+dequant, weights "
-                                   f"pre-packed, output channels split over {cores} threads"},
-        "e2e": {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }))
-
-
-def cpu_baseline_sample(m, n, k, wb, ab, budget_s=8.0):
-    """The reference step timed on 1 host thread (the reference's own thread
-    count at M<=64, gemm.hpp:88-92) over a bounded sample of the workload."""
-    from oracle.oracle import RefOracle
-    rng = np.random.default_rng(42)
-    x = rng.standard_normal((m, k)).astype(np.float16).astype(np.float64)
-    wc = rng.integers(0, 1 << wb, (n, k), dtype=np.uint8)
-    sb = rng.uniform(1e-3, 1e-2, n)
-    zb = rng.integers(0, 1 << wb, n).astype(np.int32)
-    if not RefOracle.available():
-        return None
-    run = RefOracle().linear(wc, wb, sb, zb, threads=1)
-    out = np.zeros((m, n))
-    run(x, ab, out)
-    reps, t0 = 0, time.perf_counter()
-    while time.perf_counter() - t0 < budget_s:
-        run(x, ab, out)
-        reps += 1
-    dt = (time.perf_counter() - t0) / reps
-    return {"value": round(packed_bytes(n, k, wb) / dt / 1e9, 4), "unit": "GB/s", "cores": 1,
-            "kind": "reference",
-            "sample": f"{reps} full-workload reference steps ({dt * 1e3:.2f} ms each) in {budget_s:.0f} s: "
-                      "quantize+bitpack+gemm_arbitrary(default_tile)+zero_point_correct+dequant, "
-                      "weights pre-packed, 1 thread (reference uses ceil(M/64) threads)"}
-
-
-# ---------------------------------------------------------------------------
-# our arm
-# ---------------------------------------------------------------------------
-def build_layer(abq, torch, m, n, k, wb, ab, copies, seed=42):
-    rng = np.random.default_rng(seed)
-    x = rng.standard_normal((m, k)).astype(np.float16)
-    wc = rng.integers(0, 1 << wb, (n, k), dtype=np.uint8)
-    sb = rng.uniform(1e-3, 1e-2, n)
-    zb = rng.integers(0, 1 << wb, n).astype(np.int32)
-    base = abq.PackedWeights.from_planes(abq.bitpack(wc, wb), sb, zb)
-    ws = [base] + [base.copy() for _ in range(copies - 1)]
-    return x, wc, sb, zb, ws
-
-
 def time_graph(torch, body, copies, steps, warmup, world):
-    """Capture `copies` steps (one per weight copy) in a CUDA graph and replay
-    until exactly `steps` steps ran; returns total device ms (max over ranks)."""
+    """Capture `copies` steps (one per weight copy) in a CUDA graph, plus a
+    graph of the steps % copies remainder; replay both during warm-up (so the
+    timed replays are never a graph's first), then time exactly `steps` steps.
+    Returns total device ms (max over ranks) and the wall-clock window."""
     s = torch.cuda.Stream()
     s.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(s):
@@ -261,6 +223,9 @@ def time_graph(torch, body, copies, steps, warmup, world):
                 body(i)
     for _ in range(max(1, -(-warmup // copies))):
         g_full.replay()
+    if g_rem is not None:
+        g_rem.replay()
+        g_full.replay()
     torch.cuda.synchronize()
     barrier(world)
     torch.cuda.synchronize()
@@ -279,144 +244,349 @@ def time_graph(torch, body, copies, steps, warmup, world):
     return ms, (t_wall0, t_wall1)
 
 
+def synth_layer(rng, n, k, wb):
+    wc = rng.integers(0, 1 << wb, (n, k), dtype=np.uint8)
+    sb = rng.uniform(1e-3, 1e-2, n)
+    zb = rng.integers(0, 1 << wb, n).astype(np.int32)
+    return wc, sb, zb
+
+
+def rotation_copies(l2_bytes, bytes_per_copy, cap=256):
+    return int(min(cap, max(2, math.ceil(4 * l2_bytes / bytes_per_copy))))
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the reference's CPU implementation on the host cores
+# ---------------------------------------------------------------------------
+def reference_step_fn(m, n, k, wb, ab, threads, seed=42, n_sample=None):
+    """The reference's own step (oracle/_ref: unmodified headers) with
+    pre-packed weights: quantize + bitpack + code_rowsums +
+    gemm_arbitrary(default_tile) + zero_point_correct + dequant.  With
+    n_sample, only that many output channels are computed (the work is linear
+    in N; the caller scales the time)."""
+    from oracle.oracle import RefOracle
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal((m, k)).astype(np.float16).astype(np.float64)
+    ns = n if n_sample is None else min(n, n_sample)
+    wc, sb, zb = synth_layer(rng, ns, k, wb)
+    run = RefOracle().linear(wc, wb, sb, zb, threads=threads)
+    out = np.zeros((m, ns))
+    return lambda: run(x, ab, out), ns
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    from oracle.oracle import RefOracle
+    if not RefOracle.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref (reference headers) not built"}))
+        return
+    cores = os.cpu_count() or 1
+    if args.workload in LAYERS:
+        m, wb, ab, projs, unit, desc = LAYERS[args.workload]
+        # bounded sample: a fixed slice of each linear's output channels, time scaled to the full N
+        budget = 256 if m == 1 else 8 * cores
+        fns = []
+        for i, (p, n, k) in enumerate(projs):
+            f, ns = reference_step_fn(m, n, k, wb, ab, cores, seed=42 + i, n_sample=budget)
+            fns.append((f, n / ns))
+        for _ in range(max(1, args.warmup)):
+            for f, _s in fns:
+                f()
+        per_step = 0.0
+        for f, scale in fns:
+            t0 = time.perf_counter()
+            for _ in range(args.steps):
+                f()
+            per_step += (time.perf_counter() - t0) / args.steps * scale
+        dt = per_step
+        work = sum(packed_bytes(n, k, wb) for _, n, k in projs) if unit == "GB/s" else \
+            sum(2 * m * n * k for _, n, k in projs)
+        value = work / dt / 1e9 if unit == "GB/s" else work / dt / 1e12
+        sample = (f"{budget} output channels of each of the 7 linears per step, time scaled by N/{budget}: "
+                  f"reference quantize+bitpack+gemm_arbitrary(default_tile)+zero_point_correct+dequant, "
+                  f"weights pre-packed, {cores} threads")
+    else:
+        m, n, k, wb, ab, desc = WORKLOADS[args.workload]
+        unit = "GB/s" if m < 16 else "TOPS"
+        f, _ = reference_step_fn(m, n, k, wb, ab, cores)
+        for _ in range(max(1, args.warmup)):
+            f()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            f()
+        dt = (time.perf_counter() - t0) / args.steps
+        value = packed_bytes(n, k, wb) / dt / 1e9 if unit == "GB/s" else 2 * m * n * k / dt / 1e12
+        sample = (f"full workload per step: reference quantize+bitpack+code_rowsums+gemm_arbitrary(default_tile)"
+                  f"+zero_point_correct+dequant, weights pre-packed, output channels split over {cores} threads")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": unit,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
+        "higher_is_better": True, "scaling": "strong" if args.workload in LAYERS else "weak",
+        "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": config_of(args.workload, world),
+        "cpu_baseline": {"value": round(value, 4), "unit": unit, "cores": cores, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": round(value, 4), "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def cpu_baseline_sample(m, n, k, wb, ab, budget_s=8.0):
+    """The reference step on 1 host thread (the reference's own thread count at
+    M <= 64, gemm.hpp:88-92) over a bounded sample of the workload."""
+    from oracle.oracle import RefOracle
+    if not RefOracle.available():
+        return None
+    f, _ = reference_step_fn(m, n, k, wb, ab, 1)
+    f()
+    reps, t0 = 0, time.perf_counter()
+    while time.perf_counter() - t0 < budget_s:
+        f()
+        reps += 1
+    dt = (time.perf_counter() - t0) / reps
+    return {"value": round(packed_bytes(n, k, wb) / dt / 1e9, 4), "unit": "GB/s", "cores": 1,
+            "kind": "reference",
+            "sample": f"{reps} full-workload reference steps ({dt * 1e3:.2f} ms each) in {budget_s:.0f} s: "
+                      "quantize+bitpack+gemm_arbitrary(default_tile)+zero_point_correct+dequant, "
+                      "weights pre-packed, 1 thread (reference uses ceil(M/64) threads)"}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def build_linears(abq, torch, rng, m, n, k, wb, ab, copies):
+    wc, sb, zb = synth_layer(rng, n, k, wb)
+    base = abq.PackedWeights.from_planes(abq.bitpack(wc, wb), sb, zb)
+    spec = abq.QuantSpec(bits=ab, granularity=abq.api.PER_TOKEN)
+    ws = [base] + [base.copy() for _ in range(copies - 1)]
+    return wc, sb, zb, [abq.Linear(w, spec, max_m=m) for w in ws]
+
+
+def roofline_for(m, n, k, wb, step_us, peaks, peak_kind, traffic_key=None, share=1.0):
+    wbytes = packed_bytes(n, k, wb)
+    if m <= 256:  # HBM-bound (packed weight bytes dominate; SURVEY.md 8d)
+        ach = wbytes / (step_us * 1e-6) / 1e9
+        return {"bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": round(ach / peaks["hbm_gbs"], 4),
+                "traffic": ncu_traffic(traffic_key) if traffic_key else None,
+                "algorithmic_bytes_per_launch": wbytes, "peak_kind": peak_kind}
+    ops = 2 * m * n * k
+    ach = ops / (step_us * 1e-6) / 1e12
+    peak = 2 * peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+    return {"bound": "tensor", "achieved": round(ach, 1), "peak": round(peak, 1), "unit": "TFLOP/s",
+            "frac": round(ach / peak, 4), "traffic": ncu_traffic(traffic_key) if traffic_key else None,
+            "algorithmic_ops_per_launch": ops,
+            "peak_kind": f"{peak_kind}: int8 dense = 2 x sustained bf16 (B200 tensor core)"}
+
+
+def measure_part(abq, torch, name, world, steps, warmup, l2, peaks, peak_kind):
+    """One metric part on 1 GPU: step time over L2-cold rotating weights, its
+    roofline, and (M >= 8) a cuBLAS fp16 GEMM of the same shape, timed the same way."""
+    m, n, k, wb, ab, desc = WORKLOADS[name]
+    rng = np.random.default_rng(7)
+    copies = rotation_copies(l2, packed_bytes(n, k, wb), cap=128)
+    _, _, _, lins = build_linears(abq, torch, rng, m, n, k, wb, ab, copies)
+    x = torch.from_numpy(rng.standard_normal((m, k)).astype(np.float16)).cuda()
+    y = torch.empty((m, n), dtype=torch.float16, device="cuda")
+    ms, _ = time_graph(torch, lambda i: lins[i](x, out=y), copies, steps, warmup, world)
+    us = ms * 1e3 / steps
+    row = {"workload": desc, "step_us": round(us, 3),
+           "GBps_packed_weights": round(packed_bytes(n, k, wb) / us / 1e3, 1),
+           "TOPS": round(2 * m * n * k / us / 1e6, 2),
+           "roofline": roofline_for(m, n, k, wb, us, peaks, peak_kind, name)}
+    if m >= 8:
+        wf = [torch.randn((n, k), dtype=torch.float16, device="cuda")
+              for _ in range(rotation_copies(l2, n * k * 2, cap=32))]
+        xf = torch.randn((m, k), dtype=torch.float16, device="cuda")
+        yf = torch.empty((m, n), dtype=torch.float16, device="cuda")
+        cms, _ = time_graph(torch, lambda i: torch.matmul(xf, wf[i].t(), out=yf), len(wf), steps, warmup, world)
+        cus = cms * 1e3 / steps
+        row["cublas_fp16_us"] = round(cus, 3)
+        row["cublas_fp16_TOPS"] = round(2 * m * n * k / cus / 1e6, 2)
+        row["speedup_vs_cublas_fp16"] = round(cus / us, 3)
+        del wf
+    del lins
+    torch.cuda.empty_cache()
+    return row
+
+
+def run_layer(args, world, rank, local):
+    """cfg4 / cfg5: one LLaMA layer's 7 linears, column-sharded over the ranks
+    (strong scaling).  Step = the 7 shard linears back to back; the all-gather
+    of every linear's output slices is timed as a second leg."""
+    import torch
+    import paper_2408_08554_b200 as abq
+    from paper_2408_08554_b200.sharded import gather_columns, shard_bounds
+    m, wb, ab, projs, unit, desc = LAYERS[args.workload]
+    l2 = torch.cuda.get_device_properties(local).L2_cache_size
+    rng = np.random.default_rng(42 + rank)
+    spec = abq.QuantSpec(bits=ab, granularity=abq.api.PER_TOKEN)
+    shard_bytes = 0
+    layer = []
+    for p, n, k in projs:
+        lo, hi = shard_bounds(n, world)[rank]
+        wc, sb, zb = synth_layer(rng, hi - lo, k, wb)
+        w = abq.PackedWeights.from_planes(abq.bitpack(wc, wb), sb, zb)
+        shard_bytes += packed_bytes(hi - lo, k, wb)
+        xk = torch.from_numpy(np.random.default_rng(k).standard_normal((m, k)).astype(np.float16)).cuda()
+        layer.append((p, n, k, w, xk))
+    copies = rotation_copies(l2, shard_bytes, cap=32)
+    lins = [[abq.Linear(w if c == 0 else w.copy(), spec, max_m=m) for (_, _, _, w, _) in layer] for c in range(copies)]
+    ys = [torch.empty((m, w.planes.rows), dtype=torch.float16, device="cuda") for (_, _, _, w, _) in layer]
+
+    def step(c):
+        for j, (_, _, _, _, xk) in enumerate(layer):
+            lins[c][j](xk, out=ys[j])
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    l0 = abq.launch_count()
+    step(0)
+    per_step = abq.launch_count() - l0
+    ms, (tw0, tw1) = time_graph(torch, step, copies, args.steps, args.warmup, world)
+    clocks.stop()
+    step_ms = ms / args.steps
+    total_bytes = sum(packed_bytes(n, k, wb) for _, n, k in projs)
+    total_ops = sum(2 * m * n * k for _, n, k in projs)
+    work = total_bytes if unit == "GB/s" else total_ops
+    scale = 1e9 if unit == "GB/s" else 1e12
+    value = work / (step_ms * 1e-3) / scale
+    gather = None
+    if world > 1:
+        def step_gather(c):
+            step(c)
+            for j, (_, n, _, _, _) in enumerate(layer):
+                gather_columns(ys[j], n)
+        try:
+            g_ms, _ = time_graph(torch, step_gather, copies, args.steps, args.warmup, world)
+            how = "CUDA graph (7 shard linears + 7 NCCL all-gathers)"
+        except Exception as exc:  # noqa: BLE001 - graph capture of the collective unavailable
+            torch.cuda.synchronize()
+            barrier(world)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for i in range(args.steps):
+                step_gather(i % copies)
+            e1.record()
+            torch.cuda.synchronize()
+            g_ms = max_over_ranks(e0.elapsed_time(e1), world)
+            how = f"eager loop ({type(exc).__name__} capturing the collective)"
+        g_step = g_ms / args.steps
+        gather = {"ms_per_step": round(g_step, 6), "value": round(work / (g_step * 1e-3) / scale, 2),
+                  "unit": unit, "timing": how}
+    peaks, peak_kind = measured_peaks()
+    if unit == "GB/s":
+        ach = shard_bytes / (step_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": None,
+                "algorithmic_bytes_per_step_per_rank": shard_bytes, "peak_kind": peak_kind}
+    else:
+        shard_ops = total_ops / world
+        ach = shard_ops / (step_ms * 1e-3) / 1e12
+        peak = 2 * peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+        roof = {"bound": "tensor", "achieved": round(ach, 1), "peak": round(peak, 1), "unit": "TFLOP/s",
+                "frac": round(ach / peak, 4), "traffic": None, "algorithmic_ops_per_step_per_rank": shard_ops,
+                "peak_kind": f"{peak_kind}: int8 dense = 2 x sustained bf16"}
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": round(value, 2), "unit": unit, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(step_ms, 6), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": config_of(args.workload, world), "roofline": roof, "cpu_baseline": None,
+            "gpu_launches": per_step * args.steps, "launches_per_step": per_step,
+            "clocks": clocks.summary(tw0, tw1), "allgather": gather,
+            "run": {"rotation_copies": copies, "shard_bytes_per_rank": shard_bytes}}))
+
+
 def run_ours(args, world, rank, local):
     import torch
 
     import paper_2408_08554_b200 as abq
+    if args.workload in LAYERS:
+        return run_layer(args, world, rank, local)
     m, n, k, wb, ab, desc = WORKLOADS[args.workload]
     # column-parallel sharding, weak scaling (SURVEY.md 8e): the layer has
-    # world x N output channels and rank r owns channels [r*N, (r+1)*N) -- the
-    # workload's N per GPU at every GPU count.  No data-path collective; the
-    # output all-gather (where a layer's output must be reassembled) is timed
-    # as a separate leg below.
-    n_full = n * world
-    wbytes_full = packed_bytes(n_full, k, wb)
+    # world x N output channels and rank r owns channels [r*N, (r+1)*N).  No
+    # data-path collective; the output all-gather is timed as a separate leg.
     wbytes = packed_bytes(n, k, wb)
+    wbytes_full = wbytes * world
     l2 = torch.cuda.get_device_properties(local).L2_cache_size
-    copies = int(min(256, max(2, math.ceil(4 * l2 / wbytes))))
-    # every rank draws the same activations (seeded) and its own weight shard
-    x_np, wc, sb, zb, ws = build_layer(abq, torch, m, n, k, wb, ab, 1, seed=42 + rank)
+    copies = rotation_copies(l2, wbytes)
+    rng = np.random.default_rng(42 + rank)
+    wc, sb, zb, lins = build_linears(abq, torch, rng, m, n, k, wb, ab, copies)
     x_np = np.random.default_rng(42).standard_normal((m, k)).astype(np.float16)
-    shard = ws[0]
-    if args.variant != "auto":
-        abq.api.set_gemv_variant(args.variant)
-    weights = [shard] + [shard.copy() for _ in range(copies - 1)]
-    if args.variant == "popc":  # keep only the ABQP planes resident
-        for w in weights:
-            w.frag = None
-            w.tc = None
-    spec = abq.QuantSpec(bits=ab, granularity=abq.api.PER_TOKEN)
-    lins = [abq.Linear(w, spec, max_m=m) for w in weights]
-    if not args.no_prefetch_next:  # the layer sequence is known: hint each layer's successor
-        for i, lin in enumerate(lins):
-            lin.prefetch_next(lins[(i + 1) % len(lins)])
     x = torch.from_numpy(x_np).cuda()
     y = torch.empty((m, n), dtype=torch.float16, device="cuda")
 
     # ---- parity check of this exact workload against the oracle (rank 0's shard)
     parity = None
     if rank == 0 and not args.no_check:
-        from oracle.oracle import COracle
+        from oracle.oracle import COracle, exact_linear
         orc = COracle()
-        y64 = lins[0](x, out_dtype=torch.float64).cpu().numpy()
+        y64 = lins[0](x, out_dtype=torch.float64, check=True).cpu().numpy()
         ac, sa, za = orc.quantize(x_np.astype(np.float64), ab, 0, 2)
-        want = orc.quantized_linear(ac, ab, sa, za, wc, wb, sb, zb)
+        want = exact_linear(ac, sa, za, wc, sb, zb)
         y16 = lins[0](x, out_dtype=torch.float16).cpu().numpy()
         parity = bool(np.array_equal(y64, want) and np.array_equal(y16, want.astype(np.float16)))
         if not parity:
             raise SystemExit("bench: engine output differs from the oracle -- refusing to report")
 
+    a0 = abq.launch_count()
+    lins[0](x, out=y)
+    per_step = abq.launch_count() - a0
+
     clocks = ClockSampler(local)
     clocks.start()
-    launches0 = abq.launch_count()
-
-    # ---- headline: full step (K1 + K2/K4), weights rotated past L2
-    ms, (tw0, tw1) = time_graph(torch, lambda i: lins[i](x, out=y, check=False), copies, args.steps,
-                                args.warmup, world)
-    step_launches = (abq.launch_count() - launches0)
+    ms, (tw0, tw1) = time_graph(torch, lambda i: lins[i](x, out=y), copies, args.steps, args.warmup, world)
     clocks.stop()
     clk = clocks.summary(tw0, tw1)
     ms_per_step = ms / args.steps
-    value = wbytes_full / (ms_per_step * 1e-3) / 1e9  # whole-job bytes (all ranks) per step time
-
-    # graph capture recorded (copies + rem + warm) * launches-per-step; launches per step:
-    per_step = 0
-    a0 = abq.launch_count()
-    lins[0](x, out=y, check=False)
-    per_step = abq.launch_count() - a0
-    gpu_launches = per_step * args.steps
-
-    # ---- dominant kernel: with the fused single-launch path the step IS the
-    # kernel (timed above with CUDA events on its stream); otherwise time the
-    # GEMV + fused-epilogue kernel alone, back to back, on the same rotation.
-    fused = per_step == 1
-    if fused:
-        kernel_us = ms_per_step * 1e3
-        kernel_name = "gemv_dec_kernel (ReQuant prologue + tensor-pipe plane GEMV + epilogue)"
-    else:
-        a_planes, sa, za, ra = abq.api.quant_pack_act(x, spec)
-        kms, _ = time_graph(torch, lambda i: abq.linear_planes(a_planes, sa, za, ra, weights[i], out=y),
-                            copies, args.steps, args.warmup, world)
-        kernel_us = kms * 1e3 / args.steps
-        kernel_name = "gemv_popc_kernel (AND+popcount plane GEMV + epilogue)"
-    peak, peak_kind, _ = measured_peaks()
-    achieved = wbytes / (kernel_us * 1e-6) / 1e9
-    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": ncu_traffic(args.workload),
-                "kernel": kernel_name, "kernel_us": round(kernel_us, 3),
-                "algorithmic_bytes_per_launch": wbytes, "peak_kind": f"of {peak_kind}",
-                "kernel_share_of_step": round(kernel_us / (ms_per_step * 1e3), 3)}
+    step_us = ms_per_step * 1e3
+    unit = "GB/s" if m < 16 else "TOPS"
+    value = wbytes_full / (ms_per_step * 1e-3) / 1e9 if unit == "GB/s" else \
+        2 * m * n * k * world / (ms_per_step * 1e-3) / 1e12
+    peaks, peak_kind = measured_peaks()
+    roofline = roofline_for(m, n, k, wb, step_us, peaks, peak_kind, args.workload)
+    roofline["kernel"] = ("gemv_dec_kernel (ReQuant prologue + tensor-pipe plane GEMV + epilogue), one launch per step"
+                          if per_step == 1 else f"{per_step} launches per step (ReQuant + GEMM)")
+    roofline["kernel_us"] = round(step_us, 3)
+    roofline["kernel_us_is"] = ("per-step device time in a PDL-chained CUDA graph of back-to-back layers "
+                                "(consecutive launches overlap; an isolated launch is longer, see profiles/)")
 
     # ---- end to end through the public API with host buffers (GraphedLinear:
     # H2D x from pinned host, engine, D2H y into pinned host, every step)
-    e2e = None
-    if True:
-        gl = [abq.GraphedLinear(lins[i], m) for i in range(min(copies, 64))]
-        for g in gl:
-            g.x_host.copy_(torch.from_numpy(x_np))
-        for i in range(args.warmup):
-            gl[i % len(gl)].step()
-        torch.cuda.synchronize()
-        barrier(world)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for i in range(args.steps):
-            gl[i % len(gl)].step()
-        e1.record()
-        torch.cuda.synchronize()
-        e_ms = max_over_ranks(e0.elapsed_time(e1), world) / args.steps
-        # eager (per-call Python API, no graph) for reference
-        t0 = time.perf_counter()
-        eager_steps = min(args.steps, 2000)
-        xh = gl[0].x_host
-        yh = gl[0].y_host
-        xd = torch.empty_like(gl[0].x_dev)
-        for i in range(eager_steps):
-            xd.copy_(xh, non_blocking=True)
-            lins[i % copies](xd, out=y, check=False)
-            yh.copy_(y, non_blocking=True)
-        torch.cuda.synchronize()
-        eager_ms = (time.perf_counter() - t0) * 1e3 / eager_steps
-        e2e = {"value": round(wbytes_full / (e_ms * 1e-3) / 1e9, 1), "unit": "GB/s",
-               "h2d_bytes_per_step": gl[0].h2d_bytes, "d2h_bytes_per_step": gl[0].d2h_bytes,
-               "ms_per_step": round(e_ms, 5), "api": "abq.GraphedLinear.step()",
-               "eager_api_ms_per_step": round(eager_ms, 5)}
+    gl = [abq.GraphedLinear(lins[i], m) for i in range(min(copies, 64))]
+    for g in gl:
+        g.x_host.copy_(torch.from_numpy(x_np))
+    for i in range(max(args.warmup, len(gl))):
+        gl[i % len(gl)].step()
+    torch.cuda.synchronize()
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(args.steps):
+        gl[i % len(gl)].step()
+    e1.record()
+    torch.cuda.synchronize()
+    e_ms = max_over_ranks(e0.elapsed_time(e1), world) / args.steps
+    e_val = wbytes_full / (e_ms * 1e-3) / 1e9 if unit == "GB/s" else 2 * m * n * k * world / (e_ms * 1e-3) / 1e12
+    e2e = {"value": round(e_val, 2), "unit": unit, "h2d_bytes_per_step": gl[0].h2d_bytes,
+           "d2h_bytes_per_step": gl[0].d2h_bytes, "ms_per_step": round(e_ms, 5), "api": "abq.GraphedLinear.step()"}
+    del gl
 
-    # ---- reassembly leg (N > 1): the same step followed by the NCCL all-gather
-    # of the fp16 output slices over NVLink (sharded.gather_columns), captured in
-    # the same kind of CUDA graph; reported beside the compute-only headline.
+    # ---- reassembly leg (N > 1): the step followed by the NCCL all-gather of
+    # the fp16 output slices (sharded.gather_columns)
     gather = None
     if world > 1:
-        import torch.distributed as dist
-        buf = torch.empty((world, m, n), dtype=torch.float16, device="cuda")
+        from paper_2408_08554_b200.sharded import gather_columns
 
         def step_gather(i):
-            lins[i](x, out=y, check=False)
-            dist.all_gather_into_tensor(buf, y)
+            lins[i](x, out=y)
+            gather_columns(y, n * world)
         try:
             g_ms, _ = time_graph(torch, step_gather, copies, args.steps, args.warmup, world)
             how = "CUDA graph (engine step + ncclAllGather)"
-        except Exception as exc:  # graph capture of the collective unavailable: eager loop
+        except Exception as exc:  # noqa: BLE001
             torch.cuda.synchronize()
             barrier(world)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -430,96 +600,67 @@ def run_ours(args, world, rank, local):
         g_step = g_ms / args.steps
         gather = {"ms_per_step": round(g_step, 6), "value": round(wbytes_full / (g_step * 1e-3) / 1e9, 1),
                   "unit": "GB/s", "gather_bytes_per_rank": m * n * 2, "timing": how}
+    del lins
+    torch.cuda.empty_cache()
+
+    # ---- the other parts of the metric (N=1): W2A8 M=1 GEMV at LLaMA-7B
+    # shapes, W8A8 M=1, and the M=128 GEMM vs cuBLAS fp16
+    parts = None
+    if world == 1 and not args.no_parts:
+        part_steps = max(args.steps, 400)
+        parts = {name: measure_part(abq, torch, name, world, part_steps, max(args.warmup, 20), l2, peaks,
+                                    peak_kind) for name in PARTS if name != args.workload}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline_sample(m, n_full, k, wb, ab, budget_s=args.cpu_seconds)
+        cpu = cpu_baseline_sample(m, n, k, wb, ab, budget_s=args.cpu_seconds)
 
     line = {
-        "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world,
+        "metric": METRIC, "value": round(value, 2), "unit": unit, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 6),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "int32", "data": "synthetic",
-        "config": {"workload": desc, "m": m, "n": n_full, "n_per_gpu": n, "k": k, "w_bits": wb, "a_bits": ab,
-                   "parallelism": f"N-sharded x{world} (column-parallel)" if world > 1 else "single",
-                   "l2": f"rotating {copies} packed-weight copies ({copies * wbytes / 1e6:.0f} MB > 4x L2)",
-                   "step": "fp16 x -> ReQuant+BitPack -> plane GEMV -> zero-point+dequant -> fp16 y",
-                   "graph": "CUDA graph replay",
-                   "prefetch_next": not args.no_prefetch_next},
-        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches,
+        "dtype": "int32", "data": "synthetic", "config": config_of(args.workload, world),
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": per_step * args.steps,
         "launches_per_step": per_step, "clocks": clk, "parity": "bit-exact vs oracle" if parity else None,
-        "allgather": gather,
+        "allgather": gather, "parts": parts,
+        "run": {"rotation_copies": copies, "rotation_bytes": copies * wbytes, "n_per_rank": n},
     }
-    if args.sweep and rank == 0:
-        line["sweep"] = sweep(abq, torch, world)
     if rank == 0:
         print(json.dumps(line))
 
 
-def sweep(abq, torch, world):
-    """kernel-level table over the BASELINE configs (not the headline)."""
-    rows = []
-    for name, (m, n, k, wb, ab, desc) in WORKLOADS.items():
-        x_np, wc, sb, zb, _ = build_layer(abq, torch, m, n, k, wb, ab, 1)
-        wbytes = packed_bytes(n, k, wb)
-        l2 = torch.cuda.get_device_properties(0).L2_cache_size
-        copies = int(min(128, max(2, math.ceil(4 * l2 / wbytes))))
-        _, _, _, _, ws = build_layer(abq, torch, m, n, k, wb, ab, copies)
-        spec = abq.QuantSpec(bits=ab, granularity=abq.api.PER_TOKEN)
-        lins = [abq.Linear(w, spec, max_m=m) for w in ws]
-        x = torch.from_numpy(x_np).cuda()
-        y = torch.empty((m, n), dtype=torch.float16, device="cuda")
-        steps = 400
-        ms, _ = time_graph(torch, lambda i: lins[i](x, out=y, check=False), copies, steps, 20, world)
-        a_planes, sa, za, ra = abq.api.quant_pack_act(x, spec)
-        kms, _ = time_graph(torch, lambda i: abq.linear_planes(a_planes, sa, za, ra, ws[i], out=y),
-                            copies, steps, 20, world)
-        step_us, kern_us = ms * 1e3 / steps, kms * 1e3 / steps
-        row = {"workload": name, "step_us": round(step_us, 3), "kernel_us": round(kern_us, 3),
-               "kernel_GBps": round(wbytes / kern_us / 1e3, 1), "TOPS": round(2 * m * n * k / step_us / 1e6, 2)}
-        if m >= 16 and (ab, wb) in ((4, 4), (8, 8), (8, 2), (8, 4), (4, 8), (2, 2)):
-            # b1 tensor-core (mma.sync .b1 and.popc) plane GEMM, the BTC alternative
-            bsteps = 40
-            bms, _ = time_graph(torch, lambda i: abq.gemm_btc(a_planes, ws[i].planes), copies, bsteps, 3, world)
-            row["btc_b1_gemm_us"] = round(bms * 1e3 / bsteps, 3)
-        if m >= 8:
-            # cuBLAS fp16 comparator at the same shape (weights rotated past L2)
-            wf = [torch.randn((n, k), dtype=torch.float16, device="cuda") for _ in range(
-                max(2, math.ceil(4 * l2 / (n * k * 2))))]
-            xf = torch.randn((m, k), dtype=torch.float16, device="cuda")
-            yf = torch.empty((m, n), dtype=torch.float16, device="cuda")
-            cms, _ = time_graph(torch, lambda i: torch.matmul(xf, wf[i].t(), out=yf), len(wf), steps, 20,
-                                world)
-            row["cublas_fp16_us"] = round(cms * 1e3 / steps, 3)
-        rows.append(row)
-        del lins, ws
-        torch.cuda.empty_cache()
-    return rows
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20000)
+    ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=50)
     ap.add_argument("--impl", default="abq", choices=["abq", "reference"])
-    ap.add_argument("--workload", default="cfg2_w4a4_m1", choices=sorted(WORKLOADS))
-    ap.add_argument("--sweep", action="store_true")
+    ap.add_argument("--workload", default="cfg2_w4a4_m1", choices=sorted(list(WORKLOADS) + list(LAYERS)))
     ap.add_argument("--no-check", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--no-prefetch-next", action="store_true",
-                    help="do not give each layer its successor as an L2 prefetch hint")
+    ap.add_argument("--no-parts", action="store_true", help="headline workload only")
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
-    ap.add_argument("--variant", default="auto", choices=["auto", "popc", "recomb"],
-                    help="decode GEMV: auto | popc (AND+popcount) | recomb (planes on the int8 tensor pipe)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch under torchrun on this node
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if args.impl == "reference":
         run_reference(args, world, rank)
         return
-    world, rank, local = dist_setup(args)
+    world, rank, local = dist_setup()
     run_ours(args, world, rank, local)
     if world > 1:
         import torch.distributed as dist

@@ -306,3 +306,40 @@ def load_golden(path: str) -> dict:
     """tests/golden/*.npz -> dict name -> ndarray"""
     with np.load(path) as z:
         return {k: z[k] for k in z.files}
+
+
+# ---------------------------------------------------------------------------
+# large-shape restatement of quantized_linear (gemm.hpp:266-307) for the
+# LLaMA-sized parity tests, where the bit-serial C loop would take minutes.
+# The code product sum_k a_ik * w_jk is a sum of integers < 2^53 (K * 255^2 at
+# K = 2^17 is 2^33), so an fp64 BLAS matmul of the codes is exact; the
+# zero-point correction is int64 (gemm.hpp:245-251) and the dequant is
+# (s_a[i] * s_b[j]) * corrected in IEEE double, the reference's order
+# (gemm.hpp:298).  Pinned against COracle.quantized_linear (tests/test_oracle.py).
+# ---------------------------------------------------------------------------
+def exact_code_product(a_codes, w_codes) -> np.ndarray:
+    a = np.ascontiguousarray(a_codes, np.uint8)
+    w = np.ascontiguousarray(w_codes, np.uint8)
+    k = a.shape[1]
+    assert w.shape[1] == k
+    assert k * 255 * 255 < (1 << 53)
+    return (a.astype(np.float64) @ w.astype(np.float64).T).astype(np.int64)
+
+
+def exact_linear(a_codes, s_a, z_a, w_codes, s_b, z_b, acc=None) -> np.ndarray:
+    """quantized_linear on codes with per-token (act) / per-channel (weight)
+    parameters; float64 [M][N], bit-identical to the reference."""
+    a = np.ascontiguousarray(a_codes, np.uint8)
+    w = np.ascontiguousarray(w_codes, np.uint8)
+    k = a.shape[1]
+    if acc is None:
+        acc = exact_code_product(a, w)
+    ra = a.sum(axis=1, dtype=np.int64)
+    cb = w.sum(axis=1, dtype=np.int64)
+    za = np.asarray(z_a, np.int64).reshape(-1, 1)
+    zb = np.asarray(z_b, np.int64).reshape(1, -1)
+    corr = acc - za * cb.reshape(1, -1) - zb * ra.reshape(-1, 1) + k * za * zb
+    if np.all(np.abs(corr) < (1 << 31)):
+        corr = corr.astype(np.int32)  # the int32 path casts (gemm.hpp:252); values agree either way
+    sab = np.asarray(s_a, np.float64).reshape(-1, 1) * np.asarray(s_b, np.float64).reshape(1, -1)
+    return sab * corr.astype(np.float64)

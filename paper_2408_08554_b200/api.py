@@ -767,16 +767,47 @@ class Linear:
         return self
 
     def __call__(self, x: torch.Tensor, out: Optional[torch.Tensor] = None,
-                 out_dtype=torch.float16, check: bool = True) -> torch.Tensor:
+                 out_dtype=torch.float16, check: bool = False) -> torch.Tensor:
+        """y = quantized_linear(ReQuant(x), W) in one engine call.
+
+        check=False (the serving default) is launch-only: a non-finite
+        activation is recorded on the device and raised by the next
+        raise_if_nonfinite(); check=True synchronises and raises at once
+        (quantizer.hpp:155-160 semantics)."""
+        if not isinstance(x, torch.Tensor) or x.dim() != 2:
+            raise ShapeError("Linear: activations must be a 2-D tensor [M][K]")
+        if x.dtype not in (torch.float16, torch.float32, torch.float64):
+            raise ValueError(f"Linear: unsupported activation dtype {x.dtype}")
+        if x.device != self.ws.device:
+            raise ValueError(f"Linear: activations on {x.device}, weights on {self.ws.device}")
+        if not x.is_contiguous():
+            raise ValueError("Linear: activations must be contiguous (row stride K)")
         m = x.shape[0]
         if m > self.max_m:
             raise ValueError(f"Linear: m={m} exceeds max_m={self.max_m}")
+        n = self.w.planes.rows
         if out is None:
-            out = torch.empty((m, self.w.planes.rows), dtype=out_dtype, device=x.device)
-        _check(L.lib().abq_linear(_ptr(x), _dtype_code(x), m, self.k, C.byref(self._sc),
+            out = torch.empty((m, n), dtype=out_dtype, device=x.device)
+        else:
+            if out.dtype not in _OUT:
+                raise ValueError(f"Linear: unsupported output dtype {out.dtype}")
+            if tuple(out.shape) != (m, n) or not out.is_contiguous() or out.device != x.device:
+                raise ShapeError(f"Linear: out must be a contiguous ({m}, {n}) tensor on {x.device}")
+        # x.shape[1] (not self.k): the C-ABI rejects an inner-dimension mismatch
+        _check(L.lib().abq_linear(_ptr(x), _dtype_code(x), m, x.shape[1], C.byref(self._sc),
                                   C.byref(self._wc), _ptr(out), _OUT[out.dtype], _ptr(self.ws),
                                   self.ws_bytes, None if check else _ptr(self.err), _stream()))
+        if not check:
+            self._last_k = x.shape[1]
         return out
+
+    def raise_if_nonfinite(self) -> None:
+        """Synchronise and raise abq.ValueError if the last check=False call
+        saw a non-finite activation (the report is reset by every call)."""
+        v = int(self.err.item())
+        if v != -1:
+            k = getattr(self, "_last_k", self.k)
+            raise ValueError(f"quantize: non-finite element at ({v // k},{v % k})")
 
 
 class GraphedLinear:

@@ -551,7 +551,10 @@ size_t abq_linear_workspace_bytes(size_t m, size_t n, size_t k, unsigned act_pla
   return align256(imma_ws_bytes(n, k)) + align256(tc_sk_flag_bytes(n)) + 256 +
          align256(size_t(act_planes) * m * wpr_of(k) * 8) + align256(m * 8) + align256(m * 4) +
          align256(m * 8) + 256 + align256(tc_act_bytes(m, k)) + align256(m * k) +
-         align256(tc_sk_part_bytes(m, n));
+         align256(tc_sk_part_bytes(std::min<size_t>(m, 256), n));
+  // (the stream-K partial tiles are sized for min(m, 256) tokens: the GEMM only
+  // runs stream-K up to 256 tokens, and the total must not shrink as m grows,
+  // so a workspace sized for max_m serves every m <= max_m)
 }
 
 int abq_linear(const void* x, int x_dtype, size_t m, size_t k, const abq_quant_spec* act_spec,

@@ -88,12 +88,12 @@ def test_btc_gemm_matches_oracle(abq, orc, m, n, k, p, q):
     (33, 19000, 1024, 5, 3),    # row-tiles (149) >= SMs: no stream-K
     (100, 640, 11008, 6, 6),    # long K, 5 row-tiles -> 10 CTAs of ~43 k-blocks
 ])
-def test_tc_stream_k(abq, orc, m, n, k, wbits, abits, monkeypatch):
+def test_tc_stream_k(abq, orc, m, n, k, wbits, abits):
     """stream-K prefill GEMM (one token tile, row-tiles < SMs): bit-exact against
     the oracle, repeated calls (the hand-off flags reset themselves), a
     smaller m through the same workspace, and equal to the one-CTA-per-tile
-    schedule (ABQ_TC_SK=0)."""
-    monkeypatch.setenv("ABQ_TC_SK", "1")
+    schedule (abq_set_gemm_schedule(CLASSIC))."""
+    abq.api.set_gemm_schedule("stream_k")
     rng = np.random.default_rng(m + n + k)
     wc = rng.integers(0, 1 << wbits, (n, k), dtype=np.uint8)
     sb = rng.uniform(1e-3, 1e-2, n)
@@ -110,5 +110,29 @@ def test_tc_stream_k(abq, orc, m, n, k, wbits, abits, monkeypatch):
             assert np.array_equal(y, want), (mm, rep)
         y16 = lin(xd, out_dtype=torch.float16).cpu().numpy()
         assert np.array_equal(y16, want.astype(np.float16)), mm
-    monkeypatch.setenv("ABQ_TC_SK", "0")
-    assert np.array_equal(lin(xd, out_dtype=torch.float64).cpu().numpy(), want)
+    abq.api.set_gemm_schedule("classic")
+    try:
+        assert np.array_equal(lin(xd, out_dtype=torch.float64).cpu().numpy(), want)
+    finally:
+        abq.api.set_gemm_schedule("auto")
+
+
+def test_linear_workspace_serves_every_m_up_to_max_m(abq, orc):
+    """A Linear sized for max_m accepts every m <= max_m: the workspace need is
+    monotone in m (the stream-K partial tiles are sized for min(m, 256))."""
+    lib = abq._lib.lib()
+    n, k = 11008, 4096
+    needs = [lib.abq_linear_workspace_bytes(m, n, k, 4) for m in range(1, 2049, 7)] + \
+        [lib.abq_linear_workspace_bytes(2048, n, k, 4)]
+    assert all(a <= b for a, b in zip(needs, needs[1:]))
+    rng = np.random.default_rng(31)
+    wc = rng.integers(0, 16, (n, k), dtype=np.uint8)
+    sb = rng.uniform(1e-3, 1e-2, n)
+    zb = rng.integers(0, 16, n).astype(np.int32)
+    w = abq.PackedWeights.from_planes(abq.bitpack(wc, 4), sb, zb)
+    lin = abq.Linear(w, abq.QuantSpec(bits=4, granularity=abq.api.PER_TOKEN), max_m=2048)
+    for m in (1, 128, 200, 2048):
+        x = rng.standard_normal((m, k)).astype(np.float16)
+        y = lin(torch.from_numpy(x).cuda(), out_dtype=torch.float64).cpu().numpy()
+        ac, sa, za = orc.quantize(x.astype(np.float64), 4, 0, 2)
+        assert np.array_equal(y, orc.quantized_linear(ac, 4, sa, za, wc, 4, sb, zb)), m

@@ -91,10 +91,36 @@ def test_nonfinite_activation_reported(abq, variant):
     w = abq.PackedWeights.from_planes(abq.bitpack(wc, 4), sb, zb)
     lin = abq.Linear(w, abq.QuantSpec(bits=4, granularity=abq.api.PER_TOKEN), max_m=2)
     with pytest.raises(abq.ValueError, match=r"\(1,17\)"):
-        lin(torch.from_numpy(x).cuda())
+        lin(torch.from_numpy(x).cuda(), check=True)
     # the next clean call succeeds (status word and accumulators are reset)
     x[1, 17] = 0.5
+    lin(torch.from_numpy(x).cuda(), check=True)
+    # serving default (check=False): launch-only, the report is read later
+    x[1, 17] = -np.inf
     lin(torch.from_numpy(x).cuda())
+    with pytest.raises(abq.ValueError, match=r"\(1,17\)"):
+        lin.raise_if_nonfinite()
+    x[1, 17] = 0.25
+    lin(torch.from_numpy(x).cuda())
+    lin.raise_if_nonfinite()
+
+
+def test_linear_argument_checks(abq, variant):
+    rng = np.random.default_rng(12)
+    x, wc, sb, zb = _case(rng, 2, 64, 256, 4, 4)
+    w = abq.PackedWeights.from_planes(abq.bitpack(wc, 4), sb, zb)
+    lin = abq.Linear(w, abq.QuantSpec(bits=4, granularity=abq.api.PER_TOKEN), max_m=4)
+    xt = torch.from_numpy(x).cuda()
+    with pytest.raises(abq.ShapeError, match="inner dimensions"):
+        lin(torch.zeros((2, 255), dtype=torch.float16, device="cuda"))
+    with pytest.raises(abq.ValueError, match="contiguous"):
+        lin(torch.zeros((256, 2), dtype=torch.float16, device="cuda").t())
+    with pytest.raises(abq.ShapeError):
+        lin(xt, out=torch.empty((2, 63), dtype=torch.float16, device="cuda"))
+    with pytest.raises(abq.ShapeError):
+        lin(xt, out=torch.empty((64, 2), dtype=torch.float16, device="cuda").t())
+    with pytest.raises(abq.ValueError):
+        lin(xt.cpu())
 
 
 def test_repeated_calls_are_deterministic(abq, variant):

@@ -202,3 +202,31 @@ def test_oracle_matches_reference_random(orc, ref):
     sb, zb = rng.uniform(0.01, 0.1, 3), rng.integers(0, 256, 3).astype(np.int32)
     y_ref, _ = ref.quantized_linear(a, 8, 0, 2, sa, za, b, 8, 0, 1, sb, zb)
     assert np.array_equal(orc.quantized_linear(a, 8, sa, za, b, 8, sb, zb), y_ref)
+
+
+# ---- the large-shape numpy restatement used by the LLaMA-shape GPU tests ----
+def test_exact_linear_matches_oracle_and_golden(golden, orc):
+    from oracle.oracle import exact_code_product, exact_linear
+    rng = np.random.default_rng(17)
+    for _ in range(30):
+        m, n = (int(v) for v in rng.integers(1, 40, size=2))
+        k = int(rng.integers(1, 900))
+        p, q = (int(v) for v in rng.integers(1, 9, size=2))
+        x = rng.standard_normal((m, k)) * rng.uniform(0.1, 5)
+        ac, sa, za = orc.quantize(x, p, 0, 2)
+        wc = rng.integers(0, 1 << q, (n, k), dtype=np.uint8)
+        sb = rng.uniform(1e-3, 1e-2, n)
+        zb = rng.integers(0, 1 << q, n).astype(np.int32)
+        assert np.array_equal(exact_code_product(ac, wc), orc.gemm_codes(ac, p, wc, q).astype(np.int64))
+        assert np.array_equal(exact_linear(ac, sa, za, wc, sb, zb), orc.quantized_linear(ac, p, sa, za, wc, q, sb, zb))
+    # the wide regime (p + q + log2(K+1) > 31) too
+    a = rng.integers(0, 256, (2, 40000), dtype=np.uint8)
+    b = rng.integers(0, 256, (3, 40000), dtype=np.uint8)
+    sa, za = rng.uniform(0.01, 0.1, 2), rng.integers(0, 256, 2).astype(np.int32)
+    sb, zb = rng.uniform(0.01, 0.1, 3), rng.integers(0, 256, 3).astype(np.int32)
+    assert np.array_equal(exact_linear(a, sa, za, b, sb, zb), orc.quantized_linear(a, 8, sa, za, b, 8, sb, zb))
+    # and the reference-emitted LLaMA-shaped golden outputs
+    a, w = seeded_codes(1001, 1, 4096, 8), seeded_codes(1002, 4096, 4096, 2)
+    assert np.array_equal(exact_code_product(a, w), golden["big/cfg1_w2a8/out"])
+    a, w = seeded_codes(1003, 1, 4096, 4), seeded_codes(1004, 11008, 4096, 4)
+    assert np.array_equal(exact_code_product(a, w), golden["big/cfg2_w4a4_m1/out"])
