@@ -362,6 +362,15 @@ def build_linears(abq, torch, rng, m, n, k, wb, ab, copies):
     return wc, sb, zb, [abq.Linear(w, spec, max_m=m) for w in ws]
 
 
+def build_layer(abq, torch, m, n, k, wb, ab, copies, seed=7):
+    """(x, weight codes, s_b, z_b, [PackedWeights] x copies) -- for tools/trace_*.py"""
+    rng = np.random.default_rng(seed)
+    wc, sb, zb = synth_layer(rng, n, k, wb)
+    base = abq.PackedWeights.from_planes(abq.bitpack(wc, wb), sb, zb)
+    x = rng.standard_normal((m, k)).astype(np.float16)
+    return x, wc, sb, zb, [base] + [base.copy() for _ in range(copies - 1)]
+
+
 def roofline_for(m, n, k, wb, step_us, peaks, peak_kind, traffic_key=None, share=1.0):
     wbytes = packed_bytes(n, k, wb)
     if m <= 256:  # HBM-bound (packed weight bytes dominate; SURVEY.md 8d)

@@ -24,6 +24,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
+#include <utility>
 #include <chrono>
 #include <iterator>
 #include <cstdint>
@@ -127,11 +129,55 @@ struct Matrix {
   std::size_t size() const { return rows * cols; }
   bool same_shape(const Matrix& o) const { return rows == o.rows && cols == o.cols; }
   bool operator==(const Matrix& o) const { return same_shape(o) && data == o.data; }
+  Matrix<T> transposed() const {  // core.hpp:55-62
+    Matrix<T> out(cols, rows);
+    for (std::size_t i = 0; i < rows; ++i)
+      for (std::size_t j = 0; j < cols; ++j) out.data[j * rows + i] = data[i * cols + j];
+    return out;
+  }
 };
 
 using Mat = Matrix<double>;
 using CodeMat = Matrix<std::uint8_t>;
 using IntMat = Matrix<std::int64_t>;
+
+// ---- FP64 host helpers of core.hpp:72-111 (test / calibration utilities, not
+// the engine: the quantized product itself always runs on the device) --------
+inline Mat matmul(const Mat& a, const Mat& b) {
+  if (a.cols != b.rows) throw ShapeError("matmul: inner dimensions differ");
+  Mat out(a.rows, b.cols, 0.0);
+  for (std::size_t i = 0; i < a.rows; ++i)
+    for (std::size_t k = 0; k < a.cols; ++k) {
+      const double aik = a(i, k);
+      double* row = out.data.data() + i * out.cols;
+      const double* brow = b.data.data() + k * b.cols;
+      for (std::size_t j = 0; j < b.cols; ++j) row[j] += aik * brow[j];
+    }
+  return out;
+}
+inline double max_abs_diff(const Mat& a, const Mat& b) {
+  if (!a.same_shape(b)) throw ShapeError("max_abs_diff: shape mismatch");
+  double m = 0.0;
+  for (std::size_t i = 0; i < a.data.size(); ++i) m = std::max(m, std::abs(a.data[i] - b.data[i]));
+  return m;
+}
+inline double frobenius(const Mat& a) {
+  double s = 0.0;
+  for (double v : a.data) s += v * v;
+  return std::sqrt(s);
+}
+inline double rel_diff(const Mat& got, const Mat& want) {
+  if (!got.same_shape(want)) throw ShapeError("rel_diff: shape mismatch");
+  double num = 0.0, den = 0.0;
+  for (std::size_t i = 0; i < got.data.size(); ++i) {
+    const double d = got.data[i] - want.data[i];
+    num += d * d;
+    den += want.data[i] * want.data[i];
+  }
+  return den == 0.0 ? std::sqrt(num) : std::sqrt(num / den);
+}
+/// std::round: half away from zero (core.hpp:145)
+inline double round_half_away(double v) { return std::round(v); }
 
 /// Seeded generator with the reference's distributions (core.hpp:113-142), so
 /// seeded test cases replay the reference's inputs draw for draw.
@@ -212,6 +258,18 @@ struct QuantizedTensor {
   std::size_t axis_count() const { return scales.size(); }
   std::size_t axis_of(std::size_t i, std::size_t) const {
     return spec.granularity == Granularity::PerTensor ? 0 : i;
+  }
+  /// quantizer.hpp:95-107: spec valid, every code < levels, one scale / zero
+  /// point per axis group
+  void validate() const {
+    spec.validate();
+    const unsigned max_code = spec.levels() - 1;
+    for (std::size_t i = 0; i < codes.data.size(); ++i)
+      if (codes.data[i] > max_code)
+        throw ValueError("QuantizedTensor: code out of range at flat index " + std::to_string(i));
+    const std::size_t want = spec.granularity == Granularity::PerTensor ? 1 : codes.rows;
+    if (scales.size() != want || zero_points.size() != want)
+      throw ValueError("QuantizedTensor: scale/zero_point count does not match granularity");
   }
 };
 
@@ -363,7 +421,7 @@ inline Matrix<std::int32_t> gemm_naive(const BitPlaneMatrix& a, const BitPlaneMa
 // ---- tuning (tune.hpp:51-192) --------------------------------------------------
 namespace detail {
 /// padded rows summed over the BM-row blocks covering m rows (tune.hpp:35-44)
-inline std::size_t row_padding_total(std::size_t m, unsigned p, std::size_t bm, std::size_t mma_m) {
+inline std::size_t total_row_padding(std::size_t m, unsigned p, std::size_t bm, std::size_t mma_m) {
   std::size_t total = 0;
   for (std::size_t start = 0; start < m; start += bm) {
     const std::size_t rows = p * std::min(bm, m - start);
@@ -391,10 +449,10 @@ inline std::vector<TileConfig> enumerate_tile_candidates(unsigned p, unsigned q,
           if (t.valid(p, q) && seen.emplace(t.BM, t.BN, t.BK, t.WM, t.WN).second) all.push_back(t);
         }
   std::size_t least = ~std::size_t(0);
-  for (const auto& t : all) least = std::min(least, detail::row_padding_total(m, p, t.BM, TileConfig::mma_m));
+  for (const auto& t : all) least = std::min(least, detail::total_row_padding(m, p, t.BM, TileConfig::mma_m));
   std::vector<TileConfig> out;
   std::copy_if(all.begin(), all.end(), std::back_inserter(out), [&](const TileConfig& t) {
-    return detail::row_padding_total(m, p, t.BM, TileConfig::mma_m) == least;
+    return detail::total_row_padding(m, p, t.BM, TileConfig::mma_m) == least;
   });
   if (out.empty()) out.push_back(default_tile(p, q));
   return out;
@@ -412,6 +470,11 @@ struct BenchRecord {
 };
 
 namespace detail {
+/// median  tune.hpp:108-111
+inline double median(std::vector<double> v) {
+  std::sort(v.begin(), v.end());
+  return v.size() % 2 ? v[v.size() / 2] : 0.5 * (v[v.size() / 2 - 1] + v[v.size() / 2]);
+}
 /// tops_of  tune.hpp:129-131
 inline double tops_of(std::size_t m, std::size_t n, std::size_t k, double us) {
   return 2.0 * double(m) * double(n) * double(k) / (us * 1e6);
@@ -427,9 +490,7 @@ inline double time_median_us(Fn&& fn, unsigned trials) {
     fn();
     us.push_back(std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count());
   }
-  std::sort(us.begin(), us.end());
-  const std::size_t h = us.size() / 2;
-  return us.size() % 2 ? us[h] : 0.5 * (us[h - 1] + us[h]);
+  return median(std::move(us));
 }
 }  // namespace detail
 
@@ -545,6 +606,34 @@ inline QuantizedTensor quantize(const Mat& x, const QuantSpec& spec,
   ds.to_host(q.scales.data());
   dz.to_host(q.zero_points.data());
   return q;
+}
+
+/// apply_balance  quantizer.hpp:228-241: (W diag(s), diag(s)^-1 X), the
+/// offline smoothing rescale (host FP64, like the reference; not the engine)
+inline std::pair<Mat, Mat> apply_balance(const Mat& w, const Mat& x, const std::vector<double>& s) {
+  if (w.cols != s.size() || x.rows != s.size())
+    throw ShapeError("apply_balance: s length must equal the shared inner dimension");
+  for (std::size_t k = 0; k < s.size(); ++k)
+    if (!(s[k] > 0.0)) throw ValueError("apply_balance: s[" + std::to_string(k) + "] is not positive");
+  Mat ws = w, xs = x;
+  for (std::size_t i = 0; i < w.rows; ++i)
+    for (std::size_t k = 0; k < w.cols; ++k) ws(i, k) *= s[k];
+  for (std::size_t k = 0; k < x.rows; ++k)
+    for (std::size_t j = 0; j < x.cols; ++j) xs(k, j) /= s[k];
+  return {std::move(ws), std::move(xs)};
+}
+
+/// dequantize  quantizer.hpp:243-254: (code - z) * step, on the device
+inline Mat dequantize(const QuantizedTensor& q) {
+  q.validate();
+  Mat out(q.rows(), q.cols());
+  detail::DeviceBuffer<std::uint8_t> dc(q.codes.data);
+  detail::DeviceBuffer<double> ds(q.scales), dout(out.data.size());
+  detail::DeviceBuffer<std::int32_t> dz(q.zero_points);
+  detail::check(abq_dequantize(dc.get(), q.rows(), q.cols(), ds.get(), dz.get(),
+                               q.spec.granularity == Granularity::PerTensor ? 1 : 0, dout.get(), nullptr));
+  dout.to_host(out.data.data());
+  return out;
 }
 
 inline QuantizedTensor quantize_balanced(const Mat& x, unsigned bits,

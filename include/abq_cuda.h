@@ -195,6 +195,11 @@ int abq_zero_point_correct_i64(const int64_t* acc, size_t m, size_t n, const int
                                size_t k, int64_t* out, void* stream);
 /* code_rowsums  gemm.hpp:256-261 */
 int abq_code_rowsums(const uint8_t* codes, size_t rows, size_t cols, int64_t* out, void* stream);
+/* dequantize  quantizer.hpp:243-254: out[i][j] = (code - z[g]) * step[g] in FP64,
+ * g = 0 (per_tensor) or i (per-row granularities).  Validation (code range,
+ * parameter counts) is the caller's, as QuantizedTensor::validate. */
+int abq_dequantize(const uint8_t* codes, size_t rows, size_t cols, const double* scales,
+                   const int32_t* zero_points, int per_tensor, double* out, void* stream);
 
 /* K5: colsum_b of packed weights from their planes (= code_rowsums(wt.codes),
  * gemm.hpp:278): colsum[j] = sum_t 2^t popc(W_t[j]). */

@@ -72,6 +72,8 @@ int run_bitpack(const uint8_t* codes, size_t rows, size_t cols, unsigned bits, u
 int run_unpack(const uint64_t* planes, unsigned bits, size_t rows, size_t cols, uint8_t* codes,
                cudaStream_t st);
 int run_code_rowsums(const uint8_t* codes, size_t rows, size_t cols, int64_t* out, cudaStream_t st);
+int run_dequantize(const uint8_t* codes, size_t rows, size_t cols, const double* scales, const int32_t* zps,
+                   int per_tensor, double* out, cudaStream_t st);
 int run_plane_rowsums(const uint64_t* planes, unsigned bits, size_t rows, size_t cols, int64_t* out,
                       cudaStream_t st);
 template <typename Acc>
@@ -466,6 +468,13 @@ int abq_code_rowsums(const uint8_t* codes, size_t rows, size_t cols, int64_t* ou
   int st = check_device();
   if (st) return st;
   return run_code_rowsums(codes, rows, cols, out, as_stream(stream));
+}
+
+int abq_dequantize(const uint8_t* codes, size_t rows, size_t cols, const double* scales,
+                   const int32_t* zero_points, int per_tensor, double* out, void* stream) {
+  int st = check_device();
+  if (st) return st;
+  return run_dequantize(codes, rows, cols, scales, zero_points, per_tensor, out, as_stream(stream));
 }
 
 int abq_plane_rowsums(const uint64_t* planes, unsigned bits, size_t rows, size_t cols, int64_t* out,

@@ -361,6 +361,25 @@ int run_code_rowsums(const uint8_t* codes, size_t rows, size_t cols, int64_t* ou
   return ABQ_OK;
 }
 
+// ---- dequantize  quantizer.hpp:243-254: out = (code - z) * step (FP64, RN) ---
+__global__ void dequantize_kernel(const uint8_t* __restrict__ codes, size_t rows, size_t cols,
+                                  const double* __restrict__ scales, const int32_t* __restrict__ zps,
+                                  int per_tensor, double* __restrict__ out) {
+  const size_t total = rows * cols, stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total; idx += stride) {
+    const size_t g = per_tensor ? 0 : idx / cols;
+    out[idx] = __dmul_rn(__dsub_rn(static_cast<double>(codes[idx]), static_cast<double>(zps[g])), scales[g]);
+  }
+}
+
+int run_dequantize(const uint8_t* codes, size_t rows, size_t cols, const double* scales, const int32_t* zps,
+                   int per_tensor, double* out, cudaStream_t st) {
+  if (rows == 0 || cols == 0) return ABQ_OK;
+  dequantize_kernel<<<grid_for(rows * cols, 256), 256, 0, st>>>(codes, rows, cols, scales, zps, per_tensor, out);
+  ABQ_LAUNCHED();
+  return ABQ_OK;
+}
+
 int run_plane_rowsums(const uint64_t* planes, unsigned bits, size_t rows, size_t cols, int64_t* out,
                       cudaStream_t st) {
   if (rows == 0) return ABQ_OK;

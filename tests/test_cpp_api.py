@@ -1,11 +1,21 @@
-"""Runs tests/cpp/test_api (the reference's hot-path test cases restated
-against the C++ drop-in mirror include/abq/abq.hpp) on the GPU."""
+"""C++ drop-in (include/abq/*.hpp -> libabq_cuda.so):
+
+* tests/cpp/test_api: the reference's hot-path test cases restated, on the GPU;
+* tests/cpp/ref_tests: the reference's OWN unmodified Catch2 sources
+  (test_bitkernel.cpp, test_quantizer.cpp, test_tune.cpp) compiled against the
+  drop-in headers with a Catch2-compatible shim (tests/cpp/catch2/), on the GPU;
+* (CPU) those reference sources compile against the drop-in headers, when the
+  reference tree is present (this container; the GPU box gets the binary)."""
 import os
+import shutil
 import subprocess
 
 import pytest
 
 HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+REF_TESTS = "/root/reference/proj/tests"
+REF_SRCS = ["test_bitkernel.cpp", "test_quantizer.cpp", "test_tune.cpp"]
 
 
 @pytest.mark.gpu
@@ -17,3 +27,25 @@ def test_cpp_drop_in_api():
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert r.stdout.count("PASS") == 9
+
+
+@pytest.mark.gpu
+def test_reference_unit_tests_on_drop_in():
+    exe = os.path.join(HERE, "cpp", "ref_tests")
+    if not os.path.exists(exe):
+        pytest.skip("tests/cpp/ref_tests is built by build() where the reference tree exists")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=900)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    # test_bitkernel.cpp (10) + test_quantizer.cpp (10) + test_tune.cpp (5) TEST_CASEs
+    assert "25 test cases: 25 passed, 0 failed" in r.stdout, r.stdout
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_TESTS) or shutil.which("g++") is None,
+                    reason="reference tree not present")
+def test_reference_unit_tests_compile_against_drop_in():
+    for src in REF_SRCS:
+        r = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-I" + os.path.join(HERE, "cpp"),
+                            "-I" + os.path.join(ROOT, "include"), "-I/usr/local/cuda/include",
+                            os.path.join(REF_TESTS, src)], capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, src + "\n" + r.stderr[-3000:]
