@@ -657,6 +657,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parts", action="store_true", help="headline workload only")
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
+    ap.add_argument("--tune", action="append", default=[],
+                    help="key=value launch-planning knob for sweeps (abq_set_tuning; results never depend on it)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
@@ -670,6 +672,11 @@ def main():
         run_reference(args, world, rank)
         return
     world, rank, local = dist_setup()
+    if args.tune:
+        import paper_2408_08554_b200 as abq
+        for kv in args.tune:
+            key, val = kv.split("=")
+            abq._lib.lib().abq_set_tuning(key.encode(), int(val))
     run_ours(args, world, rank, local)
     if world > 1:
         import torch.distributed as dist

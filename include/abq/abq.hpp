@@ -675,7 +675,7 @@ inline Mat quantized_linear(const QuantizedTensor& act, const QuantizedTensor& w
     detail::check(abq_weights_prepack_tc(dwp.get(), q, n, k, dlay.get(), nullptr));
   abq_weights w{dwp.get(), q, n, k, dsb.get(), dzb.get(), dcb.get(),
                 wt.spec.granularity == Granularity::PerTensor, decode ? dlay.get() : nullptr,
-                decode ? nullptr : dlay.get(), nullptr, 0};
+                decode ? nullptr : dlay.get()};
   Mat out(m, n);
   detail::DeviceBuffer<double> dy(out.data.size());
   detail::check(abq_linear_planes(&a, &w, dy.get(), ABQ_OUT_F64, nullptr));
@@ -709,7 +709,7 @@ class Weights {
   }
   abq_weights view() const {
     return abq_weights{planes_.get(), q_, n_, k_, scales_.get(), zps_.get(), colsums_.get(),
-                       per_tensor_ ? 1 : 0, frag_.get(), tc_.get(), nullptr, 0};
+                       per_tensor_ ? 1 : 0, frag_.get(), tc_.get()};
   }
   std::size_t n() const { return n_; }
   std::size_t k() const { return k_; }

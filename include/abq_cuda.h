@@ -94,13 +94,6 @@ typedef struct {
   /* optional tcgen05-GEMM copy of the planes (abq_weights_prepack_tc) used
    * for M >= 9 tokens; NULL = no prefill tensor-core path */
   const uint32_t* tc;
-  /* optional L2 prefetch hint for the decode GEMV: the fragment-major weights
-   * (frag) of the layer that runs after this one and their byte count.  The
-   * GEMV streams them into L2 (evict-first) behind its own weights, so the
-   * next layer's input-independent weight traffic overlaps this layer's
-   * activation-dependent work.  NULL = no hint. */
-  const void* prefetch_next;
-  size_t prefetch_next_bytes;
 } abq_weights;
 
 /* Activation-side metadata produced by abq_quant_pack_act (per-token or
@@ -270,9 +263,18 @@ typedef enum {
 int abq_set_gemm_schedule(int schedule);
 int abq_get_gemm_schedule(void);
 
-/* Profiling hook: when set (device buffer of >= 4 u64 per CTA, NULL = off),
- * the decode GEMV records %globaltimer at kernel start, after the ReQuant
- * prologue, after the main loop and before the split-tile epilogue. */
+/* Launch-planning knobs for sweeps and tools (results never depend on them;
+ * the defaults are the measured best): "dec_pre_kb" (decode GEMV weight-ring
+ * KB issued before the activations are awaited, default 64), "dec_ring_kb"
+ * (ring cap, 0 = whole CTA share), "dec_pdl" (0/1), "tc_dbg" (prefill GEMM
+ * experiment switches, tools/trace_gemm.py), "reset".  Returns ABQ_ERR_VALUE
+ * for an unknown key. */
+int abq_set_tuning(const char* key, long long value);
+
+/* Profiling hook (phase stamps, [grid][64] u64 per launch, NULL = off).  The
+ * stamps are compiled only into the trace build of the library
+ * (make -C paper_2408_08554_b200/csrc TRACE=1 -> libabq_cuda_trace.so, loaded by
+ * tools/trace_*.py via ABQ_LIB); in the product library this is a no-op. */
 int abq_set_trace_buffer(void* dev_words);
 
 #ifdef __cplusplus

@@ -12,7 +12,9 @@ import os
 import re
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libabq_cuda.so")
+# ABQ_LIB selects another build of the same library (tools: the trace build
+# libabq_cuda_trace.so); the product path is the in-tree libabq_cuda.so
+LIB_PATH = os.environ.get("ABQ_LIB") or os.path.join(_HERE, "libabq_cuda.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "abq_cuda.h")
 
 ABQ_OK, ABQ_ERR_SHAPE, ABQ_ERR_VALUE, ABQ_ERR_OVERFLOW, ABQ_ERR_IO, ABQ_ERR_CUDA = range(6)
@@ -39,8 +41,7 @@ class GemmStatsC(C.Structure):
 class WeightsC(C.Structure):
     _fields_ = [("planes", C.c_void_p), ("q", C.c_uint), ("n", C.c_size_t), ("k", C.c_size_t),
                 ("scales", C.c_void_p), ("zero_points", C.c_void_p), ("colsums", C.c_void_p),
-                ("per_tensor", C.c_int), ("frag", C.c_void_p), ("tc", C.c_void_p),
-                ("prefetch_next", C.c_void_p), ("prefetch_next_bytes", C.c_size_t)]
+                ("per_tensor", C.c_int), ("frag", C.c_void_p), ("tc", C.c_void_p)]
 
 
 class ActC(C.Structure):
@@ -78,6 +79,7 @@ _SIGNATURES = {
     "abq_zero_point_correct_i32": (_I, [_P, _S, _S, _P, _P, _P, _P, _S, _P, _P]),
     "abq_zero_point_correct_i64": (_I, [_P, _S, _S, _P, _P, _P, _P, _S, _P, _P]),
     "abq_code_rowsums": (_I, [_P, _S, _S, _P, _P]),
+    "abq_dequantize": (_I, [_P, _S, _S, _P, _P, _I, _P, _P]),
     "abq_plane_rowsums": (_I, [_P, _U, _S, _S, _P, _P]),
     "abq_weights_frag_bytes": (_S, [_U, _S, _S]),
     "abq_weights_prepack": (_I, [_P, _U, _S, _S, _P, _P]),
@@ -92,6 +94,7 @@ _SIGNATURES = {
     "abq_set_gemm_schedule": (_I, [_I]),
     "abq_get_gemm_schedule": (_I, []),
     "abq_set_trace_buffer": (_I, [_P]),
+    "abq_set_tuning": (_I, [C.c_char_p, C.c_longlong]),
 }
 
 

@@ -655,7 +655,7 @@ class PackedWeights:
                           self.planes.cols, _ptr(self.scales), _ptr(self.zero_points),
                           _ptr(self.colsums), int(self.per_tensor),
                           _ptr(self.frag) if self.frag is not None else None,
-                          _ptr(self.tc) if self.tc is not None else None, None, 0)
+                          _ptr(self.tc) if self.tc is not None else None)
 
     def copy(self) -> "PackedWeights":
         """Distinct HBM copy of the packed weights (same values)."""
@@ -754,17 +754,6 @@ class Linear:
         self.max_m = max_m
         self._wc = weights.c()
         self._sc = act_spec.c()
-
-    def prefetch_next(self, nxt: Optional["Linear"]) -> "Linear":
-        """Declare the layer that runs after this one: the decode GEMV then
-        streams the next layer's packed weights into L2 while this layer waits
-        for / quantizes its activations (weights are input-independent).  A
-        hint only -- results do not depend on it."""
-        f = None if nxt is None else nxt.w.frag
-        self._next = nxt  # keep the tensor alive
-        self._wc.prefetch_next = _ptr(f) if f is not None else None
-        self._wc.prefetch_next_bytes = f.numel() * f.element_size() if f is not None else 0
-        return self
 
     def __call__(self, x: torch.Tensor, out: Optional[torch.Tensor] = None,
                  out_dtype=torch.float16, check: bool = False) -> torch.Tensor:

@@ -86,15 +86,15 @@ int run_gemm_popc(const uint64_t* A, unsigned p, size_t m, const uint64_t* W, un
 size_t frag_words(unsigned q, size_t n, size_t k);
 size_t imma_ws_bytes(size_t n, size_t k);
 bool imma_supported(size_t m, size_t k);
+bool dec_supported(unsigned q, size_t n, size_t k, size_t m);
 unsigned long long*& trace_buffer();
 int run_prepack_frag(const uint64_t* planes, unsigned q, size_t n, size_t k, uint32_t* frag,
                      cudaStream_t st);
 int run_gemv_imma_planes(const uint32_t* frag, unsigned q, size_t n, size_t k, size_t m,
                          const uint64_t* a_planes, unsigned p, const EpiParams& e, cudaStream_t st);
-int run_gemv_imma_fused(const uint32_t* frag, unsigned q, size_t n, size_t k, size_t m, const void* x,
-                        int x_dtype, const QuantParams& qp, const EpiParams& e, void* ws,
-                        unsigned long long* bad_out, cudaStream_t st, const void* next_frag,
-                        size_t next_bytes);
+int run_gemv_dec(const uint32_t* frag, unsigned q, size_t n, size_t k, size_t m, const void* x, int x_dtype,
+                 const QuantParams& qp, const EpiParams& e, void* ws, unsigned long long* bad_out,
+                 cudaStream_t st);
 
 int run_gemm_bmma(const uint64_t* a, unsigned p, size_t m, const uint64_t* w, unsigned q, size_t n, size_t k,
                   int32_t* out, cudaStream_t st);
@@ -114,10 +114,15 @@ int run_act_quant(const void* x, int x_dtype, size_t m, size_t k, int mt, const 
                   uint32_t* out, int row_ld, double* s_a, int32_t* z_a, long long* rowsum,
                   unsigned long long* bad_word, cudaStream_t st);
 
-// decode GEMV on the tensor pipe: weights prepacked, M <= 8 tokens
+// decode GEMV on the tensor pipe: weights prepacked, M <= 8 tokens.  API path
+// (activation planes given, abq_linear_planes): gemv_imma_kernel
 static bool use_imma(const abq_weights* w, size_t m, size_t k) {
   return w->frag != nullptr && m >= 1 && m <= 8 && imma_supported(m, k) &&
          g_gemv_variant != ABQ_GEMV_POPC;
+}
+// serving path (abq_linear, activations quantized on the fly): gemv_dec_kernel
+static bool use_dec(const abq_weights* w, size_t m, size_t k) {
+  return w->frag != nullptr && dec_supported(w->q, w->n, k, m) && g_gemv_variant != ABQ_GEMV_POPC;
 }
 // prefill GEMM on tcgen05: weights prepacked (tc planes), M >= 9 tokens
 static bool use_tc(const abq_weights* w, size_t m, size_t k, bool wide) {
@@ -293,6 +298,19 @@ int abq_set_gemm_schedule(int schedule) {
   return ABQ_OK;
 }
 int abq_get_gemm_schedule(void) { return gemm_schedule(); }
+
+int abq_set_tuning(const char* key, long long value) {
+  if (!key) return fail(ABQ_ERR_VALUE, "abq_set_tuning: null key");
+  DecTuning& t = dec_tuning();
+  const std::string k(key);
+  if (k == "dec_pre_kb" && value >= -1) t.pre_kb = static_cast<int>(value);
+  else if (k == "dec_ring_kb" && value >= 0) t.ring_kb = static_cast<int>(value);
+  else if (k == "dec_pdl") t.pdl = value != 0;
+  else if (k == "tc_dbg") t.tc_dbg = static_cast<int>(value);
+  else if (k == "reset") t = DecTuning{};
+  else return fail(ABQ_ERR_VALUE, "abq_set_tuning: unknown key or bad value '%s'=%lld", key, value);
+  return ABQ_OK;
+}
 
 int abq_set_trace_buffer(void* dev_words) {
   trace_buffer() = static_cast<unsigned long long*>(dev_words);
@@ -605,7 +623,7 @@ int abq_linear(const void* x, int x_dtype, size_t m, size_t k, const abq_quant_s
   }
   unsigned long long* bad = err_index ? reinterpret_cast<unsigned long long*>(err_index) : sc;
   cudaStream_t s = as_stream(stream);
-  if (use_imma(w, m, k)) {
+  if (use_dec(w, m, k)) {
     // single launch: ReQuant prologue + tensor-pipe plane GEMV + fused epilogue
     EpiParams e{};
     e.mode = mode;
@@ -618,8 +636,7 @@ int abq_linear(const void* x, int x_dtype, size_t m, size_t k, const abq_quant_s
     e.colsum_b = w->colsums;
     e.k = static_cast<long long>(k);
     const QuantParams qp = params_of(*act_spec);
-    st = run_gemv_imma_fused(w->frag, w->q, w->n, k, m, x, x_dtype, qp, e, ws_imma, bad, s, w->prefetch_next,
-                             w->prefetch_next ? w->prefetch_next_bytes : 0);
+    st = run_gemv_dec(w->frag, w->q, w->n, k, m, x, x_dtype, qp, e, ws_imma, bad, s);
     if (st) return st;
   } else if (use_tc(w, m, k, !fits_int32_host(p, w->q, k))) {
     // ReQuant straight to u8 codes (K1), then the tcgen05 GEMM with the fused epilogue

@@ -16,6 +16,16 @@ namespace abq_dev {
 
 // ---- host-side error state (thread-local, C-ABI abq_last_error) -----------
 std::string& last_error();
+
+// Process-wide launch-planning knobs, set through abq_set_tuning (tools and
+// sweeps only; the defaults are the measured best).  Results never depend on them.
+struct DecTuning {
+  int pre_kb = -1;   // decode GEMV: weight-ring KB issued before the activations are awaited (-1 = auto)
+  int ring_kb = 0;   // decode GEMV: ring size cap in KB (0 = the CTA's whole share when it fits)
+  int pdl = 1;       // decode GEMV: programmatic dependent launch
+  int tc_dbg = 0;    // prefill GEMM: experiment switches (tools/trace_gemm.py), 0 in production
+};
+DecTuning& dec_tuning();
 int fail(int status, const char* fmt, ...);
 uint64_t& launch_counter();
 int num_sms();

@@ -349,7 +349,7 @@ struct TcParams {
   unsigned long long* bad_word;  // ReQuant status (~index, 0 = none), published to bad_out
   unsigned long long* bad_out;
   unsigned long long* trace;  // optional [grid][64] clock64 / globaltimer stamps (profiling)
-  int dbg;                    // experiments (ABQ_TC_DBG): 2 MMA skips the A wait, 4 no UMMA,
+  int dbg;                    // experiments (abq_set_tuning "tc_dbg"): 2 MMA skips the A wait, 4 no UMMA,
                               // 8 no activation TMA, 16 no weight TMA, 32 no widening (results invalid)
   // stream-K (one token tile, grid < rowtiles x kblocks units): CTA b owns the
   // units [b T / G, (b + 1) T / G) of the (row-tile, k-block) sequence; a
@@ -886,13 +886,12 @@ int run_gemm_tc(const uint32_t* wtc, unsigned q, size_t n, size_t k, const uint8
   P.kblocks = static_cast<int>((k + kTcK - 1) / kTcK);
   P.e = e;
   P.trace = trace_buffer();
-  if (const char* env = std::getenv("ABQ_TC_DBG")) P.dbg = std::atoi(env);
-  const char* sk_env = std::getenv("ABQ_TC_SK");
-  // an explicit schedule wins; else ABQ_TC_SK (experiments); else the default
+  P.dbg = dec_tuning().tc_dbg;
+  // an explicit schedule (abq_set_gemm_schedule) wins; else the default
   const int sched = gemm_schedule();
   const bool sk_on = sched == ABQ_GEMM_STREAM_K ? true
                      : sched == ABQ_GEMM_CLASSIC ? false
-                     : (sk_env ? std::atoi(sk_env) != 0 : tc_stream_k_auto(P.rowtiles));
+                     : tc_stream_k_auto(P.rowtiles);
   if (sk_flags && sk_part && m <= 256 && sk_on) {
     P.sk = 1;
     P.sk_flags = sk_flags;

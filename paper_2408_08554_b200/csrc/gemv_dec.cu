@@ -11,23 +11,32 @@
 // q x 512 contiguous bytes, units ordered row-tile-major.  Same byte count as
 // the ABQP planes.
 //
-// Shape of the kernel (measurements: profiles/r01_microbench_burst.txt,
-// r01_microbench_sync.txt, r01_trace_dec_*.txt):
-//  * each CTA owns whole row-tiles (no cross-CTA reduction) and, first thing,
-//    asks L2 to prefetch its entire weight range with bulk prefetches
-//    (cp.async.bulk.prefetch.L2, evict-first): HBM streams at full rate while
-//    the CTA quantizes the activations, with no shared-memory or register
-//    cost; the weights are then read with 16-byte loads that hit L2;
-//  * 16 warps, one IMMA m16n8k32 (16 weight rows x 32 k x 8 tokens) stream
-//    per warp over units U0 + warp + 16 j, D units of loads in flight per warp;
-//  * power-of-two code slices (q = 1, 2, 4, 8) are fed to IMMA as raw masked
-//    bytes (w & (mask << w*f)): one ALU op per A register, the field's 2^(w f)
-//    scale divided out exactly at the row-tile flush; other q widen the slices
-//    to byte codes;
-//  * launches are programmatic-dependent: parameters and weights are fetched
-//    before griddepcontrol.wait, the activations after it.
+// Shape of the kernel:
+//  * one CTA per SM owning whole row-tiles (no cross-CTA reduction); its
+//    packed weights stream into a shared-memory ring by 1-D TMA bulk copies,
+//    as deep as the CTA's whole share when that fits (W4 LLaMA-7B up_proj:
+//    80 units = 160 KB), issued before the activations are awaited (weights are
+//    input-independent) -- the first `preslots` slots at once, the rest right
+//    after the activation loads so those do not queue behind the stream;
+//  * the epilogue's per-channel values (s_b, z_b, colsum_b) are fetched before
+//    the activations are awaited as well;
+//  * fused ReQuant prologue: one barrier for the per-token range, step / zero
+//    point in FP64 by every warp of the token (same inputs, same results, no
+//    broadcast), codes on the fp32 pipe with an exact FP64 tie path
+//    (quant_dev.cuh), written to shared memory in IMMA B-fragment order;
+//  * main loop: 16 warps, warp w takes units w, w + 16, ... of the CTA's range;
+//    per unit one IMMA m16n8k32 stream (16 weight rows x 32 k x 8 tokens):
+//    q in {1, 2, 4, 8} fed as raw masked bytes (one LOP3 per A register, the
+//    field's 2^(q f) scale divided out exactly when the unit is folded), other
+//    q widened to byte codes.  Two accumulator sets alternate between units so
+//    that a unit's fold overlaps the next unit's IMMAs; folded sums stay in
+//    registers while the row-tile repeats and go to shared memory (one atomic
+//    per row and token) when it changes;
+//  * launches are programmatic-dependent (PDL): griddepcontrol.launch_dependents
+//    first thing, griddepcontrol.wait right before the activations are read.
+// Profiling stamps (tools/trace_dec.py) exist only in the ABQ_TRACE build
+// (make TRACE=1 -> libabq_cuda_trace.so), not in the product library.
 #include <algorithm>
-#include <cstdlib>
 
 #include "common.cuh"
 #include "gemv_frag.cuh"
@@ -38,11 +47,12 @@ namespace abq_dev {
 constexpr int kDecWarps = 16;  // 4 per SM sub-partition, <= 128 registers each
 constexpr int kDecUPS = 8;     // units per ring slot = warps sharing a slot
 constexpr int kDecThreads = kDecWarps * 32;
+constexpr int kDecCtasPerSm = 1;
+constexpr int kDecXR = 4;      // fused ReQuant: 16-byte activation vectors per thread
 
 struct DecParams {
   const uint32_t* frag;
   int q, n, k, rowtiles, kblocks, m;
-  int U;  // rowtiles * kblocks
   // activations: fp16 rows quantized in the prologue, or codes + stats written
   // by act_quant_kernel (the PDL primary of this launch)
   const __half* x16;
@@ -54,21 +64,13 @@ struct DecParams {
   EpiParams e;
   unsigned long long* bad_word;  // non-finite input report (see run_gemv_dec)
   unsigned long long* bad_out;
-  unsigned long long* trace;     // optional [grid][64] stamps (tools/trace_dec.py)
-  int prefetch;                  // L2 bulk prefetch of the CTA's weights (default 0)
-  int slots;                     // TMA ring slots of kDecUPS units
-  int preslots;                  // ring slots issued before the activations are awaited
-  const unsigned char* next_frag;  // L2 prefetch hint: the next layer's weights (or null)
-  size_t next_bytes;
+  int slots;     // TMA ring slots of kDecUPS units
+  int preslots;  // ring slots issued before the activations are awaited
+  unsigned long long* trace;  // ABQ_TRACE build only: [grid][64] stamps
 };
 
-// named barrier over the consumer warps (the producer never joins)
-__device__ __forceinline__ void cta_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kDecWarps * 32) : "memory"); }
 __device__ __forceinline__ void mbar_init_n(uint64_t* bar, unsigned n) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(n));
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
 
 struct DecSmem {  // carve-up of the dynamic shared memory (host and device agree)
@@ -86,12 +88,7 @@ __host__ __device__ inline DecSmem dec_smem(int q, int slots, int mt, int kpad, 
   s.total = s.ccs + static_cast<size_t>(nlrt_max) * 16 * 8;
   return s;
 }
-__host__ __device__ inline int dec_nlrt_max(int rowtiles, int grid) { return (rowtiles + grid - 1) / grid + 1; }
-
-__device__ __forceinline__ void l2_prefetch_bulk(const void* p, uint32_t bytes, uint64_t pol) {
-  asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(p), "r"(bytes), "l"(pol)
-               : "memory");
-}
+__host__ __device__ inline int dec_nlrt_max(int rowtiles, int grid) { return (rowtiles + grid - 1) / grid; }
 
 // non-finite inputs of one thread's vectors -> atomicMax(~flat index) (the
 // smallest bad index wins); out of line: it only runs when one was seen
@@ -106,66 +103,92 @@ static __device__ __noinline__ void report_nonfinite_f16(const uint4* xr, int t,
   }
 }
 
+#ifdef ABQ_TRACE
+#define DEC_STAMP(slot, value)                  \
+  do {                                          \
+    if (P.trace && tid == 0) trace[slot] = (value); \
+  } while (0)
+#else
+#define DEC_STAMP(slot, value) \
+  do {                         \
+  } while (0)
+#endif
+
 template <int QT, int MT>
-__global__ void __launch_bounds__(kDecThreads, 1) gemv_dec_kernel(const __grid_constant__ DecParams Pc) {
+__global__ void __launch_bounds__(kDecThreads, kDecCtasPerSm) gemv_dec_kernel(const __grid_constant__ DecParams P) {
   constexpr int NW = kDecWarps, UPS = kDecUPS, NG = NW / UPS;
   constexpr int unit_bytes = QT * 512;
   constexpr int slot_bytes = UPS * unit_bytes;
   constexpr bool RAW = (QT & (QT - 1)) == 0;  // q in {1, 2, 4, 8}: raw masked fields
   constexpr int NF = RAW ? 8 / QT : 1;         // fields (scales) per byte lane
-  constexpr int NA = NF >= 2 ? NF : 2;         // accumulator sets (>= 2 independent chains)
+  constexpr int NA = NF >= 2 ? NF : 2;         // accumulators per set (>= 2 independent chains)
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ __align__(16) DecParams P;
-  __shared__ float r_lo[NW], r_hi[NW];
-  __shared__ int r_sum[NW];
+  __shared__ int r_lo[NW], r_hi[NW];
   __shared__ double s_sa[MT];
-  __shared__ long long s_za[MT], s_ra[MT];
-  __shared__ float s_inv[MT];
-  __shared__ long long s_wend;
+  __shared__ int s_za[MT];
+  __shared__ long long s_ra[MT];
+  __shared__ int r_sum[NW];  // per-warp code sums of the fused ReQuant
 
-  const unsigned long long t_entry = gtimer();  // profiling: true CTA start
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   asm volatile("griddepcontrol.launch_dependents;");
+#ifdef ABQ_TRACE
+  unsigned long long* trace = P.trace ? P.trace + 64 * blockIdx.x : nullptr;
+  if (trace && tid == 0) {
+    trace[8] = gtimer();
+    trace[0] = clock64();
+  }
+#endif
+  // the parameter block is read through the constant cache: touch every line
+  // before the weight stream starts (a miss behind it waits for the stream)
+  if (warp == NW - 1) warm_param_block(P, lane);
 
-  // ---- 0. this CTA's row-tiles [rt_first, rt_end) = units [U0, U1)
+  // ---- 0. this CTA's row-tiles [rt_first, rt_end) = units [U0, U0 + nu)
   const int G = gridDim.x;
-  const int rowtiles = Pc.rowtiles, kblocks = Pc.kblocks, S = Pc.slots;
+  const int rowtiles = P.rowtiles, kbl = P.kblocks, S = P.slots;
   // The rowtiles % G CTAs with one row-tile more come FIRST: the next layer's
   // CTAs are launched in blockIdx order onto SMs as this layer's CTAs retire,
-  // so its heavy CTAs land on the SMs freed first (by this layer's light ones)
-  // and the late starters are light.
+  // so its heavy CTAs land on the SMs freed first.
   const int rt_base = rowtiles / G, rt_heavy = rowtiles - rt_base * G;
-  auto rt_start = [&](int b) { return b < rt_heavy ? b * (rt_base + 1) : rt_heavy + b * rt_base; };
-  const int rt_first = rt_start(blockIdx.x);
-  const int rt_end = rt_start(blockIdx.x + 1);
-  const int U0 = rt_first * kblocks, U1 = rt_end * kblocks;
-  const int nlrt = rt_end - rt_first;
-  const int nsl = (U1 - U0 + UPS - 1) / UPS;
-  const int kpad = kblocks * kKBlock;
+  const int rt_first = blockIdx.x < rt_heavy ? blockIdx.x * (rt_base + 1) : rt_heavy + blockIdx.x * rt_base;
+  const int nlrt = rt_base + (static_cast<int>(blockIdx.x) < rt_heavy ? 1 : 0);
+  const int U0 = rt_first * kbl, nu = nlrt * kbl;
+  const int nsl = (nu + UPS - 1) / UPS;
+  const int kpad = kbl * kKBlock;
   const DecSmem L = dec_smem(QT, S, MT, kpad, dec_nlrt_max(rowtiles, G));
   unsigned char* ring = smem + L.ring;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bars);
   unsigned* relcnt = reinterpret_cast<unsigned*>(full + S);  // warps done with each slot
+  uint32_t* act = reinterpret_cast<uint32_t*>(smem + L.act);
+  uint32_t* accs = reinterpret_cast<uint32_t*>(smem + L.accs);
+  double* c_sb = reinterpret_cast<double*>(smem + L.csb);
+  long long* c_zb = reinterpret_cast<long long*>(smem + L.czb);
+  long long* c_cs = reinterpret_cast<long long*>(smem + L.ccs);
 
-  // ---- ring set-up by thread 0: full barriers, then (after the CTA barrier
-  // below) the L2 bulk prefetch of the CTA's weights and of the next layer's,
-  // and the first S slots.  Later slots are refilled by the last warp to
-  // release a slot (release() below): no producer warp, so 16 warps x 128
-  // registers fit the SM.
-  const unsigned char* wsrc = reinterpret_cast<const unsigned char*>(Pc.frag) + static_cast<size_t>(U0) * unit_bytes;
+  // epilogue values of this CTA's channels (input-independent): requested into
+  // registers before the weight stream is started, so they do not queue behind
+  // it; stored to shared memory only after the main loop
+  const bool dequant = P.e.mode != EPI_ACC_I32 && P.e.mode != EPI_ACC_I64;
+  const int pj = rt_first * kRowTile + tid;
+  const bool has_p = dequant && tid < nlrt * 16 && pj < P.n;
+  double p_sb = 0.0;
+  int p_zb = 0;
+  long long p_cs = 0;
+  if (has_p) {
+    p_sb = P.e.s_b[static_cast<size_t>(pj) * P.e.sb_stride];
+    p_zb = P.e.z_b[static_cast<size_t>(pj) * P.e.zb_stride];
+    p_cs = P.e.colsum_b[pj];
+  }
+  const unsigned char* wsrc = reinterpret_cast<const unsigned char*>(P.frag) + static_cast<size_t>(U0) * unit_bytes;
   const uint64_t pol = l2_evict_first_policy();
   auto issue_slot = [&](int i, int sl) {  // thread-level: TMA of slot index i into ring slot sl
-    const int nu = min(UPS, U1 - U0 - i * UPS);
-    const uint32_t bytes = static_cast<uint32_t>(nu * unit_bytes);
+    const int n_units = min(UPS, nu - i * UPS);
+    const uint32_t bytes = static_cast<uint32_t>(n_units * unit_bytes);
     mbar_expect_tx(&full[sl], bytes);
     tma_bulk_g2s_hint(ring + static_cast<size_t>(sl) * slot_bytes, wsrc + static_cast<size_t>(i) * slot_bytes, bytes,
                       &full[sl], pol);
   };
-  // Set-up spread over lanes (one thread doing it serially took ~2 us, all on
-  // the launch's critical path): warp 0 lane s initialises barrier s and, once
-  // the initialisation is fenced, issues slot s; warp 1's lanes issue the L2
-  // bulk prefetches (the CTA's range beyond the ring, then its share of the
-  // successor layer), one 32 KB chunk per lane per round.
+  // ---- 1. ring: warp 0 lane s initialises barrier s and, once the
+  // initialisation is fenced, issues slot s (for s < preslots)
   if (warp == 0) {
     if (lane < S) {
       mbar_init_n(&full[lane], 1);
@@ -174,91 +197,28 @@ __global__ void __launch_bounds__(kDecThreads, 1) gemv_dec_kernel(const __grid_c
     __syncwarp();
     if (lane == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncwarp();
-    for (int i = lane; i < min(S, Pc.preslots) && i < nsl; i += 32) issue_slot(i, i);
-  } else if (warp == 1 && Pc.prefetch) {
-    // (the ring slots issued after the activation load are prefetched too, so
-    // their copies hit L2)
-    const size_t total = static_cast<size_t>(U1 - U0) * unit_bytes;
-    for (size_t off = static_cast<size_t>(min(S, Pc.preslots)) * slot_bytes + static_cast<size_t>(lane) * 32768;
-         off < total;
-         off += 32u * 32768)
-      l2_prefetch_bulk(wsrc + off, static_cast<uint32_t>(total - off < 32768 ? total - off : 32768), pol);
-    // the next layer's weights (input-independent) stream into L2 behind ours
-    if (Pc.next_frag) {
-      const size_t nb = Pc.next_bytes, lo = (nb * blockIdx.x / G) & ~size_t(15),
-                   hi = (nb * (blockIdx.x + 1) / G) & ~size_t(15);
-      for (size_t off = lo + static_cast<size_t>(lane) * 32768; off < hi; off += 32u * 32768)
-        l2_prefetch_bulk(Pc.next_frag + off, static_cast<uint32_t>(hi - off < 32768 ? hi - off : 32768), pol);
-    }
+    for (int i = lane; i < min(S, P.preslots) && i < nsl; i += 32) issue_slot(i, i);
   }
-
-  // ======================= consumer warps ====================================
-  // this thread's epilogue channel parameters (<= 1 channel per thread here;
-  // more are loaded below), requested first
-  const bool dequant = Pc.e.mode != EPI_ACC_I32 && Pc.e.mode != EPI_ACC_I64;
-  const int pj = rt_first * kRowTile + tid;
-  const bool has_p = dequant && tid < nlrt * 16 && pj < Pc.n;
-  double p_sb = 0.0;
-  int p_zb = 0;  // int32 as loaded: a conversion here would wait for the load before the barrier
-  long long p_cs = 0;
-  if (has_p) {
-    p_sb = Pc.e.s_b[static_cast<size_t>(pj) * Pc.e.sb_stride];
-    p_zb = Pc.e.z_b[static_cast<size_t>(pj) * Pc.e.zb_stride];
-    p_cs = Pc.e.colsum_b[pj];
-  }
-
-  // ---- 1. parameter block to shared memory (all threads at once; read lazily
-  // from the constant bank, every first touch of a line would be a separate
-  // round trip), epilogue parameters of this CTA's channels
-  for (int i = tid; i < static_cast<int>(sizeof(DecParams) / 4); i += NW * 32)
-    reinterpret_cast<uint32_t*>(&P)[i] = reinterpret_cast<const uint32_t*>(&Pc)[i];
-  __syncthreads();  // parameter block and barrier initialisation visible
-  unsigned long long* trace = P.trace ? P.trace + 64 * blockIdx.x : nullptr;
-  if (trace && tid == 0) {
-    trace[0] = clock64();
-    trace[8] = gtimer();
-    trace[12] = t_entry;
-    s_wend = 0;
-  }
-  uint32_t* act = reinterpret_cast<uint32_t*>(smem + L.act);
-  uint32_t* accs = reinterpret_cast<uint32_t*>(smem + L.accs);
-  double* c_sb = reinterpret_cast<double*>(smem + L.csb);
-  int* c_zb = reinterpret_cast<int*>(smem + L.czb);
-  long long* c_cs = reinterpret_cast<long long*>(smem + L.ccs);
+  // zeroed row-tile sums, zero codes past K
+  for (int idx = tid; idx < nlrt * 16 * MT; idx += kDecThreads) accs[idx] = 0;
   const int tok_n = min(MT, P.m);
-  constexpr int kCT = NW * 32;
-  if (has_p) {
-    c_sb[tid] = p_sb;
-    c_zb[tid] = p_zb;
-    c_cs[tid] = p_cs;
-  }
-  for (int idx = tid + kCT; dequant && idx < nlrt * 16; idx += kCT) {
-    const int j = rt_first * kRowTile + idx;
-    if (j < P.n) {
-      c_sb[idx] = P.e.s_b[static_cast<size_t>(j) * P.e.sb_stride];
-      c_zb[idx] = P.e.z_b[static_cast<size_t>(j) * P.e.zb_stride];
-      c_cs[idx] = P.e.colsum_b[j];
-    }
-  }
-  for (int idx = tid; idx < nlrt * 16 * MT; idx += kCT) accs[idx] = 0;
-  if (P.x16) {  // codes past K (to the k-block multiple) are zero
+  if (P.x16) {
     const int k4 = P.k >> 2, ntail = (kpad >> 2) - k4;
-    for (int idx = tid; idx < ntail * MT; idx += kCT) act[act_frag_index(k4 + idx / MT, idx % MT, MT)] = 0u;
+    for (int idx = tid; idx < ntail * MT; idx += kDecThreads) act[act_frag_index(k4 + idx / MT, idx % MT, MT)] = 0u;
   }
+  __syncthreads();  // barrier initialisation and the zeroed state visible
+  DEC_STAMP(1, clock64());
+
   // ---- 2. the activations, which the previous kernel may still be producing
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  if (trace && tid == 0) trace[4] = clock64();
-
+  DEC_STAMP(2, clock64());
   if (P.x16) {
-    // Fused ReQuant, per token, fp16 rows (K % 8 == 0, K <= 32 * TPT: the
-    // host routes longer rows through act_quant_kernel).  GT warps per token;
-    // each thread loads its (<= XR) 16-byte vectors of the row in one batch.
-    // One CTA barrier for the range; every warp then derives step / zero point
-    // itself (no second barrier), codes go to shared memory and the code sum to
-    // a shared atomic, and the barrier before the main loop publishes both.
+    // Fused ReQuant, per token, fp16 rows (K % 8 == 0, K <= 32 * TPT: the host
+    // routes longer rows through act_quant_kernel).  GT warps per token; each
+    // thread loads its (<= XR) 16-byte vectors of the row in one batch.
     constexpr int GT = NW / MT;  // MT is a power of two <= NW
     constexpr int TPT = GT * 32;
-    constexpr int XR = 4;
+    constexpr int XR = kDecXR;
     const int t = warp / GT;
     const int l = (warp % GT) * 32 + lane;
     const int nvec = P.k >> 3;
@@ -270,12 +230,11 @@ __global__ void __launch_bounds__(kDecThreads, 1) gemv_dec_kernel(const __grid_c
       const int v = l + r * TPT;
       xv[r] = active && v < nvec ? __ldg(xr + v) : make_uint4(0u, 0u, 0u, 0u);
     }
-    // the rest of the ring only now: shared-memory-bound TMA traffic into this
-    // SM ahead of the activation loads delayed them (~0.2 us on the critical path)
+    // the rest of the ring only now, behind the activation loads
     if (warp == 0)
-      for (int i = P.preslots + lane; i < P.slots && i < nsl; i += 32) issue_slot(i, i);
+      for (int i = P.preslots + lane; i < S && i < nsl; i += 32) issue_slot(i, i);
     // min / max in the order-preserving integer image of fp32 (exact for fp16
-    // inputs): one REDUX per warp instead of a shuffle tree
+    // inputs): one REDUX per warp
     auto ord = [](float f) {
       const int b = __float_as_int(f);
       return b >= 0 ? b : b ^ 0x7FFFFFFF;
@@ -302,35 +261,30 @@ __global__ void __launch_bounds__(kDecThreads, 1) gemv_dec_kernel(const __grid_c
     lo = __reduce_min_sync(0xffffffffu, lo);
     hi = __reduce_max_sync(0xffffffffu, hi);
     if (lane == 0) {
-      r_lo[warp] = __int_as_float(lo);  // raw bits: decoded below
-      r_hi[warp] = __int_as_float(hi);
-      if (warp % GT == 0) s_ra[t] = 0;
+      r_lo[warp] = lo;
+      r_hi[warp] = hi;
     }
-    cta_sync();
-    if (trace && tid == 0) trace[5] = clock64();
-    int rsum = 0;
+    __syncthreads();
+    DEC_STAMP(3, clock64());
     if (active) {
       const int base = warp - warp % GT;  // first warp of this token
-      int l2 = lane < GT ? __float_as_int(r_lo[base + lane]) : 0x7FFFFFFF;
-      int h2 = lane < GT ? __float_as_int(r_hi[base + lane]) : static_cast<int>(0x80000000u);
+      int l2 = lane < GT ? r_lo[base + lane] : 0x7FFFFFFF;
+      int h2 = lane < GT ? r_hi[base + lane] : static_cast<int>(0x80000000u);
       l2 = __reduce_min_sync(0xffffffffu, l2);
       h2 = __reduce_max_sync(0xffffffffu, h2);
-      // step / zero point in FP64 (quantizer.hpp:169-201) by lane 0 of every
-      // warp of the token (identical inputs, identical results), broadcast
+      // step / zero point in FP64 (quantizer.hpp:169-201), every lane (same
+      // inputs, same results: no divergence, no broadcast)
       double step = 0.0;
       int z = 0;
       float inv32 = 0.0f;
-      if (lane < 2) group_params(P.qp, unord(l2), unord(h2), &step, &z);
-      if (lane == 1) inv32 = f32_reciprocal(step);  // lane 0 finishes z meanwhile
-      step = __shfl_sync(0xffffffffu, step, 0);
-      z = __shfl_sync(0xffffffffu, z, 0);
-      inv32 = __shfl_sync(0xffffffffu, inv32, 1);
+      group_params_fast(P.qp, unord(l2), unord(h2), &step, &z, &inv32);
       if (warp == base && lane == 0) {
         s_sa[t] = step;
         s_za[t] = z;
       }
-      if (trace && tid == 0) trace[6] = clock64();
+      DEC_STAMP(4, clock64());
       const int topi = static_cast<int>(P.qp.levels - 1);
+      int rsum = 0;
 #pragma unroll
       for (int r = 0; r < XR; ++r) {
         const int v = l + r * TPT;
@@ -341,7 +295,9 @@ __global__ void __launch_bounds__(kDecThreads, 1) gemv_dec_kernel(const __grid_c
         act[act_frag_index(2 * v + 1, t, MT)] = w1;
       }
       rsum = __reduce_add_sync(0xffffffffu, rsum);  // < 2^31: <= 255 * 65536
-      if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&s_ra[t]), static_cast<unsigned long long>(rsum));
+      if (lane == 0) r_sum[warp] = rsum;
+    } else if (lane == 0) {
+      r_sum[warp] = 0;
     }
     if (report && tid == 0) {
       const unsigned long long w = atomicExch(P.bad_word, 0ull);
@@ -353,7 +309,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) gemv_dec_kernel(const __grid_c
     const uint4* src = reinterpret_cast<const uint4*>(P.act_frag);
     uint4* dst = reinterpret_cast<uint4*>(act);
     const int nv = MT * kpad / 16;  // act_quant_kernel zero-fills codes past K
-    for (int idx = tid; idx < nv; idx += kCT) dst[idx] = __ldcg(src + idx);
+    for (int idx = tid; idx < nv; idx += kDecThreads) dst[idx] = __ldcg(src + idx);
     if (tid < tok_n) {
       s_sa[tid] = P.s_a[tid];
       s_za[tid] = P.z_a[tid];
@@ -365,30 +321,26 @@ __global__ void __launch_bounds__(kDecThreads, 1) gemv_dec_kernel(const __grid_c
       *P.bad_word = 0ull;
     }
   }
-  cta_sync();
-  if (trace && tid == 0) trace[1] = clock64();
+  __syncthreads();
+  DEC_STAMP(5, clock64());
 
-  // ---- 3. main loop over the TMA ring.
-  // Warp group grp = warp / UPS takes the slots i = grp (mod NG), warp % UPS
-  // its unit of each.  Per unit: the weights come from shared memory into one
-  // of two register buffers (the next unit's are requested before this
-  // unit's IMMAs issue), the IMMAs accumulate into one of two accumulator
-  // sets, and the other set -- the previous unit's -- is folded into the
-  // row-tile sums AFTER these IMMAs are issued, so consecutive units' IMMA
-  // chains overlap instead of serialising on the flush.
+  // ---- 3. main loop.  Local unit l = warp + NW j lives in ring slot index
+  // l / UPS = grp + NG j (group grp = warp / UPS takes the slots = grp mod NG),
+  // at position warp % UPS within the slot.
   const int g = lane >> 2, tig = lane & 3;
-  const uint32_t act_lane = smem_addr(act) + ((g * 4 + tig) * 8);  // B-fragment word pair of (g, tig)
   const bool has_b = g < MT;
+  const uint32_t act_lane = smem_addr(act) + ((g * 4 + tig) * 8);  // B-fragment word pair of (g, tig)
   uint2 b[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) b[c] = make_uint2(0u, 0u);
   int cur_kb = -1;
   auto load_b = [&](int k_b) {  // B fragments of a k-block (kept while it repeats)
     cur_kb = k_b;
+    if (!has_b) return;
     const uint32_t ab = act_lane + k_b * (8 * MT * 4 * 8);
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      b[c] = make_uint2(0u, 0u);
-      if (has_b) asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(b[c].x), "=r"(b[c].y) : "r"(ab + c * MT * 32));
-    }
+    for (int c = 0; c < 8; ++c)
+      asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(b[c].x), "=r"(b[c].y) : "r"(ab + c * MT * 32));
   };
   auto mma_unit = [&](int (&acc)[NA][4], const uint4 (&w)[QT]) {
     if constexpr (RAW) {
@@ -412,12 +364,29 @@ __global__ void __launch_bounds__(kDecThreads, 1) gemv_dec_kernel(const __grid_c
       }
     }
   };
-  auto flush_set = [&](int (&acc)[NA][4], int r_t) {
-    const int lrt = r_t - rt_first;
+  // running sums of the current row-tile (this warp's k-blocks), fields folded
+  uint32_t tot[4] = {0u, 0u, 0u, 0u};
+  int tot_rt = -1;
+  auto flush_tot = [&]() {
+    if (tot_rt < 0) return;
+    const int lrt = tot_rt - rt_first;
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
-      // field f holds 2^(QT f) * its partial sum, exactly (the true row-tile
-      // sum is < 2^32 for K <= 65536, and so is every scaled field sum)
+      const int row = g + 8 * (r >> 1), tok = 2 * tig + (r & 1);
+      if (tok < tok_n) atomicAdd(&accs[(lrt * 16 + row) * MT + tok], tot[r]);
+      tot[r] = 0u;
+    }
+  };
+  // fold a unit's accumulator set into the row-tile sums.  Field f holds
+  // 2^(QT f) * its partial sum exactly (every per-unit sum is < 2^31; the
+  // row-tile sum < 2^32 for K <= 65536); the fields are divided out exactly.
+  auto fold = [&](int (&acc)[NA][4], int r_t) {
+    if (r_t != tot_rt) {
+      flush_tot();
+      tot_rt = r_t;
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
       uint32_t v = 0;
 #pragma unroll
       for (int f = 0; f < NA; ++f) {
@@ -425,18 +394,12 @@ __global__ void __launch_bounds__(kDecThreads, 1) gemv_dec_kernel(const __grid_c
         v += static_cast<uint32_t>(acc[f][r]) >> sh;
         acc[f][r] = 0;
       }
-      const int row = g + 8 * (r >> 1), tok = 2 * tig + (r & 1);
-      if (tok < tok_n) atomicAdd(&accs[(lrt * 16 + row) * MT + tok], v);
+      tot[r] += v;
     }
   };
   {
-    // loop-invariant scalars re-read from the shared copy of the parameter
-    // block: left to ptxas they are re-fetched from the constant bank (LDC)
-    // inside the loop
-    const int S_ = *reinterpret_cast<volatile int*>(&P.slots);
-    const int kbl = *reinterpret_cast<volatile int*>(&P.kblocks);
-    const int grp = warp / UPS, off = grp * UPS + warp % UPS;
-    const int nw = U1 - U0 > off ? (U1 - U0 - off + NW - 1) / NW : 0;  // this warp's units
+    const int grp = warp / UPS;
+    const int nw = nu > warp ? (nu - warp + NW - 1) / NW : 0;  // this warp's units
     const uint32_t ring_lane = smem_addr(ring) + (warp % UPS) * unit_bytes + lane * 16;
     auto lds_unit = [&](int sl, uint4 (&w)[QT]) {
       const uint32_t a = ring_lane + sl * slot_bytes;
@@ -445,43 +408,32 @@ __global__ void __launch_bounds__(kDecThreads, 1) gemv_dec_kernel(const __grid_c
         asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
                      : "=r"(w[t].x), "=r"(w[t].y), "=r"(w[t].z), "=r"(w[t].w) : "r"(a + t * 512));
     };
-    long long t_wait = 0;  // profiling (trace mode only)
-    auto wait_full = [&](int sl, uint32_t p) {
-      if (trace) {
-        const long long t0 = clock64();
-        mbar_wait_parity(&full[sl], p);
-        t_wait += clock64() - t0;
-      } else {
-        mbar_wait_parity(&full[sl], p);
-      }
-    };
     // the last of the UPS warps done with ring slot sl refills it with slot
-    // index i + S (its data is in registers: the IMMAs reading it have issued)
-    const bool refill = nsl > S_;  // else every slot was loaded once, at kernel start
+    // index i + S (its data is in registers: the loads have returned)
+    const bool refill = nsl > S;  // else every slot was loaded once, at kernel start
     auto release = [&](int sl, int i) {
       if (!refill) return;
       __syncwarp();
-      if (lane == 0 && i + S_ < nsl && atomicAdd(&relcnt[sl], 1u) == UPS - 1) {
+      if (lane == 0 && i + S < nsl && atomicAdd(&relcnt[sl], 1u) == UPS - 1) {
         relcnt[sl] = 0;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue_slot(i + S_, sl);
+        issue_slot(i + S, sl);
       }
     };
-    // fetch cursor: slot / parity / row-tile / k-block of the next unit to fetch
-    int fs = grp, fi = grp;  // ring slot / slot index of the next fetch (NG <= S)
+    int accA[NA][4], accB[NA][4];
+#pragma unroll
+    for (int f = 0; f < NA; ++f)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) accA[f][r] = accB[f][r] = 0;
+    // fetch cursor (slot index, ring slot, parity, row-tile, k-block)
+    int fi = grp, fs = grp;
     uint32_t fph = 0;
-    int frt = (U0 + off) / kbl, fkb = U0 + off - frt * kbl;
-    auto fetch = [&](uint4 (&w)[QT], int& sl, int& idx, int& r_t, int& k_b) {
-      sl = fs;
-      idx = fi;
+    int frt = (U0 + warp) / kbl, fkb = U0 + warp - frt * kbl;
+    auto advance = [&]() {
       fi += NG;
-      r_t = frt;
-      k_b = fkb;
-      wait_full(fs, fph);
-      lds_unit(fs, w);
       fs += NG;
-      if (fs >= S_) {
-        fs -= S_;
+      if (fs >= S) {
+        fs -= S;
         fph ^= 1u;
       }
       fkb += NW;
@@ -490,122 +442,64 @@ __global__ void __launch_bounds__(kDecThreads, 1) gemv_dec_kernel(const __grid_c
         ++frt;
       }
     };
-    // Fast path, layers with 16 k-blocks (K in (3840, 4096]: LLaMA q/k/v/o/
-    // gate/up): warp w owns k-block w of every row-tile of the CTA, so its j-th
-    // unit is row-tile rt_first + j.  Each row-tile gets its own accumulator set
-    // in registers (fully unrolled, static indices): the IMMA chains of all
-    // units are independent and nothing is flushed until the loop is done.
-    constexpr int RTMAX = (QT == 4 || QT == 8) ? 6 : (QT == 2 ? 3 : 0);
-    bool fast_done = false;
-    if constexpr (RTMAX > 0 && NG == 2) {
-      if (kbl == NW && nw <= RTMAX) {
-        constexpr bool DB = QT <= 4;  // two register buffers where they fit
-        if (nw > 0 && cur_kb != warp) load_b(warp);
-        int acc[RTMAX][NA][4];
-#pragma unroll
-        for (int j = 0; j < RTMAX; ++j)
-#pragma unroll
-          for (int f = 0; f < NA; ++f)
-#pragma unroll
-            for (int r = 0; r < 4; ++r) acc[j][f][r] = 0;
-        uint4 wbuf[DB ? 2 : 1][QT];
-        int s0 = grp;  // ring slot of the warp's j-th unit (slot index grp + 2 j)
-        uint32_t p0 = 0;
-        if (DB && nw > 0) {
-          wait_full(s0, p0);
-          lds_unit(s0, wbuf[0]);
-        }
-#pragma unroll
-        for (int j = 0; j < RTMAX; ++j) {
-          if (j < nw) {
-            int s1 = s0 + NG;
-            uint32_t p1 = p0;
-            if (s1 >= S_) {
-              s1 -= S_;
-              p1 ^= 1u;
-            }
-            if constexpr (DB) {
-              if (j + 1 < nw) {
-                wait_full(s1, p1);
-                lds_unit(s1, wbuf[(j + 1) & 1]);
-              }
-            } else {
-              wait_full(s0, p0);
-              lds_unit(s0, wbuf[0]);
-            }
-            mma_unit(acc[j], wbuf[DB ? (j & 1) : 0]);
-            release(s0, grp + NG * j);
-            s0 = s1;
-            p0 = p1;
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < RTMAX; ++j)
-          if (j < nw) flush_set(acc[j], rt_first + j);
-        fast_done = true;
-      }
+    uint4 w[QT];
+    int rtA = -1, rtB = -1;
+    for (int j = 0; j < nw; j += 2) {
+      // unit j -> set A (fold set B = unit j - 1 behind its IMMAs)
+      mbar_wait_parity(&full[fs], fph);
+      lds_unit(fs, w);
+      const int slA = fs, iA = fi, kbA = fkb;
+      rtA = frt;
+      advance();
+      if (kbA != cur_kb) load_b(kbA);
+      mma_unit(accA, w);
+      release(slA, iA);
+      if (j > 0) fold(accB, rtB);
+      if (j + 1 >= nw) break;
+      // unit j + 1 -> set B (fold set A behind its IMMAs)
+      mbar_wait_parity(&full[fs], fph);
+      lds_unit(fs, w);
+      const int slB = fs, iB = fi, kbB = fkb;
+      rtB = frt;
+      advance();
+      if (kbB != cur_kb) load_b(kbB);
+      mma_unit(accB, w);
+      release(slB, iB);
+      fold(accA, rtA);
+      rtA = -1;
     }
-    if (trace && lane == 0) trace[24 + warp] = t_wait;
-    int accA[NA][4], accB[NA][4];
-#pragma unroll
-    for (int f = 0; f < NA; ++f)
-#pragma unroll
-      for (int r = 0; r < 4; ++r) accA[f][r] = accB[f][r] = 0;
-    if (fast_done) {
-    } else if constexpr (QT <= 6) {
-      uint4 wA[QT], wB[QT];
-      int sA = 0, iA = 0, rtA = 0, kbA = 0, sB = 0, iB = 0, rtB = 0, kbB = 0;
-      if (nw > 0) fetch(wA, sA, iA, rtA, kbA);
-      for (int j = 0; j < nw; j += 2) {
-        // unit j (buffer A, accumulators A); unit j + 1 prefetched into B
-        const int rtB_prev = rtB;  // unit j - 1 (j > 0)
-        if (j + 1 < nw) fetch(wB, sB, iB, rtB, kbB);
-        if (kbA != cur_kb) load_b(kbA);
-        mma_unit(accA, wA);
-        if (j > 0) flush_set(accB, rtB_prev);
-        release(sA, iA);
-        if (j + 1 >= nw) {
-          flush_set(accA, rtA);
-          break;
-        }
-        // unit j + 1 (buffer B, accumulators B); unit j + 2 prefetched into A
-        const int rtA_done = rtA;
-        if (j + 2 < nw) fetch(wA, sA, iA, rtA, kbA);
-        if (kbB != cur_kb) load_b(kbB);
-        mma_unit(accB, wB);
-        flush_set(accA, rtA_done);
-        release(sB, iB);
-        if (j + 2 >= nw) flush_set(accB, rtB);
-      }
-    } else {  // one register buffer (two would spill at this register budget)
-      uint4 wA[QT];
-      int sA = 0, iA = 0, rtA = 0, kbA = 0, rtP = -1;
-      for (int j = 0; j < nw; ++j) {
-        fetch(wA, sA, iA, rtA, kbA);
-        if (kbA != cur_kb) load_b(kbA);
-        if (j & 1) {
-          mma_unit(accB, wA);
-          flush_set(accA, rtP);
-        } else {
-          mma_unit(accA, wA);
-          if (j > 0) flush_set(accB, rtP);
-        }
-        release(sA, iA);
-        rtP = rtA;
-      }
-      if (nw > 0) {
-        if ((nw - 1) & 1) flush_set(accB, rtP);
-        else flush_set(accA, rtP);
-      }
+    if (rtA >= 0) fold(accA, rtA);
+    else if (nw > 0 && (nw & 1) == 0) fold(accB, rtB);
+    flush_tot();
+  }
+  // epilogue values to shared memory (requested at kernel start), token code
+  // sums of the fused ReQuant from the per-warp partials
+  if (has_p) {
+    c_sb[tid] = p_sb;
+    c_zb[tid] = p_zb;
+    c_cs[tid] = p_cs;
+  }
+  for (int idx = tid + kDecThreads; dequant && idx < nlrt * 16; idx += kDecThreads) {
+    const int j = rt_first * kRowTile + idx;
+    if (j < P.n) {
+      c_sb[idx] = P.e.s_b[static_cast<size_t>(j) * P.e.sb_stride];
+      c_zb[idx] = P.e.z_b[static_cast<size_t>(j) * P.e.zb_stride];
+      c_cs[idx] = P.e.colsum_b[j];
     }
   }
-  if (trace && lane == 0) atomicMax(&s_wend, static_cast<long long>(clock64()));
-  cta_sync();
-  if (trace && tid == 0) trace[2] = s_wend;
+  if (P.x16 && tid < tok_n) {
+    constexpr int GT = NW / MT;
+    long long s = 0;
+#pragma unroll
+    for (int w2 = 0; w2 < GT; ++w2) s += r_sum[tid * GT + w2];
+    s_ra[tid] = s;
+  }
+  __syncthreads();
+  DEC_STAMP(6, clock64());
 
   // ---- 4. epilogue: zero-point correction + dequant of this CTA's channels
   const EpiParams& E = P.e;
-  for (int idx = tid; idx < nlrt * 16 * MT; idx += kCT) {
+  for (int idx = tid; idx < nlrt * 16 * MT; idx += kDecThreads) {
     const int i = idx & (MT - 1), rc = idx / MT, lrt = rc >> 4, row = rc & 15;
     const int j = (rt_first + lrt) * kRowTile + row;
     if (i >= tok_n || j >= P.n) continue;
@@ -614,7 +508,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) gemv_dec_kernel(const __grid_c
       epi_store_v(E, i, j, a, 0.0, 0, 0);
       continue;
     }
-    const long long za = s_za[i], zb = static_cast<long long>(c_zb[rc]);
+    const long long za = s_za[i], zb = c_zb[rc];
     const long long corr = a - za * c_cs[rc] - zb * s_ra[i] + E.k * za * zb;
     const long long o = static_cast<long long>(i) * E.ldo + j;
     if (E.mode == EPI_CORR_I64) {
@@ -629,10 +523,12 @@ __global__ void __launch_bounds__(kDecThreads, 1) gemv_dec_kernel(const __grid_c
     else
       static_cast<float*>(E.out)[o] = __double2float_rn(y);
   }
+#ifdef ABQ_TRACE
   if (trace && tid == 0) {
-    trace[3] = clock64();
+    trace[7] = clock64();
     trace[9] = gtimer();
   }
+#endif
 }
 
 // ============================================================================
@@ -640,11 +536,18 @@ __global__ void __launch_bounds__(kDecThreads, 1) gemv_dec_kernel(const __grid_c
 // ============================================================================
 unsigned long long*& trace_buffer();
 
+DecTuning& dec_tuning() {
+  static DecTuning t;
+  return t;
+}
+
 template <int QT, int MT>
 static int launch_dec2(const DecParams& P, int grid, size_t smem, bool pdl, cudaStream_t st) {
   auto kern = gemv_dec_kernel<QT, MT>;
   if (smem > 220 * 1024) return fail(ABQ_ERR_VALUE, "gemv_dec: shared memory plan too large (%zu B)", smem);
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (err == cudaSuccess)
+    err = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   if (err != cudaSuccess) return fail(ABQ_ERR_CUDA, "gemv_dec: smem attribute: %s", cudaGetErrorString(err));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
@@ -680,17 +583,47 @@ int run_act_quant(const void* x, int x_dtype, size_t m, size_t k, int mt, const 
                   uint32_t* out, int row_ld, double* s_a, int32_t* z_a, long long* rowsum,
                   unsigned long long* bad_word, cudaStream_t st);
 
+static int dec_mt(size_t m) { return m <= 1 ? 1 : m <= 2 ? 2 : m <= 4 ? 4 : 8; }
+static const size_t kDecSmemBudget = 212 * 1024;
+
+// ring slots for a layer: as deep as the CTA's whole weight share when that
+// fits in shared memory (then every TMA copy is issued at kernel start and no
+// refill latency is exposed), else as many as fit (>= 2)
+static int dec_slots(unsigned q, size_t n, size_t k, int mt, int grid) {
+  const int rowtiles = static_cast<int>((n + kRowTile - 1) / kRowTile);
+  const int kblocks = static_cast<int>((k + kKBlock - 1) / kKBlock);
+  const int nl = dec_nlrt_max(rowtiles, grid);
+  const int min_slots = 2;
+  int slots = std::max(min_slots, std::min(32, (nl * kblocks + kDecUPS - 1) / kDecUPS));
+  if (dec_tuning().ring_kb > 0)
+    slots = std::max(min_slots, static_cast<int>(dec_tuning().ring_kb * 1024 / (size_t(kDecUPS) * q * 512)));
+  while (slots > min_slots && dec_smem(q, slots, mt, kblocks * kKBlock, nl).total > kDecSmemBudget) --slots;
+  return slots;
+}
+
+// the decode GEMV handles this layer (activation codes of mt tokens plus a
+// minimal 2-slot ring and the per-channel epilogue values fit shared memory)
+bool dec_supported(unsigned q, size_t n, size_t k, size_t m) {
+  if (m < 1 || m > 8 || n == 0 || k == 0 || k > 65536 || q < 1 || q > 8) return false;
+  const int mt = dec_mt(m);
+  const int rowtiles = static_cast<int>((n + kRowTile - 1) / kRowTile);
+  const int grid = std::min(num_sms(), rowtiles);
+  const int kblocks = static_cast<int>((k + kKBlock - 1) / kKBlock);
+  return dec_smem(q, 2, mt, kblocks * kKBlock, dec_nlrt_max(rowtiles, grid)).total <=
+         kDecSmemBudget;
+}
+
 // Serving decode path (m <= 8).  `ws` = imma_ws_bytes(n, k) of zero-filled
-// device memory (left zeroed): stream-K accumulators, counters, activation
-// codes, stats, the non-finite report word.  fp16 per-token activations with
-// K % 8 == 0 are quantized inside the GEMV (one launch); anything else goes
-// through act_quant_kernel first, with this kernel as its PDL secondary.
-// Every launch is itself PDL-enabled so consecutive layers overlap.
+// device memory (left zeroed): activation codes, stats, the non-finite report
+// word.  fp16 per-token activations with K % 8 == 0 are quantized inside the
+// GEMV (one launch); anything else goes through act_quant_kernel first, with
+// this kernel as its PDL secondary.  Every launch is itself PDL-enabled so
+// consecutive layers overlap.
 int run_gemv_dec(const uint32_t* frag, unsigned q, size_t n, size_t k, size_t m, const void* x, int x_dtype,
                  const QuantParams& qp, const EpiParams& e, void* ws, unsigned long long* bad_out,
-                 cudaStream_t st, const void* next_frag, size_t next_bytes) {
+                 cudaStream_t st) {
   if (m == 0 || n == 0) return ABQ_OK;
-  if (m > 8) return fail(ABQ_ERR_VALUE, "gemv_dec: m <= 8 only");
+  if (!dec_supported(q, n, k, m)) return fail(ABQ_ERR_VALUE, "gemv_dec: layer shape not supported");
   DecParams P{};
   P.frag = frag;
   P.q = static_cast<int>(q);
@@ -699,19 +632,10 @@ int run_gemv_dec(const uint32_t* frag, unsigned q, size_t n, size_t k, size_t m,
   P.rowtiles = static_cast<int>((n + kRowTile - 1) / kRowTile);
   P.kblocks = static_cast<int>((k + kKBlock - 1) / kKBlock);
   P.m = static_cast<int>(m);
-  P.U = P.rowtiles * P.kblocks;
   P.e = e;
   P.qp = qp;
   P.trace = trace_buffer();
-  // L2 bulk prefetch of the CTA's range beyond the pre-issued ring slots and of
-  // the successor layer: off by default -- measured slower on every decode
-  // shape (profiles/r01_dec_prefetch_sweep.txt: W4A4 M=1 7.56 -> 7.32 us, W8A8
-  // M=1 10.0 -> 8.4 us, W4A4 M=8 11.3 -> 9.9 us); ABQ_DEC_PREFETCH=1 restores it.
-  P.prefetch = 0;
-  P.next_frag = static_cast<const unsigned char*>(next_frag);
-  P.next_bytes = next_frag ? next_bytes : 0;
-  if (const char* env = std::getenv("ABQ_DEC_PREFETCH")) P.prefetch = env[0] == '1';
-  const int mt = m <= 1 ? 1 : m <= 2 ? 2 : m <= 4 ? 4 : 8;
+  const int mt = dec_mt(m);
   const int kpad = P.kblocks * kKBlock;
   // workspace (imma_ws_bytes layout): [row-tile accumulators][counters][codes][stats][report word]
   char* w = static_cast<char*>(ws);
@@ -724,9 +648,9 @@ int run_gemv_dec(const uint32_t* frag, unsigned q, size_t n, size_t k, size_t m,
   long long* rowsum = reinterpret_cast<long long*>(w + 128);
   P.bad_word = reinterpret_cast<unsigned long long*>(w + 192);
   P.bad_out = bad_out;
-  // fused ReQuant: each of the 32*kDecWarps/mt consumer threads of a token holds <= 4 vectors of 8
+  // fused ReQuant: each of the 32*kDecWarps/mt threads of a token holds <= kDecXR vectors of 8
   const bool fused = x_dtype == ABQ_F16 && !qp.per_tensor && k % 8 == 0 &&
-                     k <= static_cast<size_t>(32 * kDecWarps * 32 / mt);
+                     k <= static_cast<size_t>(8 * kDecXR * 32 * kDecWarps / mt);
   if (fused) {
     P.x16 = static_cast<const __half*>(x);
   } else {
@@ -738,27 +662,20 @@ int run_gemv_dec(const uint32_t* frag, unsigned q, size_t n, size_t k, size_t m,
     P.rowsum = rowsum;
   }
   const int grid = std::min(num_sms(), P.rowtiles);
-  // Ring (one CTA per SM): as deep as the CTA's whole weight share when that
-  // fits in shared memory -- then every TMA copy is issued at kernel start and
-  // no refill latency is exposed at the tail of the main loop -- else ~208 KB.
   const int nl = dec_nlrt_max(P.rowtiles, grid);
+  P.slots = dec_slots(q, n, k, mt, grid);
   const size_t slot_bytes = static_cast<size_t>(kDecUPS) * q * 512;
-  const int max_units = ((P.rowtiles + grid - 1) / grid) * P.kblocks;
-  int slots = (max_units + kDecUPS - 1) / kDecUPS;
-  if (const char* env = std::getenv("ABQ_DEC_RING_KB")) slots = static_cast<int>(std::atoi(env) * 1024 / slot_bytes);
-  const int min_slots = kDecWarps / kDecUPS;
-  slots = std::max(min_slots, std::min(32, slots));
-  const size_t budget = 212 * 1024;
-  while (slots > min_slots && dec_smem(q, slots, mt, kpad, nl).total > budget) --slots;
-  P.slots = slots;
-  // slots in flight before the activations are awaited: ~64 KB (the rest is
-  // L2-prefetched and copied once the activation loads are issued)
-  int pre_kb = 64;
-  if (const char* env = std::getenv("ABQ_DEC_PRE_KB")) pre_kb = std::atoi(env);
-  P.preslots = fused ? std::max(1, std::min(slots, static_cast<int>(pre_kb * 1024 / slot_bytes))) : slots;
-  const size_t smem = dec_smem(q, slots, mt, kpad, nl).total;
-  bool pdl = true;
-  if (const char* env = std::getenv("ABQ_DEC_PDL")) pdl = env[0] == '1';
+  // slots in flight before the activations are awaited (the rest is issued
+  // right behind the activation loads)
+  // Measured (profiles/r02_dec_prekb_sweep.txt): when the ring holds the CTA's
+  // whole share, issuing it only behind the activation loads is fastest (the
+  // activations do not queue behind the stream); when it must be refilled
+  // (W8 at LLaMA-7B up_proj: 305 KB per SM), ~64 KB up front is.
+  const int whole = (nl * P.kblocks + kDecUPS - 1) / kDecUPS;
+  const int pre_kb = dec_tuning().pre_kb >= 0 ? dec_tuning().pre_kb : (P.slots >= whole ? 0 : 64);
+  P.preslots = fused ? std::max(0, std::min(P.slots, static_cast<int>(pre_kb * 1024 / slot_bytes))) : P.slots;
+  const size_t smem = dec_smem(q, P.slots, mt, kpad, nl).total;
+  const bool pdl = dec_tuning().pdl != 0;
   switch (mt) {
     case 1: return launch_dec1<1>(P, grid, smem, pdl, st);
     case 2: return launch_dec1<2>(P, grid, smem, pdl, st);

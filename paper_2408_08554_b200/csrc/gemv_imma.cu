@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(kActThreads) act_quant_kernel(const T* __restr
       int z = 0;
       float inv32 = 0.0f;
       if (lane < 2) group_params(qp, unord(l2), unord(h2), &step, &z);
-      if (lane == 1) inv32 = f32_reciprocal(step);
+      if (lane == 1) inv32 = f32_reciprocal_fast(step);
       step = __shfl_sync(0xffffffffu, step, 0);
       z = __shfl_sync(0xffffffffu, z, 0);
       inv32 = __shfl_sync(0xffffffffu, inv32, 1);
@@ -976,73 +976,6 @@ int run_act_quant(const void* x, int x_dtype, size_t m, size_t k, int mt, const 
 #undef ABQ_ACTQ
   ABQ_LAUNCHED();
   return ABQ_OK;
-}
-
-int run_gemv_dec(const uint32_t* frag, unsigned q, size_t n, size_t k, size_t m, const void* x, int x_dtype,
-                 const QuantParams& qp, const EpiParams& e, void* ws, unsigned long long* bad_out,
-                 cudaStream_t st, const void* next_frag, size_t next_bytes);
-
-// Serving path: act_quant_kernel (ReQuant into B-fragment codes) followed by the
-// stream-K GEMV with programmatic dependent launch.  `ws` must be
-// imma_ws_bytes(n, k) of zero-filled device memory (left zeroed).
-int run_gemv_imma_fused(const uint32_t* frag, unsigned q, size_t n, size_t k, size_t m, const void* x,
-                        int x_dtype, const QuantParams& qp, const EpiParams& e, void* ws,
-                        unsigned long long* bad_out, cudaStream_t st, const void* next_frag,
-                        size_t next_bytes) {
-  if (m == 0 || n == 0) return ABQ_OK;
-  // the serving kernel is gemv_dec_kernel (gemv_dec.cu); ABQ_GEMV_KERNEL=imma
-  // selects this earlier per-warp-ring kernel for comparison
-  const char* kern_env = std::getenv("ABQ_GEMV_KERNEL");
-  if (!(kern_env && std::strcmp(kern_env, "imma") == 0))
-    return run_gemv_dec(frag, q, n, k, m, x, x_dtype, qp, e, ws, bad_out, st, next_frag, next_bytes);
-  ImmaParams P = base_params(frag, q, n, k, m, e);
-  const int mt = pick_imma_mt(static_cast<int>(m));
-  const size_t rowtiles = P.rowtiles;
-  const size_t kpad = static_cast<size_t>(P.kblocks) * kKBlock;
-  char* w = static_cast<char*>(ws);
-  P.gacc = reinterpret_cast<long long*>(w);
-  w += rowtiles * 16 * 8 * 8;
-  P.gcnt = reinterpret_cast<unsigned*>(w);
-  w += (rowtiles * 4 + 255) & ~size_t(255);
-  uint32_t* act_frag = reinterpret_cast<uint32_t*>(w);
-  w += 8 * kpad;
-  double* s_a = reinterpret_cast<double*>(w);
-  int32_t* z_a = reinterpret_cast<int32_t*>(w + 64);
-  long long* rowsum = reinterpret_cast<long long*>(w + 128);
-  unsigned long long* bad_word = reinterpret_cast<unsigned long long*>(w + 192);
-  P.act_frag = act_frag;
-  P.s_a = s_a;
-  P.z_a = z_a;
-  P.rowsum = rowsum;
-  P.bad_word = bad_word;
-  P.bad_out = bad_out;
-  P.qp = qp;
-  // m <= 2 fp16 per-token rows: ReQuant fused into every CTA's prologue (one
-  // launch); otherwise a separate ReQuant kernel overlapped by PDL.
-  bool fused = x_dtype == ABQ_F16 && !qp.per_tensor && m <= 2 && k % 8 == 0 &&
-               k <= static_cast<size_t>(8 * 4 * imma_warps(P.q) * 32);
-  if (const char* env = std::getenv("ABQ_GEMV_FUSED")) fused = fused && env[0] == '1';
-  if (const char* env = std::getenv("ABQ_EXP_LATE_RING")) P.late_ring = env[0] == '1';
-  if (fused) {
-    P.x16 = static_cast<const __half*>(x);
-  } else {
-    int st_code = run_act_quant(x, x_dtype, m, k, mt, qp, act_frag, 0, s_a, z_a, rowsum, bad_word, st);
-    if (st_code) return st_code;
-  }
-  // Stream-K (unit-granular split, cross-CTA partial sums) pays a global fence
-  // and atomics; with >= 4 row-tiles per SM the row-tile-granular split is
-  // balanced enough and has no cross-CTA traffic.  ABQ_GEMV_STREAMK=0/1 overrides.
-  bool stream_k = P.rowtiles < 4 * num_sms();
-  if (const char* env = std::getenv("ABQ_GEMV_STREAMK")) stream_k = env[0] == '1';
-  if (!stream_k) {
-    P.gacc = nullptr;
-    P.gcnt = nullptr;
-  }
-  int gx;
-  plan_grid(P, mt, stream_k, &gx);
-  const int gy = static_cast<int>((m + mt - 1) / mt);
-  if (gy != 1) return fail(ABQ_ERR_VALUE, "gemv_imma: fused path supports m <= 8");
-  return launch_mt<false>(P, mt, gx, gy, !fused, st);
 }
 
 }  // namespace abq_dev

@@ -119,6 +119,51 @@ __device__ __forceinline__ float f32_reciprocal(double step) {
   return step > 0x1p-100 && step < 0x1p100 ? static_cast<float>(1.0 / step) : CUDART_NAN_F;
 }
 
+// Same bound via the fp32 reciprocal of RN32(step) (no FP64 division on the
+// prologue's critical path): inv32 is within (1 + 2^-24)^2 - 1 < 2^-22.9 of
+// 1/step, so q = RN32(v * inv32) in quant_code_f32 / quant_codes8_f16 is within
+// |q| * 2^-22.3 of v/step, still inside their 2^-21 tie band.
+__device__ __forceinline__ float f32_reciprocal_fast(double step) {
+  return step > 0x1p-100 && step < 0x1p100 ? __frcp_rn(__double2float_rn(step)) : CUDART_NAN_F;
+}
+
+// group_params plus inv32 = f32_reciprocal_fast(step), with the asymmetric
+// zero point z = clamp(round(RN64(-lo / step))) taken from the fp32 quotient
+// qz = RN32(RN32(-lo) * inv32) -- within |qz| * 2^-21.9 of -lo/step -- whenever
+// qz is farther than max(|qz|, 1) * 2^-20 from the nearest n + 1/2 (then both
+// round to rint(qz)); otherwise, and for |qz| >= 2^22, by the IEEE quotient.
+// One FP64 division (step) on the prologue's critical path instead of three.
+__device__ __forceinline__ void group_params_fast(const QuantParams& qp, double lo_raw, double hi_raw,
+                                                  double* step_out, int* z_out, float* inv_out) {
+  if (qp.scheme != ABQ_ASYMMETRIC) {
+    group_params(qp, lo_raw, hi_raw, step_out, z_out);
+    *inv_out = f32_reciprocal_fast(*step_out);
+    return;
+  }
+  const double lo = __dmul_rn(qp.beta, lo_raw);
+  const double hi = __dmul_rn(qp.alpha, hi_raw);
+  if (hi == lo) {
+    *step_out = 1.0;
+    *z_out = 0;
+    *inv_out = 1.0f;
+    return;
+  }
+  const double step = __dsub_rn(hi, lo) / static_cast<double>(qp.levels - 1);
+  const float inv32 = f32_reciprocal_fast(step);
+  const float q = __fmul_rn(__double2float_rn(-lo), inv32);
+  const float t = __fadd_rn(q, 12582912.0f);  // 1.5 * 2^23
+  const float r = __fsub_rn(t, 12582912.0f);
+  const float d = __fsub_rn(0.5f, fabsf(__fsub_rn(q, r)));
+  double zz = (fabsf(q) < 4194304.0f && d > fmaxf(fabsf(q), 1.0f) * 9.5367431640625e-07f)  // 2^22, 2^-20
+                  ? static_cast<double>(r)
+                  : round(-lo / step);
+  const double top = static_cast<double>(qp.levels - 1);
+  zz = zz < 0.0 ? 0.0 : (top < zz ? top : zz);
+  *step_out = step;
+  *z_out = static_cast<int>(zz);
+  *inv_out = inv32;
+}
+
 // Same result as quant_code for a value exactly representable in fp32 (fp16 /
 // fp32 activations without a compensation pair), on the fp32 pipe.
 // q = RN32(v * RN32(1/step)) is within |q| * 2^-22.9 of the reference's

@@ -135,29 +135,24 @@ def test_repeated_calls_are_deterministic(abq, variant):
         assert torch.equal(lin(xd, out_dtype=torch.float64, check=False), first)
 
 
-def test_prefetch_next_hint_is_transparent(abq, orc):
-    """abq_weights.prefetch_next only moves the successor's weight traffic into
-    L2 earlier: results with the hint (chained, cyclic) equal those without and
-    the oracle, for every layer of the chain."""
+def test_chained_layers_back_to_back(abq, orc):
+    """layers of different shapes launched back to back on one stream (the
+    PDL chain: each launch starts while its predecessor drains, and waits for
+    it before reading activations), outputs read only at the end: every layer
+    equals the oracle, repeatedly."""
     rng = np.random.default_rng(11)
     m, k = 2, 1024
     layers = []
     for n, wb, ab in ((700, 4, 4), (300, 2, 8), (513, 8, 3)):
         x, wc, sb, zb = _case(rng, m, n, k, wb, ab)
         w = abq.PackedWeights.from_planes(abq.bitpack(wc, wb), sb, zb)
-        layers.append((x, wc, sb, zb, wb, ab, w))
-    plain = [abq.Linear(L[6], abq.QuantSpec(bits=L[5], granularity=abq.api.PER_TOKEN), max_m=m) for L in layers]
-    hinted = [abq.Linear(L[6], abq.QuantSpec(bits=L[5], granularity=abq.api.PER_TOKEN), max_m=m) for L in layers]
-    for i, lin in enumerate(hinted):
-        lin.prefetch_next(hinted[(i + 1) % len(hinted)])
+        lin = abq.Linear(w, abq.QuantSpec(bits=ab, granularity=abq.api.PER_TOKEN), max_m=m)
+        ac, sa, za = orc.quantize(x.astype(np.float64), ab, 0, 2)
+        layers.append((torch.from_numpy(x).cuda(), lin, orc.quantized_linear(ac, ab, sa, za, wc, wb, sb, zb)))
     for rep in range(3):
-        for (x, wc, sb, zb, wb, ab, _), lp, lh in zip(layers, plain, hinted):
-            xt = torch.from_numpy(x).cuda()
-            y0 = lp(xt, out_dtype=torch.float64).cpu().numpy()
-            y1 = lh(xt, out_dtype=torch.float64).cpu().numpy()
-            ac, sa, za = orc.quantize(x.astype(np.float64), ab, 0, 2)
-            want = orc.quantized_linear(ac, ab, sa, za, wc, wb, sb, zb)
-            assert np.array_equal(y0, want) and np.array_equal(y1, want), (rep, wb, ab)
+        outs = [lin(xt, out_dtype=torch.float64) for xt, lin, _ in layers * 2]
+        for (xt, lin, want), y in zip(layers * 2, outs):
+            assert np.array_equal(y.cpu().numpy(), want), rep
 
 
 @pytest.mark.parametrize("m,n,k,wb,ab", [
@@ -172,7 +167,12 @@ def test_serving_gemv_llama_shapes(abq, orc, m, n, k, wb, ab):
     w = abq.PackedWeights.from_planes(abq.bitpack(wc, wb), sb, zb)
     lin = abq.Linear(w, abq.QuantSpec(bits=ab, granularity=abq.api.PER_TOKEN), max_m=m)
     xt = torch.from_numpy(x).cuda()
+    n0 = abq.launch_count()
     y64 = lin(xt, out_dtype=torch.float64).cpu().numpy()
+    # the serving decode path: ONE launch with the ReQuant fused into the GEMV
+    # prologue (K * tokens small enough), else the ReQuant kernel + the GEMV
+    fused = k * (1 if m == 1 else 2 if m == 2 else 4 if m <= 4 else 8) <= 16384
+    assert abq.launch_count() - n0 == (1 if fused else 2), (m, k)
     y16 = lin(xt, out_dtype=torch.float16).cpu().numpy()
     ac, sa, za = orc.quantize(x.astype(np.float64), ab, 0, 2)
     want = orc.quantized_linear(ac, ab, sa, za, wc, wb, sb, zb)
