@@ -71,8 +71,21 @@ LAYERS = {
         "cfg5 LLaMA-70B W4A4 prefill layer (q,k,v,o,gate,up,down), M=2048, N-sharded over the ranks"),
 }
 
+# decode layer chains (LLaMA-7B, M=1): the 7 linears of one layer in their real
+# order, the producers of their inputs with the ReQuant fused in (SURVEY.md
+# 8f-2): RMSNorm+ReQuant -> q, k, v; o (fused-prologue GEMV on a fixed fp16
+# attention output: attention is out of scope); RMSNorm+ReQuant -> gate, up;
+# SiLU(gate)*up+ReQuant -> down.  name -> (w_bits, a_bits, description)
+CHAINS = {
+    "llama7b_decode_chain_w4a4": (4, 4, "LLaMA-7B decode layer chain W4A4 M=1 (q,k,v,o,gate,up,down + fused-ReQuant producers)"),
+    "llama7b_decode_chain_w2a8": (2, 8, "LLaMA-7B decode layer chain W2A8 M=1 (q,k,v,o,gate,up,down + fused-ReQuant producers)"),
+}
+CHAIN_LINEARS = [("q", 4096, 4096), ("k", 4096, 4096), ("v", 4096, 4096), ("o", 4096, 4096),
+                 ("gate", 11008, 4096), ("up", 11008, 4096), ("down", 4096, 11008)]
+
 # the parts of the headline metric measured beside the headline (N=1)
-PARTS = ["cfg1_w2a8", "w2a8_m1_gate_up", "w2a8_m1_down", "cfg2_w8a8_m1", "cfg2_w4a4_m128", "cfg2_w8a8_m128"]
+PARTS = ["cfg1_w2a8", "w2a8_m1_gate_up", "w2a8_m1_down", "cfg2_w8a8_m1", "cfg2_w4a4_m128", "cfg2_w8a8_m128",
+         "llama7b_decode_chain_w4a4", "llama7b_decode_chain_w2a8"]
 
 
 def packed_bytes(n, k, w_bits):
@@ -414,6 +427,80 @@ def measure_part(abq, torch, name, world, steps, warmup, l2, peaks, peak_kind):
         row["cublas_fp16_TOPS"] = round(2 * m * n * k / cus / 1e6, 2)
         row["speedup_vs_cublas_fp16"] = round(cus / us, 3)
         del wf
+    del lins, cat
+    torch.cuda.empty_cache()
+    return row
+
+
+def measure_chain(abq, torch, name, steps, warmup, l2, peaks, peak_kind, world=1):
+    """One LLaMA-7B decode layer chain per step (CHAINS), L2-cold (rotating
+    copies of the whole layer), CUDA-graph replay.  Also times the same chain
+    with every GEMV re-quantizing its fp16 input in its own prologue (the
+    producers still run, their codes unused) -- the unfused comparator."""
+    wb, ab, desc = CHAINS[name]
+    rng = np.random.default_rng(11)
+    spec = abq.QuantSpec(bits=ab, granularity=abq.api.PER_TOKEN)
+    layer_bytes = sum(packed_bytes(n, k, wb) for _, n, k in CHAIN_LINEARS)
+    copies = rotation_copies(l2, layer_bytes, cap=16)
+    base = []
+    for _, n, k in CHAIN_LINEARS:
+        wc, sb, zb = synth_layer(rng, n, k, wb)
+        base.append(abq.PackedWeights.from_planes(abq.bitpack(wc, wb), sb, zb))
+    lins = [[abq.Linear(w if c == 0 else w.copy(), spec, max_m=1) for w in base] for c in range(copies)]
+    f16 = lambda *s: torch.from_numpy(rng.standard_normal(s).astype(np.float16)).cuda()  # noqa: E731
+    x, ctx, x2 = f16(1, 4096), f16(1, 4096), f16(1, 4096)
+    g1 = torch.from_numpy(rng.uniform(0.8, 1.2, 4096).astype(np.float16)).cuda()
+    g2 = torch.from_numpy(rng.uniform(0.8, 1.2, 4096).astype(np.float16)).cuda()
+    h1, h2, act = (torch.empty((1, 4096), dtype=torch.float16, device="cuda") for _ in range(3))
+    act = torch.empty((1, 11008), dtype=torch.float16, device="cuda")
+    ys = [torch.empty((1, n), dtype=torch.float16, device="cuda") for _, n, _ in CHAIN_LINEARS]
+    qa1, qa2, qa3 = abq.QAct(1, 4096, spec), abq.QAct(1, 4096, spec), abq.QAct(1, 11008, spec)
+
+    # q/k/v and gate/up read the same input: one concatenated launch each
+    # (PackedWeights.concat; column blocks = the separate projections' outputs)
+    cat = [[abq.Linear(abq.PackedWeights.concat([L[0].w, L[1].w, L[2].w]), spec, max_m=1),
+            abq.Linear(abq.PackedWeights.concat([L[4].w, L[5].w]), spec, max_m=1)] for L in lins]
+    yqkv = torch.empty((1, 3 * 4096), dtype=torch.float16, device="cuda")
+    ygu = torch.empty((1, 2 * 11008), dtype=torch.float16, device="cuda")
+
+    def fused(c):
+        L, (qkv, gu) = lins[c], cat[c]
+        abq.rmsnorm_quant(x, g1, 1e-6, spec, out=qa1)
+        qkv(qa1, out=yqkv)
+        L[3](ctx, out=ys[3])
+        abq.rmsnorm_quant(x2, g2, 1e-6, spec, out=qa2)
+        gu(qa2, out=ygu)
+        abq.silu_mul_quant(ygu[:, :11008], ygu[:, 11008:], spec, out=qa3)
+        L[6](qa3, out=ys[6])
+
+    def unfused(c):
+        L = lins[c]
+        abq.rmsnorm_quant(x, g1, 1e-6, spec, out=qa1, y_out=h1)
+        for j in range(3):
+            L[j](h1, out=ys[j])
+        L[3](ctx, out=ys[3])
+        abq.rmsnorm_quant(x2, g2, 1e-6, spec, out=qa2, y_out=h2)
+        L[4](h2, out=ys[4])
+        L[5](h2, out=ys[5])
+        abq.silu_mul_quant(ys[4], ys[5], spec, out=qa3, y_out=act)
+        L[6](act, out=ys[6])
+
+    l0 = abq.launch_count()
+    fused(0)
+    per_step = abq.launch_count() - l0
+    ms, _ = time_graph(torch, fused, copies, steps, warmup, world)
+    us = ms * 1e3 / steps
+    ums, _ = time_graph(torch, unfused, copies, steps, warmup, world)
+    uus = ums * 1e3 / steps
+    ach = layer_bytes / (us * 1e-6) / 1e9
+    row = {"workload": desc, "step_us": round(us, 3), "GBps_packed_weights": round(ach, 1),
+           "roofline": {"bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                        "frac": round(ach / peaks["hbm_gbs"], 4), "algorithmic_bytes_per_step": layer_bytes,
+                        "peak_kind": peak_kind},
+           "launches_per_step": per_step, "unfused_step_us": round(uus, 3),
+           "unfused_GBps": round(layer_bytes / (uus * 1e-6) / 1e9, 1),
+           "note": "fused: RMSNorm/SiLU*up producers emit the codes, q/k/v and gate/up run as one concatenated "
+                   "launch each; unfused: 7 separate GEMVs each re-quantizing its fp16 input in its prologue"}
     del lins
     torch.cuda.empty_cache()
     return row
@@ -513,6 +600,11 @@ def run_ours(args, world, rank, local):
     import paper_2408_08554_b200 as abq
     if args.workload in LAYERS:
         return run_layer(args, world, rank, local)
+    if args.workload in CHAINS:  # tool mode: the chain part alone
+        peaks, peak_kind = measured_peaks()
+        l2 = torch.cuda.get_device_properties(local).L2_cache_size
+        print(json.dumps(measure_chain(abq, torch, args.workload, args.steps, args.warmup, l2, peaks, peak_kind)))
+        return
     m, n, k, wb, ab, desc = WORKLOADS[args.workload]
     # column-parallel sharding, weak scaling: the layer has
     # world x N output channels and rank r owns channels [r*N, (r+1)*N).  No
@@ -617,8 +709,16 @@ def run_ours(args, world, rank, local):
     parts = None
     if world == 1 and not args.no_parts:
         part_steps = max(args.steps, 400)
-        parts = {name: measure_part(abq, torch, name, world, part_steps, max(args.warmup, 20), l2, peaks,
-                                    peak_kind) for name in PARTS if name != args.workload}
+        parts = {}
+        for name in PARTS:
+            if name == args.workload:
+                continue
+            if name in CHAINS:
+                parts[name] = measure_chain(abq, torch, name, max(args.steps, 200), max(args.warmup, 10), l2,
+                                            peaks, peak_kind)
+            else:
+                parts[name] = measure_part(abq, torch, name, world, part_steps, max(args.warmup, 20), l2, peaks,
+                                           peak_kind)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -652,7 +752,7 @@ def main():
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=50)
     ap.add_argument("--impl", default="abq", choices=["abq", "reference"])
-    ap.add_argument("--workload", default="cfg2_w4a4_m1", choices=sorted(list(WORKLOADS) + list(LAYERS)))
+    ap.add_argument("--workload", default="cfg2_w4a4_m1", choices=sorted(list(WORKLOADS) + list(LAYERS) + list(CHAINS)))
     ap.add_argument("--no-check", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parts", action="store_true", help="headline workload only")

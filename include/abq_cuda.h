@@ -241,6 +241,38 @@ int abq_linear(const void* x, int x_dtype, size_t m, size_t k, const abq_quant_s
                const abq_weights* w, void* y, int out_kind, void* workspace,
                size_t workspace_bytes, int64_t* err_index, void* stream);
 
+/* ---- producer-fused ReQuant for decode --------------------
+ * The op that produces a decode linear's input -- RMSNorm (toyblock.hpp:257,
+ * 267) or SiLU(gate) * up (toyblock.hpp:274-275) -- quantizes its own fp16
+ * output per token (quantizer.hpp:146-213, same codes / s_a / z_a / row sums as
+ * abq_quant_pack_act on that output) straight into the decode GEMV's code
+ * layout; abq_linear_qact consumes it, so every projection that reads the same
+ * activations (q/k/v, gate/up) shares one ReQuant.  m <= 8 tokens, per-token
+ * asymmetric / symmetric / balanced spec, K % 8 == 0, K <= 16384.
+ * err_index (device int64, may be NULL => synchronous check): the caller sets
+ * it to -1; the smallest flat index of a non-finite output element is written
+ * (atomic min), -1 stays when every element is finite. */
+typedef struct {
+  uint32_t* codes;      /* abq_qact_codes_bytes(m, k) bytes, device */
+  double* scales;       /* [m] s_a */
+  int32_t* zero_points; /* [m] z_a */
+  int64_t* rowsums;     /* [m] code row sums */
+  size_t m, k;
+  unsigned bits;        /* activation bits the codes were made with */
+} abq_qact;
+size_t abq_qact_codes_bytes(size_t m, size_t k);
+/* y = fp16(gain * fp16(x * rsqrt(mean(x^2) + eps))), x / gain / y_out fp16 [m][k] / [k]
+ * (LLaMA RMSNorm); y_out may be NULL. */
+int abq_rmsnorm_quant(const void* x, const void* gain, float eps, size_t m, size_t k,
+                      const abq_quant_spec* spec, void* y_out, const abq_qact* out, int64_t* err_index,
+                      void* stream);
+/* y = fp16(fp16(silu(gate)) * up), fp16 [m][k]; y_out may be NULL. */
+int abq_silu_mul_quant(const void* gate, const void* up, size_t m, size_t k, const abq_quant_spec* spec,
+                       void* y_out, const abq_qact* out, int64_t* err_index, void* stream);
+/* decode linear on producer-quantized activations (w->frag required): one
+ * GEMV launch, no ReQuant phases on its critical path. */
+int abq_linear_qact(const abq_qact* act, const abq_weights* w, void* y, int out_kind, void* stream);
+
 /* ---- kernel selection (decode GEMV variants) -------------- */
 typedef enum {
   ABQ_GEMV_AUTO = 0,

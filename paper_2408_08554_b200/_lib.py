@@ -38,6 +38,11 @@ class GemmStatsC(C.Structure):
     _fields_ = [("block_tiles", C.c_uint64), ("plane_pair_products", C.c_uint64)]
 
 
+class QActC(C.Structure):
+    _fields_ = [("codes", C.c_void_p), ("scales", C.c_void_p), ("zero_points", C.c_void_p),
+                ("rowsums", C.c_void_p), ("m", C.c_size_t), ("k", C.c_size_t), ("bits", C.c_uint)]
+
+
 class WeightsC(C.Structure):
     _fields_ = [("planes", C.c_void_p), ("q", C.c_uint), ("n", C.c_size_t), ("k", C.c_size_t),
                 ("scales", C.c_void_p), ("zero_points", C.c_void_p), ("colsums", C.c_void_p),
@@ -89,6 +94,10 @@ _SIGNATURES = {
     "abq_linear_workspace_bytes": (_S, [_S, _S, _S, _U]),
     "abq_linear": (_I, [_P, _I, _S, _S, C.POINTER(QuantSpecC), C.POINTER(WeightsC), _P, _I, _P, _S,
                         _P, _P]),
+    "abq_qact_codes_bytes": (_S, [_S, _S]),
+    "abq_rmsnorm_quant": (_I, [_P, _P, C.c_float, _S, _S, C.POINTER(QuantSpecC), _P, C.POINTER(QActC), _P, _P]),
+    "abq_silu_mul_quant": (_I, [_P, _P, _S, _S, C.POINTER(QuantSpecC), _P, C.POINTER(QActC), _P, _P]),
+    "abq_linear_qact": (_I, [C.POINTER(QActC), C.POINTER(WeightsC), _P, _I, _P]),
     "abq_set_gemv_variant": (_I, [_I]),
     "abq_get_gemv_variant": (_I, []),
     "abq_set_gemm_schedule": (_I, [_I]),

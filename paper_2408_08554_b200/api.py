@@ -665,6 +665,26 @@ class PackedWeights:
                              self.frag.clone() if self.frag is not None else None,
                              self.tc.clone() if self.tc is not None else None)
 
+    @staticmethod
+    def concat(parts: List["PackedWeights"]) -> "PackedWeights":
+        """Output-channel concatenation of layers that read the same input
+        (fused q/k/v, gate/up): one engine launch computes all of them; column
+        block j of the result is parts[j]'s output exactly (channels are
+        independent)."""
+        if not parts:
+            raise ValueError("PackedWeights.concat: no parts")
+        p0 = parts[0].planes
+        if any(w.planes.planes != p0.planes or w.planes.cols != p0.cols for w in parts):
+            raise ShapeError("PackedWeights.concat: parts differ in bit width or K")
+        if any(w.per_tensor for w in parts):
+            raise ValueError("PackedWeights.concat: per-channel weight scales required")
+        pm = BitPlaneMatrix(p0.planes, sum(w.planes.rows for w in parts), p0.cols,
+                            torch.cat([w.planes.data for w in parts], dim=1).contiguous())
+        return PackedWeights(pm, torch.cat([w.scales for w in parts]), torch.cat([w.zero_points for w in parts]),
+                             torch.cat([w.colsums for w in parts]), False,
+                             prepack_frag(pm) if parts[0].frag is not None else None,
+                             prepack_tc(pm) if parts[0].tc is not None else None)
+
     def shard(self, rank: int, world: int) -> "PackedWeights":
         """Column-parallel slice: output channels [rank*N/G, (rank+1)*N/G)
         (SURVEY.md 8e).  Each plane contributes a contiguous row range."""
@@ -735,6 +755,95 @@ def quant_pack_act(x: torch.Tensor, spec: QuantSpec):
     return BitPlaneMatrix(p, m, k, planes), sa, za, ra
 
 
+class QAct:
+    """Per-token quantized activations made by a producer op with the ReQuant
+    fused in (rmsnorm_quant / silu_mul_quant), in the decode
+    GEMV's code layout: codes + s_a / z_a / code row sums (quantizer.hpp:146-213
+    applied to the producer's fp16 output).  Consumed by Linear(qact); one
+    QAct feeds every projection that reads the same activations."""
+
+    def __init__(self, m: int, k: int, spec: QuantSpec, device=None):
+        spec.validate()
+        if spec.granularity == PER_TENSOR:
+            raise ValueError("QAct: the fused ReQuant is per token")
+        dev = device or _dev()
+        self.m, self.k, self.spec = m, k, spec
+        nbytes = int(L.lib().abq_qact_codes_bytes(m, k))
+        self.codes = torch.zeros(max(1, nbytes // 4), dtype=torch.int32, device=dev)
+        self.scales = torch.empty(m, dtype=torch.float64, device=dev)
+        self.zero_points = torch.empty(m, dtype=torch.int32, device=dev)
+        self.rowsums = torch.empty(m, dtype=torch.int64, device=dev)
+        self.err = torch.full((1,), -1, dtype=torch.int64, device=dev)
+        self._c = L.QActC(_ptr(self.codes), _ptr(self.scales), _ptr(self.zero_points), _ptr(self.rowsums),
+                          m, k, spec.bits)
+        self._sc = spec.c()
+
+    def c(self) -> L.QActC:
+        return self._c
+
+    def codes_matrix(self) -> np.ndarray:
+        """u8 codes [m][k] decoded from the GEMV layout (tests / inspection)."""
+        mt = 1 if self.m <= 1 else 2 if self.m <= 2 else 4 if self.m <= 4 else 8
+        kpad = -(-self.k // 256) * 256
+        words = self.codes.cpu().numpy().view(np.uint32)
+        out = np.zeros((self.m, self.k), dtype=np.uint8)
+        v = np.arange(self.k // 4)
+        kb, rem = v >> 6, v & 63
+        for t in range(self.m):
+            tb, i = divmod(t, mt)
+            idx = ((((kb * 8 + (rem >> 3)) * mt + i) * 4 + (rem & 3)) * 2) + ((rem >> 2) & 1)
+            w = words[tb * mt * kpad // 4 + idx]
+            out[t, :4 * len(v)] = np.stack([(w >> (8 * b)) & 0xFF for b in range(4)], 1).reshape(-1)
+        return out
+
+    def raise_if_nonfinite(self) -> None:
+        v = int(self.err.item())
+        if v != -1:
+            raise ValueError(f"quantize: non-finite element at ({v // self.k},{v % self.k})")
+
+
+def _producer_out(x: torch.Tensor, spec: QuantSpec, out: Optional[QAct]) -> QAct:
+    m, k = x.shape
+    if out is None:
+        out = QAct(m, k, spec, x.device)
+    elif (out.m, out.k) != (m, k) or out.spec.bits != spec.bits:
+        raise ShapeError("QAct shape / bits differ from the producer input")
+    return out
+
+
+def rmsnorm_quant(x: torch.Tensor, gain: torch.Tensor, eps: float, spec: QuantSpec,
+                  out: Optional[QAct] = None, y_out: Optional[torch.Tensor] = None,
+                  check: bool = False) -> QAct:
+    """LLaMA RMSNorm y = gain * fp16(x * rsqrt(mean(x^2) + eps)) (fp16 in/out)
+    with the per-token ReQuant of y fused in (toyblock.hpp:257 -> 228-240).
+    check=False: launch-only, a non-finite y is recorded in out.err."""
+    if x.dtype != torch.float16 or gain.dtype != torch.float16 or x.dim() != 2 or not x.is_contiguous():
+        raise ValueError("rmsnorm_quant: contiguous fp16 x [m][k] and fp16 gain [k] required")
+    out = _producer_out(x, spec, out)
+    if not check:
+        out.err.fill_(-1)
+    _check(L.lib().abq_rmsnorm_quant(_ptr(x), _ptr(gain.contiguous()), float(eps), x.shape[0], x.shape[1],
+                                     C.byref(out._sc), _ptr(y_out) if y_out is not None else None,
+                                     C.byref(out._c), None if check else _ptr(out.err), _stream()))
+    return out
+
+
+def silu_mul_quant(gate: torch.Tensor, up: torch.Tensor, spec: QuantSpec, out: Optional[QAct] = None,
+                   y_out: Optional[torch.Tensor] = None, check: bool = False) -> QAct:
+    """y = fp16(fp16(silu(gate)) * up) with the per-token ReQuant of y fused in
+    (toyblock.hpp:274-275 -> 228-240)."""
+    if gate.dtype != torch.float16 or up.dtype != torch.float16 or gate.shape != up.shape or gate.dim() != 2:
+        raise ValueError("silu_mul_quant: fp16 gate / up of the same [m][k] shape required")
+    gate, up = gate.contiguous(), up.contiguous()
+    out = _producer_out(gate, spec, out)
+    if not check:
+        out.err.fill_(-1)
+    _check(L.lib().abq_silu_mul_quant(_ptr(gate), _ptr(up), gate.shape[0], gate.shape[1], C.byref(out._sc),
+                                      _ptr(y_out) if y_out is not None else None, C.byref(out._c),
+                                      None if check else _ptr(out.err), _stream()))
+    return out
+
+
 class Linear:
     """One-call engine linear from fp16/fp32/fp64 activations: ReQuant +
     BitPacking (K1), plane GEMV/GEMM (K2/K3) and the fused epilogue (K4).
@@ -763,6 +872,8 @@ class Linear:
         activation is recorded on the device and raised by the next
         raise_if_nonfinite(); check=True synchronises and raises at once
         (quantizer.hpp:155-160 semantics)."""
+        if isinstance(x, QAct):
+            return self._call_qact(x, out, out_dtype)
         if not isinstance(x, torch.Tensor) or x.dim() != 2:
             raise ShapeError("Linear: activations must be a 2-D tensor [M][K]")
         if x.dtype not in (torch.float16, torch.float32, torch.float64):
@@ -788,6 +899,18 @@ class Linear:
                                   self.ws_bytes, None if check else _ptr(self.err), _stream()))
         if not check:
             self._last_k = x.shape[1]
+        return out
+
+    def _call_qact(self, a: "QAct", out, out_dtype) -> torch.Tensor:
+        """decode linear on producer-quantized activations (abq_linear_qact)"""
+        if a.m > self.max_m:
+            raise ValueError(f"Linear: m={a.m} exceeds max_m={self.max_m}")
+        n = self.w.planes.rows
+        if out is None:
+            out = torch.empty((a.m, n), dtype=out_dtype, device=a.codes.device)
+        elif out.dtype not in _OUT or tuple(out.shape) != (a.m, n) or not out.is_contiguous():
+            raise ShapeError(f"Linear: out must be a contiguous ({a.m}, {n}) tensor of a supported dtype")
+        _check(L.lib().abq_linear_qact(C.byref(a.c()), C.byref(self._wc), _ptr(out), _OUT[out.dtype], _stream()))
         return out
 
     def raise_if_nonfinite(self) -> None:

@@ -87,6 +87,17 @@ size_t frag_words(unsigned q, size_t n, size_t k);
 size_t imma_ws_bytes(size_t n, size_t k);
 bool imma_supported(size_t m, size_t k);
 bool dec_supported(unsigned q, size_t n, size_t k, size_t m);
+int run_gemv_dec_qact(const uint32_t* frag, unsigned q, size_t n, size_t k, size_t m, const uint32_t* codes,
+                      const double* s_a, const int32_t* z_a, const long long* rowsum, const QuantParams& qp,
+                      const EpiParams& e, cudaStream_t st);
+size_t qact_codes_bytes(size_t m, size_t k);
+bool qact_supported(size_t m, size_t k);
+int run_rmsnorm_quant(const __half* x, const __half* gain, float eps, size_t m, size_t k, const QuantParams& qp,
+                      __half* y_out, uint32_t* codes, double* s_a, int32_t* z_a, long long* rowsum,
+                      unsigned long long* err, cudaStream_t st);
+int run_silu_mul_quant(const __half* gate, const __half* up, size_t m, size_t k, const QuantParams& qp,
+                       __half* y_out, uint32_t* codes, double* s_a, int32_t* z_a, long long* rowsum,
+                       unsigned long long* err, cudaStream_t st);
 unsigned long long*& trace_buffer();
 int run_prepack_frag(const uint64_t* planes, unsigned q, size_t n, size_t k, uint32_t* frag,
                      cudaStream_t st);
@@ -248,6 +259,48 @@ static EpiParams raw_epi(void* out, size_t n, bool wide) {
 
 using namespace abq_dev;
 
+static int epi_mode_of(int out_kind, int* mode) {
+  switch (out_kind) {
+    case ABQ_OUT_F64: *mode = EPI_F64; return ABQ_OK;
+    case ABQ_OUT_F16: *mode = EPI_F16; return ABQ_OK;
+    case ABQ_OUT_F32: *mode = EPI_F32; return ABQ_OK;
+    case ABQ_OUT_CORR_I64: *mode = EPI_CORR_I64; return ABQ_OK;
+    default: return fail(ABQ_ERR_VALUE, "linear: unknown out_kind %d", out_kind);
+  }
+}
+
+static int check_qact(const abq_qact* out, const abq_quant_spec* spec, size_t m, size_t k, const char* who) {
+  int st = validate_spec(spec);
+  if (st) return st;
+  if (spec->granularity == ABQ_PER_TENSOR)
+    return fail(ABQ_ERR_VALUE, "%s: per-token activation spec required (the ReQuant is fused per token)", who);
+  if (!out || !out->codes || !out->scales || !out->zero_points || !out->rowsums)
+    return fail(ABQ_ERR_VALUE, "%s: output buffers missing", who);
+  if (out->m != m || out->k != k) return fail(ABQ_ERR_SHAPE, "%s: output shape differs from the input", who);
+  if (!qact_supported(m, k))
+    return fail(ABQ_ERR_VALUE, "%s: m <= 8 tokens, K %% 8 == 0 and K <= 16384 required (m=%zu, K=%zu)", who, m, k);
+  if (out->bits != spec->bits) return fail(ABQ_ERR_VALUE, "%s: out->bits differs from the spec", who);
+  return check_device();
+}
+
+template <typename Launch>
+static int producer_call(int64_t* err_index, size_t k, cudaStream_t s, Launch&& launch) {
+  unsigned long long* sc = nullptr;
+  unsigned long long* err = reinterpret_cast<unsigned long long*>(err_index);
+  if (!err) {
+    sc = scratch_words();
+    if (!sc) return fail(ABQ_ERR_CUDA, "producer: cannot allocate device scratch");
+    ABQ_CUDA_TRY(cudaMemsetAsync(sc, 0xFF, 8, s));
+    err = sc;
+  }
+  int st = launch(err);
+  if (st || err_index) return st;
+  unsigned long long b = 0;
+  if ((st = sync_read(sc, s, &b))) return st;
+  if (b != ~0ull) return fail(ABQ_ERR_VALUE, "quantize: non-finite element at (%llu,%llu)", b / k, b % k);
+  return ABQ_OK;
+}
+
 extern "C" {
 
 const char* abq_last_error(void) { return last_error().c_str(); }
@@ -298,6 +351,64 @@ int abq_set_gemm_schedule(int schedule) {
   return ABQ_OK;
 }
 int abq_get_gemm_schedule(void) { return gemm_schedule(); }
+
+// ---- producer-fused ReQuant (producer.cu) ----------------------------------
+size_t abq_qact_codes_bytes(size_t m, size_t k) { return qact_codes_bytes(m, k); }
+
+int abq_rmsnorm_quant(const void* x, const void* gain, float eps, size_t m, size_t k, const abq_quant_spec* spec,
+                      void* y_out, const abq_qact* out, int64_t* err_index, void* stream) {
+  int st = check_qact(out, spec, m, k, "rmsnorm_quant");
+  if (st) return st;
+  if (!x || !gain) return fail(ABQ_ERR_VALUE, "rmsnorm_quant: null input");
+  if (!(eps >= 0.0f)) return fail(ABQ_ERR_VALUE, "rmsnorm_quant: eps must be >= 0");
+  const QuantParams qp = params_of(*spec);
+  cudaStream_t s = as_stream(stream);
+  return producer_call(err_index, k, s, [&](unsigned long long* err) {
+    return run_rmsnorm_quant(static_cast<const __half*>(x), static_cast<const __half*>(gain), eps, m, k, qp,
+                             static_cast<__half*>(y_out), out->codes, out->scales, out->zero_points,
+                             reinterpret_cast<long long*>(out->rowsums), err, s);
+  });
+}
+
+int abq_silu_mul_quant(const void* gate, const void* up, size_t m, size_t k, const abq_quant_spec* spec,
+                       void* y_out, const abq_qact* out, int64_t* err_index, void* stream) {
+  int st = check_qact(out, spec, m, k, "silu_mul_quant");
+  if (st) return st;
+  if (!gate || !up) return fail(ABQ_ERR_VALUE, "silu_mul_quant: null input");
+  const QuantParams qp = params_of(*spec);
+  cudaStream_t s = as_stream(stream);
+  return producer_call(err_index, k, s, [&](unsigned long long* err) {
+    return run_silu_mul_quant(static_cast<const __half*>(gate), static_cast<const __half*>(up), m, k, qp,
+                              static_cast<__half*>(y_out), out->codes, out->scales, out->zero_points,
+                              reinterpret_cast<long long*>(out->rowsums), err, s);
+  });
+}
+
+int abq_linear_qact(const abq_qact* act, const abq_weights* w, void* y, int out_kind, void* stream) {
+  if (!act || !w) return fail(ABQ_ERR_VALUE, "linear_qact: null argument");
+  if (act->k != w->k) return fail(ABQ_ERR_SHAPE, "quantized_linear: inner dimensions differ");
+  if (!w->frag) return fail(ABQ_ERR_VALUE, "linear_qact: weights lack the decode (frag) layout");
+  if (!dec_supported(w->q, w->n, act->k, act->m))
+    return fail(ABQ_ERR_VALUE, "linear_qact: decode GEMV does not cover m=%zu n=%zu K=%zu", act->m, w->n, act->k);
+  if (act->bits < 1 || act->bits > 8) return fail(ABQ_ERR_VALUE, "linear_qact: activation bits must be in [1,8]");
+  int mode = 0, st = epi_mode_of(out_kind, &mode);
+  if (st) return st;
+  if ((st = check_device())) return st;
+  EpiParams e{};
+  e.mode = mode;
+  e.out = y;
+  e.ldo = static_cast<long long>(w->n);
+  e.s_b = w->scales;
+  e.sb_stride = w->per_tensor ? 0 : 1;
+  e.z_b = w->zero_points;
+  e.zb_stride = w->per_tensor ? 0 : 1;
+  e.colsum_b = w->colsums;
+  e.k = static_cast<long long>(act->k);
+  QuantParams qp{};
+  qp.bits = act->bits;
+  return run_gemv_dec_qact(w->frag, w->q, w->n, act->k, act->m, act->codes, act->scales, act->zero_points,
+                           reinterpret_cast<const long long*>(act->rowsums), qp, e, as_stream(stream));
+}
 
 int abq_set_tuning(const char* key, long long value) {
   if (!key) return fail(ABQ_ERR_VALUE, "abq_set_tuning: null key");
@@ -523,15 +634,6 @@ int abq_weights_prepack_tc(const uint64_t* planes, unsigned q, size_t n, size_t 
 }
 
 // ---- fused linear ----------------------------------------------------------
-static int epi_mode_of(int out_kind, int* mode) {
-  switch (out_kind) {
-    case ABQ_OUT_F64: *mode = EPI_F64; return ABQ_OK;
-    case ABQ_OUT_F16: *mode = EPI_F16; return ABQ_OK;
-    case ABQ_OUT_F32: *mode = EPI_F32; return ABQ_OK;
-    case ABQ_OUT_CORR_I64: *mode = EPI_CORR_I64; return ABQ_OK;
-    default: return fail(ABQ_ERR_VALUE, "linear: unknown out_kind %d", out_kind);
-  }
-}
 
 int abq_linear_planes(const abq_act* act, const abq_weights* w, void* y, int out_kind,
                       void* stream) {

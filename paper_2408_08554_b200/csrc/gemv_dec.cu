@@ -304,16 +304,39 @@ __global__ void __launch_bounds__(kDecThreads, kDecCtasPerSm) gemv_dec_kernel(co
       *P.bad_out = w ? ~w : ~0ull;
     }
   } else {
-    // codes + stats from act_quant_kernel (the host issues the whole ring up
-    // front on this path: preslots == slots)
+    // codes + stats from act_quant_kernel or a producer-fused ReQuant
+    // (producer.cu); the codes past K are zero.  Requested first, then the
+    // ring slots not issued yet, then stored.
+    constexpr int CR = 4;
     const uint4* src = reinterpret_cast<const uint4*>(P.act_frag);
     uint4* dst = reinterpret_cast<uint4*>(act);
-    const int nv = MT * kpad / 16;  // act_quant_kernel zero-fills codes past K
-    for (int idx = tid; idx < nv; idx += kDecThreads) dst[idx] = __ldcg(src + idx);
+    const int nv = MT * kpad / 16;
+    uint4 cv[CR];
+#pragma unroll
+    for (int r = 0; r < CR; ++r) {
+      const int idx = tid + r * kDecThreads;
+      if (idx < nv) cv[r] = __ldcg(src + idx);
+    }
+    double sa = 0.0;
+    int za = 0;
+    long long ra = 0;
     if (tid < tok_n) {
-      s_sa[tid] = P.s_a[tid];
-      s_za[tid] = P.z_a[tid];
-      s_ra[tid] = P.rowsum[tid];
+      sa = P.s_a[tid];
+      za = P.z_a[tid];
+      ra = P.rowsum[tid];
+    }
+    if (warp == 0)
+      for (int i = P.preslots + lane; i < S && i < nsl; i += 32) issue_slot(i, i);
+#pragma unroll
+    for (int r = 0; r < CR; ++r) {
+      const int idx = tid + r * kDecThreads;
+      if (idx < nv) dst[idx] = cv[r];
+    }
+    for (int idx = tid + CR * kDecThreads; idx < nv; idx += kDecThreads) dst[idx] = __ldcg(src + idx);
+    if (tid < tok_n) {
+      s_sa[tid] = sa;
+      s_za[tid] = za;
+      s_ra[tid] = ra;
     }
     if (blockIdx.x == 0 && tid == 0 && P.bad_out) {
       const unsigned long long w = *P.bad_word;
@@ -444,9 +467,11 @@ __global__ void __launch_bounds__(kDecThreads, kDecCtasPerSm) gemv_dec_kernel(co
     };
     uint4 w[QT];
     int rtA = -1, rtB = -1;
+    DEC_STAMP(16, clock64());
     for (int j = 0; j < nw; j += 2) {
       // unit j -> set A (fold set B = unit j - 1 behind its IMMAs)
       mbar_wait_parity(&full[fs], fph);
+      if (j == 0) DEC_STAMP(17, clock64());
       lds_unit(fs, w);
       const int slA = fs, iA = fi, kbA = fkb;
       rtA = frt;
@@ -466,11 +491,17 @@ __global__ void __launch_bounds__(kDecThreads, kDecCtasPerSm) gemv_dec_kernel(co
       mma_unit(accB, w);
       release(slB, iB);
       fold(accA, rtA);
+      if (j == 0) DEC_STAMP(18, clock64());
       rtA = -1;
     }
+    DEC_STAMP(19, clock64());
     if (rtA >= 0) fold(accA, rtA);
     else if (nw > 0 && (nw & 1) == 0) fold(accB, rtB);
     flush_tot();
+    DEC_STAMP(20, clock64());
+#ifdef ABQ_TRACE
+    if (P.trace && lane == 0) trace[24 + warp] = clock64();
+#endif
   }
   // epilogue values to shared memory (requested at kernel start), token code
   // sums of the fused ReQuant from the per-warp partials
@@ -619,6 +650,33 @@ bool dec_supported(unsigned q, size_t n, size_t k, size_t m) {
 // GEMV (one launch); anything else goes through act_quant_kernel first, with
 // this kernel as its PDL secondary.  Every launch is itself PDL-enabled so
 // consecutive layers overlap.
+static int launch_dec(DecParams& P, size_t m, bool fused, bool qact, cudaStream_t st);
+
+// Consumer of a producer-fused ReQuant (producer.cu): codes already in the
+// B-fragment layout of dec_mt(m) tokens, with s_a / z_a / code row sums.
+int run_gemv_dec_qact(const uint32_t* frag, unsigned q, size_t n, size_t k, size_t m, const uint32_t* codes,
+                      const double* s_a, const int32_t* z_a, const long long* rowsum, const QuantParams& qp,
+                      const EpiParams& e, cudaStream_t st) {
+  if (m == 0 || n == 0) return ABQ_OK;
+  if (!dec_supported(q, n, k, m)) return fail(ABQ_ERR_VALUE, "gemv_dec: layer shape not supported");
+  DecParams P{};
+  P.frag = frag;
+  P.q = static_cast<int>(q);
+  P.n = static_cast<int>(n);
+  P.k = static_cast<int>(k);
+  P.rowtiles = static_cast<int>((n + kRowTile - 1) / kRowTile);
+  P.kblocks = static_cast<int>((k + kKBlock - 1) / kKBlock);
+  P.m = static_cast<int>(m);
+  P.e = e;
+  P.qp = qp;
+  P.trace = trace_buffer();
+  P.act_frag = codes;
+  P.s_a = s_a;
+  P.z_a = z_a;
+  P.rowsum = rowsum;
+  return launch_dec(P, m, false, true, st);
+}
+
 int run_gemv_dec(const uint32_t* frag, unsigned q, size_t n, size_t k, size_t m, const void* x, int x_dtype,
                  const QuantParams& qp, const EpiParams& e, void* ws, unsigned long long* bad_out,
                  cudaStream_t st) {
@@ -661,6 +719,14 @@ int run_gemv_dec(const uint32_t* frag, unsigned q, size_t n, size_t k, size_t m,
     P.z_a = z_a;
     P.rowsum = rowsum;
   }
+  return launch_dec(P, m, fused, false, st);
+}
+
+static int launch_dec(DecParams& P, size_t m, bool fused, bool qact, cudaStream_t st) {
+  const unsigned q = static_cast<unsigned>(P.q);
+  const size_t n = static_cast<size_t>(P.n), k = static_cast<size_t>(P.k);
+  const int mt = dec_mt(m);
+  const int kpad = P.kblocks * kKBlock;
   const int grid = std::min(num_sms(), P.rowtiles);
   const int nl = dec_nlrt_max(P.rowtiles, grid);
   P.slots = dec_slots(q, n, k, mt, grid);
@@ -673,6 +739,11 @@ int run_gemv_dec(const uint32_t* frag, unsigned q, size_t n, size_t k, size_t m,
   // (W8 at LLaMA-7B up_proj: 305 KB per SM), ~64 KB up front is.
   const int whole = (nl * P.kblocks + kDecUPS - 1) / kDecUPS;
   const int pre_kb = dec_tuning().pre_kb >= 0 ? dec_tuning().pre_kb : (P.slots >= whole ? 0 : 64);
+  // (the paths whose activations come from a preceding kernel -- the
+  // ReQuant kernel or a producer with the ReQuant fused in -- issue the whole
+  // ring up front: their wait covers that kernel's run, which the stream then
+  // overlaps; measured best in the LLaMA-7B decode chain, profiles/r02_chain_prekb_sweep.txt)
+  (void)qact;
   P.preslots = fused ? std::max(0, std::min(P.slots, static_cast<int>(pre_kb * 1024 / slot_bytes))) : P.slots;
   const size_t smem = dec_smem(q, P.slots, mt, kpad, nl).total;
   const bool pdl = dec_tuning().pdl != 0;

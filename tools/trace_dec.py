@@ -61,6 +61,10 @@ for i, t in enumerate(rows):
     marks = [np.median(t[:, c] - t[:, 0]) / ghz / 1e3 for c in range(1, 8)]
     print(f"  launch {i:2d}: span {(e - a) / 1e3:6.2f} us{gap}  (CTA start skew {(t[:, 8].max() - a) / 1e3:5.2f} us)")
     print("             " + ", ".join(f"{nm} {v:.2f}" for nm, v in zip(names, marks)))
+    d = [np.median(t[:, c] - t[:, 5]) / ghz / 1e3 for c in (16, 17, 18, 19, 20)]
+    we = (t[:, 24:40] - t[:, 5:6]) / ghz / 1e3
+    print("             main loop (warp 0, us after codes): start %.2f, first data %.2f, first fold %.2f, loop end %.2f, flush end %.2f;"
+          " warp ends: min %.2f median %.2f max %.2f" % (*d, np.median(we.min(1)), np.median(np.median(we, 1)), np.median(we.max(1))))
     prev_end = e
 first, last = rows[0][:, 8].min(), rows[-1][:, 9].max()
 print(f"  first start -> last end {(last - first) / 1e3:.2f} us = {(last - first) / 1e3 / L:.3f} us per launch")
