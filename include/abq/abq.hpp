@@ -692,24 +692,38 @@ inline Mat quantized_linear(const QuantizedTensor& act, const QuantizedTensor& w
 // ---- device-resident serving API (additions, SURVEY.md 8b "Ownership") -------
 namespace device {
 
-/// Weights packed once and kept in HBM: ABQP planes + per-channel metadata.
+/// Which packed layouts stay resident in HBM: All = ABQP planes + decode
+/// (frag) + prefill (tc) layouts (every entry point, incl. the int64 path);
+/// Decode / Prefill / Both keep one layout per serving regime and drop the
+/// planes after packing (Decode serves m <= 8, Prefill any m).
+enum class Layouts { All, Decode, Prefill, Both };
+
+/// Weights packed once and kept in HBM: engine layouts + per-channel metadata.
 class Weights {
  public:
-  explicit Weights(const QuantizedTensor& wt)
+  explicit Weights(const QuantizedTensor& wt, Layouts layouts = Layouts::All)
       : q_(wt.spec.planes()), n_(wt.rows()), k_(wt.cols()),
         per_tensor_(wt.spec.granularity == Granularity::PerTensor),
         planes_(std::size_t(q_) * n_ * ((k_ + 63) / 64)), scales_(wt.scales),
-        zps_(wt.zero_points), colsums_(n_), frag_(abq_weights_frag_bytes(q_, n_, k_) / 4),
-        tc_(abq_weights_tc_bytes(q_, n_, k_) / 4) {
+        zps_(wt.zero_points), colsums_(n_),
+        frag_(layouts == Layouts::Prefill ? 0 : abq_weights_frag_bytes(q_, n_, k_) / 4),
+        tc_(layouts == Layouts::Decode ? 0 : abq_weights_tc_bytes(q_, n_, k_) / 4) {
     detail::DeviceBuffer<std::uint8_t> dc(wt.codes.data);
     detail::check(abq_bitpack(dc.get(), n_, k_, q_, planes_.get(), nullptr));
     detail::check(abq_plane_rowsums(planes_.get(), q_, n_, k_, colsums_.get(), nullptr));
-    detail::check(abq_weights_prepack(planes_.get(), q_, n_, k_, frag_.get(), nullptr));
-    detail::check(abq_weights_prepack_tc(planes_.get(), q_, n_, k_, tc_.get(), nullptr));
+    if (frag_.size()) detail::check(abq_weights_prepack(planes_.get(), q_, n_, k_, frag_.get(), nullptr));
+    if (tc_.size()) detail::check(abq_weights_prepack_tc(planes_.get(), q_, n_, k_, tc_.get(), nullptr));
+    if (layouts != Layouts::All) {
+      detail::cuda_check(cudaDeviceSynchronize(), "Weights: pack");
+      planes_ = detail::DeviceBuffer<std::uint64_t>();
+    }
   }
   abq_weights view() const {
     return abq_weights{planes_.get(), q_, n_, k_, scales_.get(), zps_.get(), colsums_.get(),
-                       per_tensor_ ? 1 : 0, frag_.get(), tc_.get()};
+                       per_tensor_ ? 1 : 0, frag_.size() ? frag_.get() : nullptr, tc_.size() ? tc_.get() : nullptr};
+  }
+  std::size_t resident_bytes() const {
+    return planes_.size() * 8 + frag_.size() * 4 + tc_.size() * 4;
   }
   std::size_t n() const { return n_; }
   std::size_t k() const { return k_; }

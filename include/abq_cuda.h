@@ -159,6 +159,14 @@ int abq_bmma(const uint64_t* a, unsigned a_planes, size_t m, unsigned a_plane, c
              unsigned b_planes, size_t n, unsigned b_plane, size_t k, int32_t* out, void* stream);
 
 /* ---- L3: engine ---------------------------------------------------------- */
+/* TileConfig -> sm_100a engine schedule used by gemm_arbitrary(_wide)
+ * (SURVEY.md 8f-3): BM caps the token tile (tcgen05 UMMA N 16..256, or the
+ * AND+popcount kernel's token block 1..8) -- written to *token_tile as the
+ * largest power of two <= min(BM, 256); BK == 128 selects the stream-K
+ * schedule (CTAs share each 128-channel row-tile's k-range), deeper BK one CTA
+ * per row-tile -- *schedule = ABQ_GEMM_STREAM_K / ABQ_GEMM_CLASSIC.  Results
+ * are identical for every valid tile; run time is not. */
+int abq_tile_engine_plan(const abq_tile_config* tile, int* token_tile, int* schedule);
 /* gemm_arbitrary  gemm.hpp:185-198: validation order ShapeError (K differs),
  * ValueError (tile), OverflowError (fits_int32).  a_k / b_k are the two
  * operands' cols. */

@@ -80,6 +80,7 @@ _SIGNATURES = {
                                 C.POINTER(GemmStatsC), _P]),
     "abq_gemm_arbitrary_wide": (_I, [_P, _U, _S, _S, _P, _U, _S, _S, C.POINTER(TileConfigC), _P,
                                      C.POINTER(GemmStatsC), _P]),
+    "abq_tile_engine_plan": (_I, [C.POINTER(TileConfigC), C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "abq_gemm_naive": (_I, [_P, _U, _S, _S, _P, _U, _S, _S, _P, _P]),
     "abq_zero_point_correct_i32": (_I, [_P, _S, _S, _P, _P, _P, _P, _S, _P, _P]),
     "abq_zero_point_correct_i64": (_I, [_P, _S, _S, _P, _P, _P, _P, _S, _P, _P]),

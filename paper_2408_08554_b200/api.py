@@ -303,6 +303,14 @@ class TileConfig:
         return f"BM{self.BM}_BN{self.BN}_BK{self.BK}_WM{self.WM}_WN{self.WN}"
 
 
+def tile_engine_plan(tile: TileConfig) -> tuple:
+    """(token_tile, schedule) the engine runs gemm_arbitrary with for this tile
+    (abq_tile_engine_plan): schedule is "stream_k" or "classic"."""
+    tt, sc = C.c_int(0), C.c_int(0)
+    _check(L.lib().abq_tile_engine_plan(C.byref(tile.c()), C.byref(tt), C.byref(sc)))
+    return tt.value, {1: "classic", 2: "stream_k"}.get(sc.value, "auto")
+
+
 def default_tile(p: int, q: int) -> TileConfig:
     """default_tile  gemm.hpp:51-59."""
     t = L.lib().abq_default_tile(p, q)
@@ -650,8 +658,30 @@ class PackedWeights:
                              plane_rowsums(pm), per_tensor, prepack_frag(pm) if frag else None,
                              prepack_tc(pm) if tc else None)
 
+    def resident(self, layouts: str) -> "PackedWeights":
+        """Serving copy that keeps ONE engine layout per regime in HBM and drops
+        the ABQP planes: 'decode' = the GEMV layout (m <= 8), 'prefill' = the
+        tcgen05 layout (any m), 'both' = the two.  Same bytes as the planes per
+        layout (the full object holds planes + frag + tc = 3x).  The API-path
+        entry points, shard() and copy() need the planes: call them on the
+        full object."""
+        if layouts not in ("decode", "prefill", "both"):
+            raise ValueError("PackedWeights.resident: layouts must be 'decode', 'prefill' or 'both'")
+        frag = self.frag if layouts in ("decode", "both") else None
+        tc = self.tc if layouts in ("prefill", "both") else None
+        if (layouts != "prefill" and frag is None) or (layouts != "decode" and tc is None):
+            raise ValueError(f"PackedWeights.resident: the {layouts} layout was not built")
+        pm = BitPlaneMatrix(self.planes.planes, self.planes.rows, self.planes.cols,
+                            torch.empty(0, dtype=torch.int64, device=self.planes.data.device))
+        return PackedWeights(pm, self.scales, self.zero_points, self.colsums, self.per_tensor, frag, tc)
+
+    def resident_bytes(self) -> int:
+        """HBM bytes of the packed weight layouts held (planes, frag, tc)."""
+        return sum(t.numel() * t.element_size() for t in (self.planes.data, self.frag, self.tc) if t is not None)
+
     def c(self) -> L.WeightsC:
-        return L.WeightsC(_ptr(self.planes.data), self.planes.planes, self.planes.rows,
+        return L.WeightsC(_ptr(self.planes.data) if self.planes.data.numel() else None,
+                          self.planes.planes, self.planes.rows,
                           self.planes.cols, _ptr(self.scales), _ptr(self.zero_points),
                           _ptr(self.colsums), int(self.per_tensor),
                           _ptr(self.frag) if self.frag is not None else None,

@@ -82,7 +82,7 @@ int run_zero_point_correct(const Acc* acc, size_t m, size_t n, const int64_t* ra
 int run_bmma(const uint64_t* a, size_t m, unsigned a_plane, const uint64_t* bt, size_t n,
              unsigned b_plane, size_t k, int32_t* out, cudaStream_t st);
 int run_gemm_popc(const uint64_t* A, unsigned p, size_t m, const uint64_t* W, unsigned q, size_t n,
-                  size_t k, bool wide, const EpiParams& e, cudaStream_t st);
+                  size_t k, bool wide, const EpiParams& e, cudaStream_t st, int token_tile = 0);
 size_t frag_words(unsigned q, size_t n, size_t k);
 size_t imma_ws_bytes(size_t n, size_t k);
 bool imma_supported(size_t m, size_t k);
@@ -116,7 +116,7 @@ bool gemm_tc_supported(size_t k);
 int run_gemm_tc(const uint32_t* wtc, unsigned q, size_t n, size_t k, const uint8_t* act, size_t m,
                 const EpiParams& e, cudaStream_t st, unsigned long long* bad_word = nullptr,
                 unsigned long long* bad_out = nullptr, bool pdl = false, unsigned* sk_flags = nullptr,
-                uint32_t* sk_part = nullptr);
+                uint32_t* sk_part = nullptr, EnginePlan plan = EnginePlan{0, 0});
 size_t tc_sk_flag_bytes(size_t n);
 int& gemm_schedule();
 size_t tc_sk_part_bytes(size_t m, size_t n);
@@ -136,8 +136,9 @@ static bool use_dec(const abq_weights* w, size_t m, size_t k) {
   return w->frag != nullptr && dec_supported(w->q, w->n, k, m) && g_gemv_variant != ABQ_GEMV_POPC;
 }
 // prefill GEMM on tcgen05: weights prepacked (tc planes), M >= 9 tokens
+// (prefill-only weights -- no frag layout resident -- serve small m here too)
 static bool use_tc(const abq_weights* w, size_t m, size_t k, bool wide) {
-  return w->tc != nullptr && m >= 9 && !wide && gemm_tc_supported(k) &&
+  return w->tc != nullptr && (m >= 9 || w->frag == nullptr) && !wide && gemm_tc_supported(k) &&
          g_gemv_variant != ABQ_GEMV_POPC;
 }
 
@@ -228,7 +229,7 @@ static void add_stats(abq_gemm_stats* stats, const abq_tile_config& t, size_t m,
 // for the GEMM, in stream-ordered scratch.
 static int gemm_tc_from_planes(const uint64_t* a, unsigned p, size_t m, const uint64_t* w_planes,
                                const uint32_t* wtc, unsigned q, size_t n, size_t k,
-                               const EpiParams& e, cudaStream_t s) {
+                               const EpiParams& e, cudaStream_t s, EnginePlan plan = EnginePlan{0, 0}) {
   uint8_t* codes = nullptr;
   ABQ_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&codes), m * k + tc_act_bytes(m, k), s));
   uint8_t* tiled = codes + m * k;  // 16-B aligned: k % 16 == 0
@@ -241,7 +242,18 @@ static int gemm_tc_from_planes(const uint64_t* a, unsigned p, size_t m, const ui
     if (!st) st = run_prepack_tc(w_planes, q, n, k, tmp, s);
     wtc = tmp;
   }
-  if (!st) st = run_gemm_tc(wtc, q, n, k, tiled, m, e, s);
+  // the stream-K schedule needs its (zeroed) flags and partial tiles
+  unsigned* flags = nullptr;
+  uint32_t* part = nullptr;
+  if (!st && plan.schedule == ABQ_GEMM_STREAM_K) {
+    cudaError_t err = cudaMallocAsync(reinterpret_cast<void**>(&flags), tc_sk_flag_bytes(n), s);
+    if (err == cudaSuccess) err = cudaMemsetAsync(flags, 0, tc_sk_flag_bytes(n), s);
+    if (err == cudaSuccess) err = cudaMallocAsync(reinterpret_cast<void**>(&part), tc_sk_part_bytes(m, n), s);
+    if (err != cudaSuccess) st = fail(ABQ_ERR_CUDA, "gemm_tc: stream-K scratch: %s", cudaGetErrorString(err));
+  }
+  if (!st) st = run_gemm_tc(wtc, q, n, k, tiled, m, e, s, nullptr, nullptr, false, flags, part, plan);
+  if (flags) cudaFreeAsync(flags, s);
+  if (part) cudaFreeAsync(part, s);
   cudaFreeAsync(codes, s);
   if (tmp) cudaFreeAsync(tmp, s);
   return st;
@@ -518,6 +530,24 @@ int abq_bmma(const uint64_t* a, unsigned a_planes, size_t m, unsigned a_plane, c
 }
 
 // ---- engine ----------------------------------------------------------------
+// TileConfig -> sm_100a engine schedule (the reference's
+// tile, gemm.hpp:19-59, picks the CPU block / warp tiling).  BM (activation
+// rows per block) caps the token tile: the tcgen05 GEMM's UMMA N (16..256) or
+// the AND+popcount kernel's token block (1..8); BK (k depth per block) selects
+// the k-split: BK == 128 -> stream-K over all SMs (CTAs share a row-tile's
+// k-range), deeper -> one CTA per 128-channel row-tile.  Results never depend
+// on it (tile transparency, test_bitkernel.cpp:104-115); time does, so the
+// reference's autotune over tile candidates times different kernels.
+static EnginePlan plan_of(const abq_tile_config* t) {
+  EnginePlan pl{0, ABQ_GEMM_AUTO};
+  if (!t) return pl;
+  int tt = 1;
+  while (tt * 2 <= static_cast<int>(std::min<size_t>(t->BM, 256))) tt *= 2;
+  pl.token_tile = tt;
+  pl.schedule = t->BK <= 128 ? ABQ_GEMM_STREAM_K : ABQ_GEMM_CLASSIC;
+  return pl;
+}
+
 static int gemm_common(const char* name, const uint64_t* a, unsigned p, size_t m, size_t a_k,
                        const uint64_t* bt, unsigned q, size_t n, size_t b_k,
                        const abq_tile_config* tile, bool wide, bool check_overflow, void* out,
@@ -541,13 +571,23 @@ static int gemm_common(const char* name, const uint64_t* a, unsigned p, size_t m
     ABQ_CUDA_TRY(cudaMemsetAsync(out, 0, m * n * (wide ? 8 : 4), as_stream(stream)));
   } else if (m >= 16 && !wide && gemm_tc_supported(a_k) && g_gemv_variant != ABQ_GEMV_POPC) {
     // prefill-shaped: recombined planes on tcgen05 (weights re-laid out per call)
-    st = gemm_tc_from_planes(a, p, m, bt, nullptr, q, n, a_k, raw_epi(out, n, wide), as_stream(stream));
+    st = gemm_tc_from_planes(a, p, m, bt, nullptr, q, n, a_k, raw_epi(out, n, wide), as_stream(stream),
+                             plan_of(tile));
     if (st) return st;
   } else {
-    st = run_gemm_popc(a, p, m, bt, q, n, a_k, wide, raw_epi(out, n, wide), as_stream(stream));
+    st = run_gemm_popc(a, p, m, bt, q, n, a_k, wide, raw_epi(out, n, wide), as_stream(stream),
+                       plan_of(tile).token_tile);
     if (st) return st;
   }
   if (tile) add_stats(stats, *tile, m, n, p, q);
+  return ABQ_OK;
+}
+
+int abq_tile_engine_plan(const abq_tile_config* tile, int* token_tile, int* schedule) {
+  if (!tile || !token_tile || !schedule) return fail(ABQ_ERR_VALUE, "tile_engine_plan: null argument");
+  const EnginePlan pl = plan_of(tile);
+  *token_tile = pl.token_tile;
+  *schedule = pl.schedule;
   return ABQ_OK;
 }
 
@@ -667,6 +707,10 @@ int abq_linear_planes(const abq_act* act, const abq_weights* w, void* y, int out
   if (use_tc(w, act->m, act->k, wide))
     return gemm_tc_from_planes(act->planes, act->p, act->m, w->planes, w->tc, w->q, w->n, act->k, e,
                                as_stream(stream));
+  if (!w->planes)
+    return fail(ABQ_ERR_VALUE,
+                "quantized_linear: no resident weight layout serves m=%zu (the decode layout covers m <= 8, "
+                "the prefill layout m >= 1; the ABQP planes were dropped)", act->m);
   return run_gemm_popc(act->planes, act->p, act->m, w->planes, w->q, w->n, act->k, wide, e,
                        as_stream(stream));
 }

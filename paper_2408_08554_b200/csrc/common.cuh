@@ -26,6 +26,13 @@ struct DecTuning {
   int tc_dbg = 0;    // prefill GEMM: experiment switches (tools/trace_gemm.py), 0 in production
 };
 DecTuning& dec_tuning();
+
+// engine schedule picked from a TileConfig (abi.cu plan_of): token-tile cap
+// (0 = by M) and the prefill GEMM schedule (ABQ_GEMM_*, 0 = auto)
+struct EnginePlan {
+  int token_tile;
+  int schedule;
+};
 int fail(int status, const char* fmt, ...);
 uint64_t& launch_counter();
 int num_sms();

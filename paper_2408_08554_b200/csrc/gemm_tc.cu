@@ -856,11 +856,12 @@ static int launch_tc(const TcParams& P, bool pdl, cudaStream_t st) {
 }
 
 template <int Q>
-static int launch_tt(const TcParams& P, bool pdl, cudaStream_t st) {
-  if (P.m <= 16) return launch_tc<Q, 16>(P, pdl, st);
-  if (P.m <= 32) return launch_tc<Q, 32>(P, pdl, st);
-  if (P.m <= 64) return launch_tc<Q, 64>(P, pdl, st);
-  if (P.m <= 128) return launch_tc<Q, 128>(P, pdl, st);
+static int launch_tt(const TcParams& P, bool pdl, cudaStream_t st, int tt_cap) {
+  const int cap = tt_cap > 0 ? std::max(16, tt_cap) : 256;  // TileConfig BM cap (abi.cu plan_of)
+  if (P.m <= 16 || cap <= 16) return launch_tc<Q, 16>(P, pdl, st);
+  if (P.m <= 32 || cap <= 32) return launch_tc<Q, 32>(P, pdl, st);
+  if (P.m <= 64 || cap <= 64) return launch_tc<Q, 64>(P, pdl, st);
+  if (P.m <= 128 || cap <= 128) return launch_tc<Q, 128>(P, pdl, st);
   return launch_tc<Q, 256>(P, pdl, st);
 }
 
@@ -870,7 +871,7 @@ bool gemm_tc_supported(size_t k) { return k > 0 && k <= 65536 && k % 16 == 0; }
 // act: tiled u8 codes (tc_act_offset, groups = tc_act_groups(m)), 16-B aligned
 int run_gemm_tc(const uint32_t* wtc, unsigned q, size_t n, size_t k, const uint8_t* act, size_t m,
                 const EpiParams& e, cudaStream_t st, unsigned long long* bad_word,
-                unsigned long long* bad_out, bool pdl, unsigned* sk_flags, uint32_t* sk_part) {
+                unsigned long long* bad_out, bool pdl, unsigned* sk_flags, uint32_t* sk_part, EnginePlan plan) {
   if (m == 0 || n == 0) return ABQ_OK;
   TcParams P{};
   P.bad_word = bad_word;
@@ -887,8 +888,9 @@ int run_gemm_tc(const uint32_t* wtc, unsigned q, size_t n, size_t k, const uint8
   P.e = e;
   P.trace = trace_buffer();
   P.dbg = dec_tuning().tc_dbg;
-  // an explicit schedule (abq_set_gemm_schedule) wins; else the default
-  const int sched = gemm_schedule();
+  // a TileConfig's schedule (abi.cu plan_of) wins, then an explicit
+  // abq_set_gemm_schedule; else the default
+  const int sched = plan.schedule != ABQ_GEMM_AUTO ? plan.schedule : gemm_schedule();
   const bool sk_on = sched == ABQ_GEMM_STREAM_K ? true
                      : sched == ABQ_GEMM_CLASSIC ? false
                      : tc_stream_k_auto(P.rowtiles);
@@ -898,14 +900,14 @@ int run_gemm_tc(const uint32_t* wtc, unsigned q, size_t n, size_t k, const uint8
     P.sk_part = sk_part;
   }
   switch (q) {
-    case 1: return launch_tt<1>(P, pdl, st);
-    case 2: return launch_tt<2>(P, pdl, st);
-    case 3: return launch_tt<3>(P, pdl, st);
-    case 4: return launch_tt<4>(P, pdl, st);
-    case 5: return launch_tt<5>(P, pdl, st);
-    case 6: return launch_tt<6>(P, pdl, st);
-    case 7: return launch_tt<7>(P, pdl, st);
-    default: return launch_tt<8>(P, pdl, st);
+    case 1: return launch_tt<1>(P, pdl, st, plan.token_tile);
+    case 2: return launch_tt<2>(P, pdl, st, plan.token_tile);
+    case 3: return launch_tt<3>(P, pdl, st, plan.token_tile);
+    case 4: return launch_tt<4>(P, pdl, st, plan.token_tile);
+    case 5: return launch_tt<5>(P, pdl, st, plan.token_tile);
+    case 6: return launch_tt<6>(P, pdl, st, plan.token_tile);
+    case 7: return launch_tt<7>(P, pdl, st, plan.token_tile);
+    default: return launch_tt<8>(P, pdl, st, plan.token_tile);
   }
 }
 

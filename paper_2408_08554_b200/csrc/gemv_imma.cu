@@ -190,11 +190,8 @@ __global__ void __launch_bounds__(kActThreads) act_quant_kernel(const T* __restr
       double step = 0.0;
       int z = 0;
       float inv32 = 0.0f;
-      if (lane < 2) group_params(qp, unord(l2), unord(h2), &step, &z);
-      if (lane == 1) inv32 = f32_reciprocal_fast(step);
-      step = __shfl_sync(0xffffffffu, step, 0);
-      z = __shfl_sync(0xffffffffu, z, 0);
-      inv32 = __shfl_sync(0xffffffffu, inv32, 1);
+      // every lane (same inputs, same results): one FP64 division, no broadcast
+      group_params_fast(qp, unord(l2), unord(h2), &step, &z, &inv32);
       if (tid == 0) {
         s_a[tok] = step;
         z_a[tok] = z;

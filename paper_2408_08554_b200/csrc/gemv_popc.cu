@@ -209,14 +209,15 @@ static int pick_mt(int m, int p, int wpr) {
 }
 
 int run_gemm_popc(const uint64_t* A, unsigned p, size_t m, const uint64_t* W, unsigned q, size_t n,
-                  size_t k, bool wide, const EpiParams& e, cudaStream_t st) {
+                  size_t k, bool wide, const EpiParams& e, cudaStream_t st, int token_tile) {
   if (m == 0 || n == 0) return ABQ_OK;
   const int wpr = static_cast<int>(wpr_of(k));
   const int ip = static_cast<int>(p), iq = static_cast<int>(q);
   const int im = static_cast<int>(m), in = static_cast<int>(n);
   if (static_cast<size_t>(p) * 1 * ((wpr + 1) & ~1) * 8 > 200 * 1024)
     return fail(ABQ_ERR_VALUE, "gemm: K=%zu too large for the staged activation planes", k);
-  const int mt = pick_mt(im, ip, wpr);
+  int mt = pick_mt(im, ip, wpr);
+  while (token_tile > 0 && mt > 1 && mt > token_tile) mt >>= 1;  // TileConfig BM cap (abi.cu plan_of)
   const bool vec = (wpr % 2) == 0;
   if (wide) {
     if (vec) return launch_mt<0, 0, true, true>(A, ip, im, W, iq, in, wpr, e, mt, st);

@@ -100,3 +100,25 @@ def test_engine_shards_concatenate_to_unsharded(abq, m, n, k, wbits, abits, grou
             parts.append(abq.Linear(shard, spec, max_m=m)(x, out_dtype=torch.float64))
             del shard
         assert torch.equal(torch.cat(parts, dim=1), full), g
+
+
+def test_resident_layouts_one_per_regime(abq, orc):
+    """PackedWeights.resident: one engine layout per serving regime in HBM (the
+    planes dropped): decode-only serves m <= 8 and refuses more, prefill-only
+    serves any m on the tcgen05 GEMM; outputs equal the full object's."""
+    rng = np.random.default_rng(77)
+    n, k = 1024, 4096
+    wc, sb, zb = _layer(rng, n, k, 4)
+    full = abq.PackedWeights.from_planes(abq.bitpack(wc, 4), sb, zb)
+    spec = abq.QuantSpec(bits=4, granularity=abq.api.PER_TOKEN)
+    dec, pre = full.resident("decode"), full.resident("prefill")
+    assert dec.resident_bytes() * 3 == full.resident_bytes() and pre.resident_bytes() * 3 == full.resident_bytes()
+    for m in (1, 8, 16, 128):
+        x = torch.from_numpy(rng.standard_normal((m, k)).astype(np.float16)).cuda()
+        want = abq.Linear(full, spec, max_m=m)(x, out_dtype=torch.float64)
+        assert torch.equal(abq.Linear(pre, spec, max_m=m)(x, out_dtype=torch.float64), want), m
+        if m <= 8:
+            assert torch.equal(abq.Linear(dec, spec, max_m=m)(x, out_dtype=torch.float64), want), m
+        else:
+            with pytest.raises(abq.ValueError):
+                abq.Linear(dec, spec, max_m=m)(x, out_dtype=torch.float64)

@@ -112,3 +112,15 @@ def test_autotune_linear(abq, orc, m, n, k):
     finally:
         abq.set_gemv_variant("auto")
         abq.set_gemm_schedule("auto")
+
+
+def test_tile_maps_to_distinct_engine_schedules():
+    """TileConfig -> engine schedule (abq_tile_engine_plan):
+    BM caps the token tile, BK == 128 selects stream-K; the reference's own
+    candidate lists therefore time different kernels."""
+    from paper_2408_08554_b200.api import tile_engine_plan
+    assert tile_engine_plan(abq.TileConfig(64, 64, 512, 64, 64, 128)) == (64, "classic")
+    assert tile_engine_plan(abq.TileConfig(16, 64, 128, 32, 64, 128)) == (16, "stream_k")
+    assert tile_engine_plan(abq.TileConfig(1, 8, 256, 8, 8, 128))[0] == 1
+    plans = {tile_engine_plan(t) for t in abq.api.enumerate_tile_candidates(4, 4, 128, 11008, 4096)}
+    assert len(plans) >= 2, plans

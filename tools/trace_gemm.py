@@ -24,6 +24,11 @@ for _ in range(3):
     lins[0](x, out=y, check=False)
 torch.cuda.synchronize()
 lib = abq._lib.lib()
+if len(sys.argv) > 3:
+    abq.api.set_gemm_schedule(sys.argv[3])
+    for _ in range(3):
+        lins[0](x, out=y, check=False)
+    torch.cuda.synchronize()
 lib.abq_set_trace_buffer(buf.data_ptr())
 lins[1](x, out=y, check=False)
 torch.cuda.synchronize()
