@@ -427,7 +427,7 @@ def measure_part(abq, torch, name, world, steps, warmup, l2, peaks, peak_kind):
         row["cublas_fp16_TOPS"] = round(2 * m * n * k / cus / 1e6, 2)
         row["speedup_vs_cublas_fp16"] = round(cus / us, 3)
         del wf
-    del lins, cat
+    del lins
     torch.cuda.empty_cache()
     return row
 
@@ -501,7 +501,7 @@ def measure_chain(abq, torch, name, steps, warmup, l2, peaks, peak_kind, world=1
            "unfused_GBps": round(layer_bytes / (uus * 1e-6) / 1e9, 1),
            "note": "fused: RMSNorm/SiLU*up producers emit the codes, q/k/v and gate/up run as one concatenated "
                    "launch each; unfused: 7 separate GEMVs each re-quantizing its fp16 input in its prologue"}
-    del lins
+    del lins, cat
     torch.cuda.empty_cache()
     return row
 

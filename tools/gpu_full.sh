@@ -1,0 +1,6 @@
+# full GPU check: the -m gpu suite, smoke, sanitizers, driver-shaped bench
+O=gpurun_out; T=${1:-full}
+timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider > $O/${T}_pytest.log 2>&1; echo "rc=$?" >> $O/${T}_pytest.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/${T}_smoke.log 2>&1; echo "rc=$?" >> $O/${T}_smoke.log
+bash tools/gpu_sanitize.sh $T
+timeout 900 python bench.py --steps 20 --warmup 5 > $O/${T}_bench20.json 2> $O/${T}_bench20.err
