@@ -114,7 +114,10 @@ static __device__ __noinline__ void report_nonfinite_f16(const uint4* xr, int t,
   } while (0)
 #endif
 
-template <int QT, int MT>
+// FUSED: fp16 activations quantized in the prologue (P.x16); else codes +
+// stats from a preceding kernel (two instantiations: each launch only fetches
+// the code of its own prologue)
+template <int QT, int MT, bool FUSED>
 __global__ void __launch_bounds__(kDecThreads, kDecCtasPerSm) gemv_dec_kernel(const __grid_constant__ DecParams P) {
   constexpr int NW = kDecWarps, UPS = kDecUPS, NG = NW / UPS;
   constexpr int unit_bytes = QT * 512;
@@ -197,12 +200,13 @@ __global__ void __launch_bounds__(kDecThreads, kDecCtasPerSm) gemv_dec_kernel(co
     __syncwarp();
     if (lane == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncwarp();
+#pragma unroll 1
     for (int i = lane; i < min(S, P.preslots) && i < nsl; i += 32) issue_slot(i, i);
   }
   // zeroed row-tile sums, zero codes past K
   for (int idx = tid; idx < nlrt * 16 * MT; idx += kDecThreads) accs[idx] = 0;
   const int tok_n = min(MT, P.m);
-  if (P.x16) {
+  if constexpr (FUSED) {
     const int k4 = P.k >> 2, ntail = (kpad >> 2) - k4;
     for (int idx = tid; idx < ntail * MT; idx += kDecThreads) act[act_frag_index(k4 + idx / MT, idx % MT, MT)] = 0u;
   }
@@ -212,7 +216,7 @@ __global__ void __launch_bounds__(kDecThreads, kDecCtasPerSm) gemv_dec_kernel(co
   // ---- 2. the activations, which the previous kernel may still be producing
   asm volatile("griddepcontrol.wait;" ::: "memory");
   DEC_STAMP(2, clock64());
-  if (P.x16) {
+  if constexpr (FUSED) {
     // Fused ReQuant, per token, fp16 rows (K % 8 == 0, K <= 32 * TPT: the host
     // routes longer rows through act_quant_kernel).  GT warps per token; each
     // thread loads its (<= XR) 16-byte vectors of the row in one batch.
@@ -231,8 +235,10 @@ __global__ void __launch_bounds__(kDecThreads, kDecCtasPerSm) gemv_dec_kernel(co
       xv[r] = active && v < nvec ? __ldg(xr + v) : make_uint4(0u, 0u, 0u, 0u);
     }
     // the rest of the ring only now, behind the activation loads
-    if (warp == 0)
+    if (warp == 0) {
+#pragma unroll 1
       for (int i = P.preslots + lane; i < S && i < nsl; i += 32) issue_slot(i, i);
+    }
     // min / max in the order-preserving integer image of fp32 (exact for fp16
     // inputs): one REDUX per warp
     auto ord = [](float f) {
@@ -325,8 +331,10 @@ __global__ void __launch_bounds__(kDecThreads, kDecCtasPerSm) gemv_dec_kernel(co
       za = P.z_a[tid];
       ra = P.rowsum[tid];
     }
-    if (warp == 0)
+    if (warp == 0) {
+#pragma unroll 1
       for (int i = P.preslots + lane; i < S && i < nsl; i += 32) issue_slot(i, i);
+    }
 #pragma unroll
     for (int r = 0; r < CR; ++r) {
       const int idx = tid + r * kDecThreads;
@@ -518,7 +526,7 @@ __global__ void __launch_bounds__(kDecThreads, kDecCtasPerSm) gemv_dec_kernel(co
       c_cs[idx] = P.e.colsum_b[j];
     }
   }
-  if (P.x16 && tid < tok_n) {
+  if (FUSED && tid < tok_n) {
     constexpr int GT = NW / MT;
     long long s = 0;
 #pragma unroll
@@ -574,7 +582,7 @@ DecTuning& dec_tuning() {
 
 template <int QT, int MT>
 static int launch_dec2(const DecParams& P, int grid, size_t smem, bool pdl, cudaStream_t st) {
-  auto kern = gemv_dec_kernel<QT, MT>;
+  auto kern = P.x16 ? gemv_dec_kernel<QT, MT, true> : gemv_dec_kernel<QT, MT, false>;
   if (smem > 220 * 1024) return fail(ABQ_ERR_VALUE, "gemv_dec: shared memory plan too large (%zu B)", smem);
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (err == cudaSuccess)
