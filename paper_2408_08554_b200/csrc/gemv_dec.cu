@@ -64,6 +64,7 @@ struct DecParams {
   EpiParams e;
   unsigned long long* bad_word;  // non-finite input report (see run_gemv_dec)
   unsigned long long* bad_out;
+  int xr;        // fused prologue: 16-byte activation vectors per thread
   int slots;     // TMA ring slots of kDecUPS units
   int preslots;  // ring slots issued before the activations are awaited
   unsigned long long* trace;  // ABQ_TRACE build only: [grid][64] stamps
@@ -117,8 +118,11 @@ static __device__ __noinline__ void report_nonfinite_f16(const uint4* xr, int t,
 // FUSED: fp16 activations quantized in the prologue (P.x16); else codes +
 // stats from a preceding kernel (two instantiations: each launch only fetches
 // the code of its own prologue)
-template <int QT, int MT, bool FUSED>
+// XF > 0: fused, XF 16-byte activation vectors per thread (1, 2 or 4: the
+// smallest that covers K, so short rows do not carry the unrolled code of long ones)
+template <int QT, int MT, int XF>
 __global__ void __launch_bounds__(kDecThreads, kDecCtasPerSm) gemv_dec_kernel(const __grid_constant__ DecParams P) {
+  constexpr bool FUSED = XF > 0;
   constexpr int NW = kDecWarps, UPS = kDecUPS, NG = NW / UPS;
   constexpr int unit_bytes = QT * 512;
   constexpr int slot_bytes = UPS * unit_bytes;
@@ -222,7 +226,7 @@ __global__ void __launch_bounds__(kDecThreads, kDecCtasPerSm) gemv_dec_kernel(co
     // thread loads its (<= XR) 16-byte vectors of the row in one batch.
     constexpr int GT = NW / MT;  // MT is a power of two <= NW
     constexpr int TPT = GT * 32;
-    constexpr int XR = kDecXR;
+    constexpr int XR = XF > 0 ? XF : 1;
     const int t = warp / GT;
     const int l = (warp % GT) * 32 + lane;
     const int nvec = P.k >> 3;
@@ -582,7 +586,9 @@ DecTuning& dec_tuning() {
 
 template <int QT, int MT>
 static int launch_dec2(const DecParams& P, int grid, size_t smem, bool pdl, cudaStream_t st) {
-  auto kern = P.x16 ? gemv_dec_kernel<QT, MT, true> : gemv_dec_kernel<QT, MT, false>;
+  auto kern = !P.x16 ? gemv_dec_kernel<QT, MT, 0>
+              : P.xr <= 1 ? gemv_dec_kernel<QT, MT, 1>
+              : P.xr <= 2 ? gemv_dec_kernel<QT, MT, 2> : gemv_dec_kernel<QT, MT, 4>;
   if (smem > 220 * 1024) return fail(ABQ_ERR_VALUE, "gemv_dec: shared memory plan too large (%zu B)", smem);
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (err == cudaSuccess)
@@ -719,6 +725,8 @@ int run_gemv_dec(const uint32_t* frag, unsigned q, size_t n, size_t k, size_t m,
                      k <= static_cast<size_t>(8 * kDecXR * 32 * kDecWarps / mt);
   if (fused) {
     P.x16 = static_cast<const __half*>(x);
+    const size_t tpt = 32 * kDecWarps / mt, nvec = k / 8;
+    P.xr = nvec <= tpt ? 1 : nvec <= 2 * tpt ? 2 : 4;
   } else {
     const int rc = run_act_quant(x, x_dtype, m, k, mt, qp, act_frag, 0, s_a, z_a, rowsum, P.bad_word, st);
     if (rc) return rc;

@@ -133,10 +133,18 @@ __device__ __forceinline__ float f32_reciprocal_fast(double step) {
 // qz is farther than max(|qz|, 1) * 2^-20 from the nearest n + 1/2 (then both
 // round to rint(qz)); otherwise, and for |qz| >= 2^22, by the IEEE quotient.
 // One FP64 division (step) on the prologue's critical path instead of three.
+// the rare paths out of line: the prologue's inline code stays small (it is
+// fetched from L2 by every launch)
+static __device__ __noinline__ void group_params_ool(const QuantParams& qp, double lo_raw, double hi_raw,
+                                                     double* step_out, int* z_out) {
+  group_params(qp, lo_raw, hi_raw, step_out, z_out);
+}
+static __device__ __noinline__ double round_div_ool(double a, double b) { return round(a / b); }
+
 __device__ __forceinline__ void group_params_fast(const QuantParams& qp, double lo_raw, double hi_raw,
                                                   double* step_out, int* z_out, float* inv_out) {
   if (qp.scheme != ABQ_ASYMMETRIC) {
-    group_params(qp, lo_raw, hi_raw, step_out, z_out);
+    group_params_ool(qp, lo_raw, hi_raw, step_out, z_out);
     *inv_out = f32_reciprocal_fast(*step_out);
     return;
   }
@@ -156,7 +164,7 @@ __device__ __forceinline__ void group_params_fast(const QuantParams& qp, double 
   const float d = __fsub_rn(0.5f, fabsf(__fsub_rn(q, r)));
   double zz = (fabsf(q) < 4194304.0f && d > fmaxf(fabsf(q), 1.0f) * 9.5367431640625e-07f)  // 2^22, 2^-20
                   ? static_cast<double>(r)
-                  : round(-lo / step);
+                  : round_div_ool(-lo, step);
   const double top = static_cast<double>(qp.levels - 1);
   zz = zz < 0.0 ? 0.0 : (top < zz ? top : zz);
   *step_out = step;
