@@ -740,6 +740,59 @@ class Weights {
   detail::DeviceBuffer<std::uint32_t> tc_;
 };
 
+/// Per-token quantized decode activations made by a producer op with the
+/// ReQuant fused in (rmsnorm_quant / silu_mul_quant below), in
+/// the decode GEMV's code layout; one QAct feeds every projection reading it.
+class QAct {
+ public:
+  QAct(std::size_t m, std::size_t k, const QuantSpec& spec)
+      : m_(m), k_(k), spec_(spec), codes_(abq_qact_codes_bytes(m, k) / 4), scales_(m), zps_(m), rows_(m) {
+    spec.validate();
+  }
+  abq_qact view() const {
+    return abq_qact{codes_.get(), scales_.get(), zps_.get(), rows_.get(), m_, k_, spec_.bits};
+  }
+  const QuantSpec& spec() const { return spec_; }
+  std::size_t m() const { return m_; }
+  std::size_t k() const { return k_; }
+  /// per-token s_a / z_a / code row sums, copied to the host
+  std::vector<double> scales() const {
+    std::vector<double> v(m_);
+    scales_.to_host(v.data());
+    return v;
+  }
+  std::vector<std::int32_t> zero_points() const {
+    std::vector<std::int32_t> v(m_);
+    zps_.to_host(v.data());
+    return v;
+  }
+
+ private:
+  std::size_t m_, k_;
+  QuantSpec spec_;
+  detail::DeviceBuffer<std::uint32_t> codes_;
+  detail::DeviceBuffer<double> scales_;
+  detail::DeviceBuffer<std::int32_t> zps_;
+  detail::DeviceBuffer<std::int64_t> rows_;
+};
+
+/// LLaMA RMSNorm y = gain * fp16(x * rsqrt(mean(x^2) + eps)) (device fp16
+/// [m][k], gain [k]; y_out may be null) with the per-token ReQuant of y fused
+/// in (toyblock.hpp:257 -> quantizer.hpp:146-213).
+inline void rmsnorm_quant(const void* x, const void* gain, float eps, std::size_t m, std::size_t k, QAct& out,
+                          void* y_out = nullptr, cudaStream_t stream = nullptr) {
+  const abq_quant_spec s = out.spec().c_spec();
+  const abq_qact v = out.view();
+  detail::check(abq_rmsnorm_quant(x, gain, eps, m, k, &s, y_out, &v, nullptr, stream));
+}
+/// y = fp16(fp16(silu(gate)) * up) with the per-token ReQuant of y fused in.
+inline void silu_mul_quant(const void* gate, const void* up, std::size_t m, std::size_t k, QAct& out,
+                           void* y_out = nullptr, cudaStream_t stream = nullptr) {
+  const abq_quant_spec s = out.spec().c_spec();
+  const abq_qact v = out.view();
+  detail::check(abq_silu_mul_quant(gate, up, m, k, &s, y_out, &v, nullptr, stream));
+}
+
 /// ReQuant + BitPacking + plane GEMV/GEMM + fused epilogue on device pointers.
 class Linear {
  public:
@@ -756,6 +809,12 @@ class Linear {
     if (m > max_m_) throw ValueError("device::Linear: m exceeds max_m");
     detail::check(abq_linear(x, x_dtype, m, w_.k, &spec_, &w_, y, out_kind, ws_.get(), ws_bytes_,
                              err_index, stream));
+  }
+  /// decode linear on producer-quantized activations (one GEMV launch)
+  void operator()(const QAct& act, void* y, int out_kind, cudaStream_t stream = nullptr) const {
+    if (act.m() > max_m_) throw ValueError("device::Linear: m exceeds max_m");
+    const abq_qact v = act.view();
+    detail::check(abq_linear_qact(&v, &w_, y, out_kind, stream));
   }
 
  private:

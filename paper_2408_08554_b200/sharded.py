@@ -42,10 +42,11 @@ def gather_columns(y_local: torch.Tensor, n_full: int, group=None) -> torch.Tens
         buf = torch.empty((world, m, width), dtype=src.dtype, device=src.device)
         dist.all_gather_into_tensor(buf, src, group=group)
         parts = [buf[r, :, :hi - lo] for r, (lo, hi) in enumerate(bounds)]
-    else:
-        lst = [torch.empty_like(src) for _ in range(world)]
-        dist.all_gather(lst, src, group=group)
-        parts = [lst[r][:, :hi - lo] for r, (lo, hi) in enumerate(bounds)]
+    else:  # gloo: host buffers (device tensors are staged through the host)
+        host = src.cpu()
+        lst = [torch.empty_like(host) for _ in range(world)]
+        dist.all_gather(lst, host, group=group)
+        parts = [lst[r][:, :hi - lo].to(src.device) for r, (lo, hi) in enumerate(bounds)]
     if m == 1 and all(hi - lo == width for lo, hi in bounds) and dist.get_backend(group) == "nccl":
         return buf.view(1, world * width)  # decode: already contiguous [1][N]
     return torch.cat(parts, dim=1)

@@ -12,6 +12,8 @@
 #include <set>
 #include <string>
 
+#include <cuda_fp16.h>
+
 #include "abq/abq.hpp"
 
 using namespace abq;
@@ -291,6 +293,42 @@ static void case_tune() {
   report(ok, "tune: reference candidate list, validity, errors, verified autotune");
 }
 
+// SURVEY.md 8f-2 through the C++ drop-in: RMSNorm with the ReQuant fused in,
+// consumed by the decode GEMV, equals the one-call linear on the producer's own
+// fp16 output (both quantize the same y, quantizer.hpp:146-213), for several
+// projections; one resident layout per regime (Layouts::Decode).
+static void case_producer_qact() {
+  bool ok = true;
+  Rng rng(61);
+  const std::size_t m = 2, k = 4096, n = 1536;
+  std::vector<__half> xh(m * k), gh(k);
+  for (auto& v : xh) v = __float2half(static_cast<float>(rng.gauss()));
+  for (auto& v : gh) v = __float2half(static_cast<float>(rng.uniform(0.5, 1.5)));
+  detail::DeviceBuffer<__half> x(xh), g(gh), y(m * k);
+  QuantSpec aspec;
+  aspec.bits = 4;
+  aspec.granularity = Granularity::PerToken;
+  device::QAct qa(m, k, aspec);
+  device::rmsnorm_quant(x.get(), g.get(), 1e-6f, m, k, qa, y.get());
+  for (int proj = 0; proj < 3; ++proj) {
+    QuantSpec wspec;
+    wspec.bits = 4;
+    wspec.granularity = Granularity::PerChannel;
+    const QuantizedTensor wt = quantize(rng.gauss_matrix(n, k, 0.02), wspec);
+    const device::Weights wd(wt, proj == 2 ? device::Layouts::Decode : device::Layouts::All);
+    const device::Linear lin(wd, aspec, m);
+    detail::DeviceBuffer<double> y1(m * n), y2(m * n);
+    lin(qa, y1.get(), ABQ_OUT_F64);
+    lin(y.get(), ABQ_F16, m, y2.get(), ABQ_OUT_F64);
+    std::vector<double> h1(m * n), h2(m * n);
+    y1.to_host(h1.data());
+    y2.to_host(h2.data());
+    CHECK(h1 == h2);
+    if (proj == 2) CHECK(wd.resident_bytes() == abq_weights_frag_bytes(4, n, k));
+  }
+  report(ok, "producer-fused ReQuant (rmsnorm_quant -> QAct -> Linear) == one-call linear on its output");
+}
+
 int main() {
   case_bitpack();
   case_bmma();
@@ -301,6 +339,7 @@ int main() {
   case_acceptance_1000();
   case_quantizer_and_padding();
   case_tune();
+  case_producer_qact();
   std::printf("%d failure(s)\n", failures);
   return failures;
 }

@@ -26,7 +26,7 @@ def test_cpp_drop_in_api():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert r.stdout.count("PASS") == 9
+    assert r.stdout.count("PASS") == 10
 
 
 @pytest.mark.gpu

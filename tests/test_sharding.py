@@ -1,7 +1,8 @@
 """N-sharded linear on 2 ranks over gloo (CPU): the channel split, the
 all-gather reassembly (M=1 and M>1, equal and unequal shards) and bit-identity
-with the unsharded result.  The per-rank compute here is the oracle standing in
-for the GPU engine (the GPU path itself is covered by the -m gpu tests)."""
+with the unsharded result.  The per-rank compute of the CPU test is the oracle standing in
+for the GPU engine; the -m gpu test runs the same sharding over the engine itself
+(two ranks sharing the one GPU of a gpurun box)."""
 import os
 import socket
 
@@ -73,3 +74,45 @@ def test_shard_bounds_cover_channels():
             assert b[0][0] == 0 and b[-1][1] == n
             assert all(b[i][1] == b[i + 1][0] for i in range(g - 1))
             assert max(hi - lo for lo, hi in b) - min(hi - lo for lo, hi in b) <= 1
+
+
+def _engine_worker(rank, world, port, q):
+    """two ranks on one GPU, gloo collective: ShardedLinear over the ENGINE
+    (PackedWeights.shard + Linear on each rank's channel slice) vs the
+    unsharded engine Linear, bit for bit."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import paper_2408_08554_b200 as abq
+    from paper_2408_08554_b200.sharded import ShardedLinear
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        for (m, n, k, wbits, abits, seed) in [(1, 1728, 5120, 2, 8, 1), (4, 1000, 2048, 4, 4, 2),
+                                              (64, 1024, 8192, 4, 4, 3)]:
+            rng = np.random.default_rng(seed)
+            wc = rng.integers(0, 1 << wbits, (n, k), dtype=np.uint8)
+            sb = rng.uniform(1e-3, 1e-2, n)
+            zb = rng.integers(0, 1 << wbits, n).astype(np.int32)
+            x = torch.from_numpy(rng.standard_normal((m, k)).astype(np.float16)).cuda()
+            w = abq.PackedWeights.from_planes(abq.bitpack(wc, wbits), sb, zb)
+            spec = abq.QuantSpec(bits=abits, granularity=abq.api.PER_TOKEN)
+            y = ShardedLinear(w, spec, max_m=m)(x, out_dtype=torch.float64)
+            full = abq.Linear(w, spec, max_m=m)(x, out_dtype=torch.float64)
+            q.put((rank, m, n, bool(torch.equal(y.cpu(), full.cpu()))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_sharded_engine_linear_gloo_two_ranks_one_gpu():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_engine_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=300) for _ in range(2 * 3)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert all(ok for (*_, ok) in results), results
