@@ -6,7 +6,9 @@ import subprocess
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 BUILD = os.path.join(ROOT, "paper_2408_08554_b200", "csrc", "build")
 WANT = {
-    "gemv_dec": ["gemv_dec_kernelILi4ELi1E", "gemv_dec_kernelILi2ELi1E", "gemv_dec_kernelILi8ELi1E"],
+    "gemv_dec": ["gemv_dec_kernelILi4ELi1ELi1E", "gemv_dec_kernelILi2ELi1ELi1E", "gemv_dec_kernelILi8ELi1ELi1E",
+                 "gemv_dec_kernelILi4ELi1ELi0E"],
+    "producer": ["rmsnorm_quant_kernel", "silu_mul_quant_kernel"],
     "gemm_tc": ["gemm_tc_kernelILi4ELi128E", "gemm_tc_kernelILi8ELi128E"],
     "gemv_popc": ["gemv_popc_kernelILi4ELi4ELi8ELi2ELb0ELb1E", "gemv_popc_kernelILi8ELi2ELi8ELi4ELb0ELb1E"],
     "gemv_imma": ["act_quant_kernelI6__halfLb0E", "act_quant_kernelI6__halfLb1E", "gemv_imma_kernelILi4ELi1ELb1E",
