@@ -429,6 +429,7 @@ int abq_set_tuning(const char* key, long long value) {
   if (k == "dec_pre_kb" && value >= -1) t.pre_kb = static_cast<int>(value);
   else if (k == "dec_ring_kb" && value >= 0) t.ring_kb = static_cast<int>(value);
   else if (k == "dec_pdl") t.pdl = value != 0;
+  else if (k == "dec_pace_ns" && value >= 0) t.pace_ns = static_cast<int>(value);
   else if (k == "tc_dbg") t.tc_dbg = static_cast<int>(value);
   else if (k == "reset") t = DecTuning{};
   else return fail(ABQ_ERR_VALUE, "abq_set_tuning: unknown key or bad value '%s'=%lld", key, value);

@@ -23,6 +23,7 @@ struct DecTuning {
   int pre_kb = -1;   // decode GEMV: weight-ring KB issued before the activations are awaited (-1 = auto)
   int ring_kb = 0;   // decode GEMV: ring size cap in KB (0 = the CTA's whole share when it fits)
   int pdl = 1;       // decode GEMV: programmatic dependent launch
+  int pace_ns = 0;   // decode GEMV: producer-warp slot spacing while awaiting activations (0 = auto)
   int tc_dbg = 0;    // prefill GEMM: experiment switches (tools/trace_gemm.py), 0 in production
 };
 DecTuning& dec_tuning();

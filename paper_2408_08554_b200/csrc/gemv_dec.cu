@@ -46,7 +46,8 @@ namespace abq_dev {
 
 constexpr int kDecWarps = 16;  // 4 per SM sub-partition, <= 128 registers each
 constexpr int kDecUPS = 8;     // units per ring slot = warps sharing a slot
-constexpr int kDecThreads = kDecWarps * 32;
+constexpr int kDecThreads = kDecWarps * 32;  // consumer threads
+constexpr int kDecBlock = kDecThreads + 32;   // + one TMA producer warp
 constexpr int kDecCtasPerSm = 1;
 constexpr int kDecXR = 4;      // fused ReQuant: 16-byte activation vectors per thread
 
@@ -65,11 +66,14 @@ struct DecParams {
   unsigned long long* bad_word;  // non-finite input report (see run_gemv_dec)
   unsigned long long* bad_out;
   int xr;        // fused prologue: 16-byte activation vectors per thread
+  int pace_ns;   // producer warp: spacing of the ring slots issued while the activations are awaited
   int slots;     // TMA ring slots of kDecUPS units
   int preslots;  // ring slots issued before the activations are awaited
   unsigned long long* trace;  // ABQ_TRACE build only: [grid][64] stamps
 };
 
+// named barrier over the consumer warps (the producer warp has exited)
+__device__ __forceinline__ void cta_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kDecThreads) : "memory"); }
 __device__ __forceinline__ void mbar_init_n(uint64_t* bar, unsigned n) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(n));
 }
@@ -121,7 +125,7 @@ static __device__ __noinline__ void report_nonfinite_f16(const uint4* xr, int t,
 // XF > 0: fused, XF 16-byte activation vectors per thread (1, 2 or 4: the
 // smallest that covers K, so short rows do not carry the unrolled code of long ones)
 template <int QT, int MT, int XF>
-__global__ void __launch_bounds__(kDecThreads, kDecCtasPerSm) gemv_dec_kernel(const __grid_constant__ DecParams P) {
+__global__ void __launch_bounds__(kDecBlock, kDecCtasPerSm) gemv_dec_kernel(const __grid_constant__ DecParams P) {
   constexpr bool FUSED = XF > 0;
   constexpr int NW = kDecWarps, UPS = kDecUPS, NG = NW / UPS;
   constexpr int unit_bytes = QT * 512;
@@ -135,8 +139,10 @@ __global__ void __launch_bounds__(kDecThreads, kDecCtasPerSm) gemv_dec_kernel(co
   __shared__ int s_za[MT];
   __shared__ long long s_ra[MT];
   __shared__ int r_sum[NW];  // per-warp code sums of the fused ReQuant
+  __shared__ int x_flag;     // consumers -> producer warp: activation loads issued
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool prod = warp == NW;  // the TMA producer warp (no activations, no compute)
   asm volatile("griddepcontrol.launch_dependents;");
 #ifdef ABQ_TRACE
   unsigned long long* trace = P.trace ? P.trace + 64 * blockIdx.x : nullptr;
@@ -176,7 +182,7 @@ __global__ void __launch_bounds__(kDecThreads, kDecCtasPerSm) gemv_dec_kernel(co
   // it; stored to shared memory only after the main loop
   const bool dequant = P.e.mode != EPI_ACC_I32 && P.e.mode != EPI_ACC_I64;
   const int pj = rt_first * kRowTile + tid;
-  const bool has_p = dequant && tid < nlrt * 16 && pj < P.n;
+  const bool has_p = !prod && dequant && tid < nlrt * 16 && pj < P.n;
   double p_sb = 0.0;
   int p_zb = 0;
   long long p_cs = 0;
@@ -194,27 +200,56 @@ __global__ void __launch_bounds__(kDecThreads, kDecCtasPerSm) gemv_dec_kernel(co
     tma_bulk_g2s_hint(ring + static_cast<size_t>(sl) * slot_bytes, wsrc + static_cast<size_t>(i) * slot_bytes, bytes,
                       &full[sl], pol);
   };
-  // ---- 1. ring: warp 0 lane s initialises barrier s and, once the
-  // initialisation is fenced, issues slot s (for s < preslots)
-  if (warp == 0) {
+  // ---- 1. ring: the producer warp's lane s initialises barrier s; the
+  // slots are issued after the set-up barrier (below)
+  if (prod) {
     if (lane < S) {
       mbar_init_n(&full[lane], 1);
       relcnt[lane] = 0;
     }
+    if (lane == 0) x_flag = 0;
     __syncwarp();
     if (lane == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncwarp();
+    // the slots issued up front go out before the set-up barrier
 #pragma unroll 1
     for (int i = lane; i < min(S, P.preslots) && i < nsl; i += 32) issue_slot(i, i);
   }
   // zeroed row-tile sums, zero codes past K
-  for (int idx = tid; idx < nlrt * 16 * MT; idx += kDecThreads) accs[idx] = 0;
   const int tok_n = min(MT, P.m);
-  if constexpr (FUSED) {
-    const int k4 = P.k >> 2, ntail = (kpad >> 2) - k4;
-    for (int idx = tid; idx < ntail * MT; idx += kDecThreads) act[act_frag_index(k4 + idx / MT, idx % MT, MT)] = 0u;
+  if (!prod) {
+    for (int idx = tid; idx < nlrt * 16 * MT; idx += kDecThreads) accs[idx] = 0;
+    if constexpr (FUSED) {
+      const int k4 = P.k >> 2, ntail = (kpad >> 2) - k4;
+      for (int idx = tid; idx < ntail * MT; idx += kDecThreads) act[act_frag_index(k4 + idx / MT, idx % MT, MT)] = 0u;
+    }
   }
   __syncthreads();  // barrier initialisation and the zeroed state visible
+  if (prod) {
+    // The weights are input-independent.  Fused path: while the consumers
+    // await the activations (the previous kernel may still be running), one
+    // ring slot per pace_ns -- about the SM's share of HBM bandwidth, so at most
+    // ~one slot is queued ahead of the activation loads when the wait returns --
+    // then, once the activation loads are issued, the rest at once.  Other
+    // paths: everything at once (the preceding kernel's run covers it).
+    const int lim = min(S, nsl);
+    int i = min(lim, P.preslots);
+    if constexpr (FUSED) {
+      if (lane == 0) {
+        while (i < lim && *reinterpret_cast<volatile int*>(&x_flag) == 0) {
+          if (P.pace_ns > 0) {
+            issue_slot(i, i);
+            ++i;
+          }
+          __nanosleep(P.pace_ns > 0 ? P.pace_ns : 64);
+        }
+      }
+      i = __shfl_sync(0xffffffffu, i, 0);
+    }
+#pragma unroll 1
+    for (int j = i + lane; j < lim; j += 32) issue_slot(j, j);  // the rest, one slot per lane
+    return;
+  }
   DEC_STAMP(1, clock64());
 
   // ---- 2. the activations, which the previous kernel may still be producing
@@ -238,11 +273,8 @@ __global__ void __launch_bounds__(kDecThreads, kDecCtasPerSm) gemv_dec_kernel(co
       const int v = l + r * TPT;
       xv[r] = active && v < nvec ? __ldg(xr + v) : make_uint4(0u, 0u, 0u, 0u);
     }
-    // the rest of the ring only now, behind the activation loads
-    if (warp == 0) {
-#pragma unroll 1
-      for (int i = P.preslots + lane; i < S && i < nsl; i += 32) issue_slot(i, i);
-    }
+    // activation loads issued: the producer warp issues the rest of the ring
+    if (tid == 0) *reinterpret_cast<volatile int*>(&x_flag) = 1;
     // min / max in the order-preserving integer image of fp32 (exact for fp16
     // inputs): one REDUX per warp
     auto ord = [](float f) {
@@ -274,7 +306,7 @@ __global__ void __launch_bounds__(kDecThreads, kDecCtasPerSm) gemv_dec_kernel(co
       r_lo[warp] = lo;
       r_hi[warp] = hi;
     }
-    __syncthreads();
+    cta_sync();
     DEC_STAMP(3, clock64());
     if (active) {
       const int base = warp - warp % GT;  // first warp of this token
@@ -335,10 +367,6 @@ __global__ void __launch_bounds__(kDecThreads, kDecCtasPerSm) gemv_dec_kernel(co
       za = P.z_a[tid];
       ra = P.rowsum[tid];
     }
-    if (warp == 0) {
-#pragma unroll 1
-      for (int i = P.preslots + lane; i < S && i < nsl; i += 32) issue_slot(i, i);
-    }
 #pragma unroll
     for (int r = 0; r < CR; ++r) {
       const int idx = tid + r * kDecThreads;
@@ -356,7 +384,7 @@ __global__ void __launch_bounds__(kDecThreads, kDecCtasPerSm) gemv_dec_kernel(co
       *P.bad_word = 0ull;
     }
   }
-  __syncthreads();
+  cta_sync();
   DEC_STAMP(5, clock64());
 
   // ---- 3. main loop.  Local unit l = warp + NW j lives in ring slot index
@@ -537,7 +565,7 @@ __global__ void __launch_bounds__(kDecThreads, kDecCtasPerSm) gemv_dec_kernel(co
     for (int w2 = 0; w2 < GT; ++w2) s += r_sum[tid * GT + w2];
     s_ra[tid] = s;
   }
-  __syncthreads();
+  cta_sync();
   DEC_STAMP(6, clock64());
 
   // ---- 4. epilogue: zero-point correction + dequant of this CTA's channels
@@ -596,7 +624,7 @@ static int launch_dec2(const DecParams& P, int grid, size_t smem, bool pdl, cuda
   if (err != cudaSuccess) return fail(ABQ_ERR_CUDA, "gemv_dec: smem attribute: %s", cudaGetErrorString(err));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kDecThreads);
+  cfg.blockDim = dim3(kDecBlock);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -761,6 +789,12 @@ static int launch_dec(DecParams& P, size_t m, bool fused, bool qact, cudaStream_
   // overlaps; measured best in the LLaMA-7B decode chain, profiles/r02_chain_prekb_sweep.txt)
   (void)qact;
   P.preslots = fused ? std::max(0, std::min(P.slots, static_cast<int>(pre_kb * 1024 / slot_bytes))) : P.slots;
+  // (measured: ~4x the SM's ~43 B/ns share of HBM bandwidth is best, profiles/r02_dec_pace_sweep.txt)
+  // Paced slots only when the ring holds the whole share; a refilled ring
+  // keeps its 64 KB up front and waits for the activation loads.
+  P.pace_ns = dec_tuning().pace_ns > 0 ? dec_tuning().pace_ns
+              : P.slots >= whole         ? static_cast<int>(slot_bytes / 160)
+                                         : 0;
   const size_t smem = dec_smem(q, P.slots, mt, kpad, nl).total;
   const bool pdl = dec_tuning().pdl != 0;
   switch (mt) {
