@@ -108,6 +108,12 @@ static __device__ __noinline__ void report_nonfinite_f16(const uint4* xr, int t,
   }
 }
 
+// raw accumulator outputs (gemm_arbitrary modes) out of line: the serving
+// epilogue's inline code stays small
+static __device__ __noinline__ void epi_store_raw(const EpiParams& E, long long i, long long j, long long acc) {
+  epi_store_v(E, i, j, acc, 0.0, 0, 0);
+}
+
 #ifdef ABQ_TRACE
 #define DEC_STAMP(slot, value)                  \
   do {                                          \
@@ -139,6 +145,7 @@ __global__ void __launch_bounds__(kDecBlock, kDecCtasPerSm) gemv_dec_kernel(cons
   __shared__ int s_za[MT];
   __shared__ long long s_ra[MT];
   __shared__ int r_sum[NW];  // per-warp code sums of the fused ReQuant
+  __shared__ float s_inv[MT], s_thr[MT];  // fused ReQuant: RN32(1/step), tie-band threshold
   __shared__ int x_flag;     // consumers -> producer warp: activation loads issued
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -308,23 +315,34 @@ __global__ void __launch_bounds__(kDecBlock, kDecCtasPerSm) gemv_dec_kernel(cons
     }
     cta_sync();
     DEC_STAMP(3, clock64());
-    if (active) {
-      const int base = warp - warp % GT;  // first warp of this token
-      int l2 = lane < GT ? r_lo[base + lane] : 0x7FFFFFFF;
-      int h2 = lane < GT ? r_hi[base + lane] : static_cast<int>(0x80000000u);
+    // step / zero point in FP64 (quantizer.hpp:169-201), the fp32 reciprocal
+    // and the per-token tie-band threshold: computed ONCE per token (the first
+    // warp of the token) and shared -- all 16 warps redundantly computing them
+    // cost more issue slots than the extra barrier
+    if (active && warp % GT == 0) {
+      int l2 = lane < GT ? r_lo[warp + lane] : 0x7FFFFFFF;
+      int h2 = lane < GT ? r_hi[warp + lane] : static_cast<int>(0x80000000u);
       l2 = __reduce_min_sync(0xffffffffu, l2);
       h2 = __reduce_max_sync(0xffffffffu, h2);
-      // step / zero point in FP64 (quantizer.hpp:169-201), every lane (same
-      // inputs, same results: no divergence, no broadcast)
-      double step = 0.0;
-      int z = 0;
-      float inv32 = 0.0f;
-      group_params_fast(P.qp, unord(l2), unord(h2), &step, &z, &inv32);
-      if (warp == base && lane == 0) {
-        s_sa[t] = step;
-        s_za[t] = z;
+      if (lane == 0) {
+        // step / zero point (quantizer.hpp:169-201) out of line: this code
+        // runs once per launch, and the kernel's code footprint is what it
+        // costs (the instruction cache does not hold the whole kernel)
+        const float flo = unord(l2), fhi = unord(h2);
+        const StepZ sz = group_params_ool(P.qp, flo, fhi);
+        const float inv32 = f32_reciprocal_fast(sz.step);
+        s_sa[t] = sz.step;
+        s_za[t] = sz.z;
+        s_inv[t] = inv32;
+        s_thr[t] = band_threshold(flo, fhi, inv32);
       }
-      DEC_STAMP(4, clock64());
+    }
+    cta_sync();
+    DEC_STAMP(4, clock64());
+    if (active) {
+      const double step = s_sa[t];
+      const int z = s_za[t];
+      const float inv32 = s_inv[t], thr = s_thr[t];
       const int topi = static_cast<int>(P.qp.levels - 1);
       int rsum = 0;
 #pragma unroll
@@ -332,7 +350,7 @@ __global__ void __launch_bounds__(kDecBlock, kDecCtasPerSm) gemv_dec_kernel(cons
         const int v = l + r * TPT;
         if (v >= nvec) break;
         uint32_t w0, w1;
-        rsum += quant_codes8_f16(xv[r], step, inv32, z, topi, &w0, &w1);
+        rsum += quant_codes8_f16_band(xv[r], step, inv32, thr, z, topi, &w0, &w1);
         act[act_frag_index(2 * v, t, MT)] = w0;
         act[act_frag_index(2 * v + 1, t, MT)] = w1;
       }
@@ -576,7 +594,7 @@ __global__ void __launch_bounds__(kDecBlock, kDecCtasPerSm) gemv_dec_kernel(cons
     if (i >= tok_n || j >= P.n) continue;
     const long long a = accs[idx];
     if (!dequant) {
-      epi_store_v(E, i, j, a, 0.0, 0, 0);
+      epi_store_raw(E, i, j, a);
       continue;
     }
     const long long za = s_za[i], zb = c_zb[rc];

@@ -133,19 +133,28 @@ __device__ __forceinline__ float f32_reciprocal_fast(double step) {
 // qz is farther than max(|qz|, 1) * 2^-20 from the nearest n + 1/2 (then both
 // round to rint(qz)); otherwise, and for |qz| >= 2^22, by the IEEE quotient.
 // One FP64 division (step) on the prologue's critical path instead of three.
-// the rare paths out of line: the prologue's inline code stays small (it is
-// fetched from L2 by every launch)
-static __device__ __noinline__ void group_params_ool(const QuantParams& qp, double lo_raw, double hi_raw,
-                                                     double* step_out, int* z_out) {
-  group_params(qp, lo_raw, hi_raw, step_out, z_out);
+// the rare paths out of line (small inline code).  Results are returned BY
+// VALUE: an out-of-line callee writing through pointers puts the caller's
+// variables in local memory, and a local-memory miss behind the SM's TMA weight
+// stream is a full L2 round trip on the critical path.
+struct StepZ {
+  double step;
+  int z;
+};
+static __device__ __noinline__ StepZ group_params_ool(QuantParams qp, double lo_raw, double hi_raw) {
+  StepZ r;
+  group_params(qp, lo_raw, hi_raw, &r.step, &r.z);
+  return r;
 }
 static __device__ __noinline__ double round_div_ool(double a, double b) { return round(a / b); }
 
 __device__ __forceinline__ void group_params_fast(const QuantParams& qp, double lo_raw, double hi_raw,
                                                   double* step_out, int* z_out, float* inv_out) {
   if (qp.scheme != ABQ_ASYMMETRIC) {
-    group_params_ool(qp, lo_raw, hi_raw, step_out, z_out);
-    *inv_out = f32_reciprocal_fast(*step_out);
+    const StepZ r = group_params_ool(qp, lo_raw, hi_raw);
+    *step_out = r.step;
+    *z_out = r.z;
+    *inv_out = f32_reciprocal_fast(r.step);
     return;
   }
   const double lo = __dmul_rn(qp.beta, lo_raw);
@@ -232,6 +241,88 @@ __device__ __forceinline__ int quant_codes8_f16(const uint4& xv, double step, fl
   }
   if (!ok) {
     const uint3 r = quant_codes8_exact(xv, step, z, top);
+    *w0 = r.x;
+    *w1 = r.y;
+    return static_cast<int>(r.z);
+  }
+  *w0 = static_cast<uint32_t>(c[0]) | (static_cast<uint32_t>(c[1]) << 8) | (static_cast<uint32_t>(c[2]) << 16) |
+        (static_cast<uint32_t>(c[3]) << 24);
+  *w1 = static_cast<uint32_t>(c[4]) | (static_cast<uint32_t>(c[5]) << 8) | (static_cast<uint32_t>(c[6]) << 16) |
+        (static_cast<uint32_t>(c[7]) << 24);
+  return c[0] + c[1] + c[2] + c[3] + c[4] + c[5] + c[6] + c[7];
+}
+
+// The exact step is only needed on the tie path: LazyStep carries what it is
+// computed from (group_params, out of line) instead of the step itself.
+struct LazyStep {
+  const QuantParams* qp;
+  float lo, hi;
+};
+static __device__ __noinline__ uint3 quant_codes8_exact_lazy(uint4 xv, QuantParams qp, float lo, float hi, int z,
+                                                             int top) {
+  const StepZ r = group_params_ool(qp, lo, hi);
+  return quant_codes8_exact(xv, r.step, z, top);
+}
+
+// Asymmetric per-token zero point and reciprocal step for the CODES, on the
+// fp32 pipe (the exact FP64 step -- s_a for the epilogue -- is computed off the
+// critical path): step32 = RN32(RN32(hi - lo) RN32(1/(L-1))), inv32 =
+// RN32(1/step32) is within (1 + 2^-24)^4 - 1 < 2^-21.99 of 1/step; codes with
+// it stay within 5 * 2^-24 < 2^-21 (the tie band) of v/step, and the zero point
+// qz = RN32(-lo inv32) within 2^-21.6 < 2^-20 (its band here).  Returns false
+// (caller takes group_params_fast) for other schemes, alpha or beta != 1, a
+// zero point inside its band, or a step outside the normal range.
+__device__ __forceinline__ bool codes_params_f32(const QuantParams& qp, float lo, float hi, float* inv_out,
+                                                 int* z_out) {
+  if (qp.scheme != ABQ_ASYMMETRIC || qp.alpha != 1.0 || qp.beta != 1.0) return false;
+  if (hi == lo) {  // degenerate range: step 1, zero point 0 (quantizer.hpp:176-178)
+    *inv_out = 1.0f;
+    *z_out = 0;
+    return true;
+  }
+  const float step32 = __fmul_rn(__fsub_rn(hi, lo), __frcp_rn(static_cast<float>(qp.levels - 1)));
+  if (!(step32 > 0x1p-100f && step32 < 0x1p100f)) return false;
+  const float inv32 = __frcp_rn(step32);
+  const float q = __fmul_rn(-lo, inv32);
+  const float t = __fadd_rn(q, 12582912.0f);
+  const float d = __fsub_rn(0.5f, fabsf(__fsub_rn(q, __fsub_rn(t, 12582912.0f))));
+  if (!(fabsf(q) < 4194304.0f && d > fmaxf(fabsf(q), 1.0f) * 9.5367431640625e-07f)) return false;  // 2^22, 2^-20
+  const int top = static_cast<int>(qp.levels - 1), zi = __float_as_int(t) - 0x4B400000;
+  *inv_out = inv32;
+  *z_out = zi < 0 ? 0 : (zi > top ? top : zi);
+  return true;
+}
+
+// Per-token form of the quant_codes8_f16 test: with Qmax >= |q| for every
+// element of the token (band_threshold), |q - rint(q)| < thr = 0.5 - max(Qmax,
+// 1) 2^-21 implies the element is outside the tie band of quant_code_f32, so
+// one compare per element replaces the per-element band arithmetic.
+__device__ __forceinline__ float band_threshold(float lo, float hi, float inv32) {
+  const float qmax = __fmul_ru(fmaxf(fabsf(lo), fabsf(hi)), __fmul_ru(inv32, 1.0000010f));  // >= every |q|
+  return qmax < 4194304.0f ? 0.5f - fmaxf(qmax, 1.0f) * 4.76837158203125e-07f : -1.0f;  // -1: all exact
+}
+template <typename StepT>
+__device__ __forceinline__ int quant_codes8_f16_band(const uint4& xv, StepT step, float inv32, float thr, int z,
+                                                     int top, uint32_t* w0, uint32_t* w1) {
+  const __half2* h2 = reinterpret_cast<const __half2*>(&xv);
+  int c[8];
+  bool ok = true;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float2 f = __half22float2(h2[e]);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const float q = __fmul_rn(h ? f.y : f.x, inv32);
+      const float t = __fadd_rn(q, 12582912.0f);  // 1.5 * 2^23: rint(q) in the low mantissa bits
+      ok = ok && fabsf(__fsub_rn(q, __fsub_rn(t, 12582912.0f))) < thr;
+      const int ci = (__float_as_int(t) - 0x4B400000) + z;
+      c[2 * e + h] = ci < 0 ? 0 : (ci > top ? top : ci);
+    }
+  }
+  if (!ok) {
+    uint3 r;
+    if constexpr (sizeof(StepT) == sizeof(double)) r = quant_codes8_exact(xv, step, z, top);
+    else r = quant_codes8_exact_lazy(xv, *step.qp, step.lo, step.hi, z, top);
     *w0 = r.x;
     *w1 = r.y;
     return static_cast<int>(r.z);

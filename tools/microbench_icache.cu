@@ -61,8 +61,15 @@ int main() {
       if (load) stream_kernel<<<sms * 4, 256, 0, s2>>>(buf, big / 16, sink);
       probe<<<sms, 512, 0, s1>>>(out, 2);  // grid of sms CTAs (may share SMs with the stream kernel)
       cudaDeviceSynchronize();
+      cudaMemcpy(h, out, sms * 4 * 8, cudaMemcpyDeviceToHost);
+      double a0 = 0, a1 = 0;
+      for (int i = 0; i < sms; ++i) {
+        a0 += h[i * 4];
+        a1 += h[i * 4 + 1];
+      }
+      printf("  launch %d (stream %s): first pass %.0f, second pass %.0f cycles\n", rep, load ? "on" : "off", a0 / sms,
+             a1 / sms);
     }
-    cudaMemcpy(h, out, sms * 4 * 8, cudaMemcpyDeviceToHost);
     double c0 = 0, c1 = 0;
     for (int i = 0; i < sms; ++i) {
       c0 += h[i * 4];

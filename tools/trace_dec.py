@@ -61,6 +61,8 @@ for i, t in enumerate(rows):
     marks = [np.median(t[:, c] - t[:, 0]) / ghz / 1e3 for c in range(1, 8)]
     print(f"  launch {i:2d}: span {(e - a) / 1e3:6.2f} us{gap}  (CTA start skew {(t[:, 8].max() - a) / 1e3:5.2f} us)")
     print("             " + ", ".join(f"{nm} {v:.2f}" for nm, v in zip(names, marks)))
+    sp = [np.median(t[:, c] - t[:, 3]) / ghz / 1e3 for c in (10, 11, 4)]
+    print("             step phase (us after range): reductions %.2f, group_params %.2f, stored %.2f" % tuple(sp))
     d = [np.median(t[:, c] - t[:, 5]) / ghz / 1e3 for c in (16, 17, 18, 19, 20)]
     we = (t[:, 24:40] - t[:, 5:6]) / ghz / 1e3
     print("             main loop (warp 0, us after codes): start %.2f, first data %.2f, first fold %.2f, loop end %.2f, flush end %.2f;"
