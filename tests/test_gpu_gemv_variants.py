@@ -178,3 +178,31 @@ def test_serving_gemv_llama_shapes(abq, orc, m, n, k, wb, ab):
     want = orc.quantized_linear(ac, ab, sa, za, wc, wb, sb, zb)
     assert np.array_equal(y64, want)
     assert np.array_equal(y16, want.astype(np.float16))
+
+
+def test_serving_linear_random_shapes_vs_oracle(abq, orc):
+    """Fuzz of the serving entry point (fused-ReQuant decode GEMV with its TMA
+    producer warp, ring refills, ragged N / K tails; the tcgen05 prefill GEMM)
+    against the oracle, bit for bit: 60 random (m, n, k, q, p) incl. shares
+    larger than the ring."""
+    rng = np.random.default_rng(2024)
+    cases = []
+    for i in range(60):
+        if i % 10 == 0:    # shares larger than the ring (refills), decode
+            m, n, k = int(rng.integers(1, 9)), int(rng.integers(9000, 24000)), int(rng.integers(512, 1024)) * 8
+        elif i % 4 == 0:   # prefill
+            m, n, k = int(rng.integers(9, 160)), int(rng.integers(1, 1500)), int(rng.integers(1, 512)) * 8
+        else:              # decode, ragged N, K multiple of 8 or not (ReQuant-kernel path)
+            m, n = int(rng.integers(1, 9)), int(rng.integers(1, 3000))
+            k = int(rng.integers(1, 1600)) * 8 if i % 3 else int(rng.integers(1, 9000))
+        wb, ab = (int(v) for v in rng.integers(1, 9, 2))
+        cases.append((m, n, k, wb, ab))
+    from oracle.oracle import exact_linear
+    for (m, n, k, wb, ab) in cases:
+        x, wc, sb, zb = _case(rng, m, n, k, wb, ab)
+        w = abq.PackedWeights.from_planes(abq.bitpack(wc, wb), sb, zb)
+        lin = abq.Linear(w, abq.QuantSpec(bits=ab, granularity=abq.api.PER_TOKEN), max_m=m)
+        y = lin(torch.from_numpy(x).cuda(), out_dtype=torch.float64).cpu().numpy()
+        ac, sa, za = orc.quantize(x.astype(np.float64), ab, 0, 2)
+        want = exact_linear(ac, sa, za, wc, sb, zb)
+        assert np.array_equal(y, want), (m, n, k, wb, ab)
