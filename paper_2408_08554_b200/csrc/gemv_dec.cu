@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(kDecBlock, kDecCtasPerSm) gemv_dec_kernel(cons
     int i = min(lim, P.preslots);
     if constexpr (FUSED) {
       if (lane == 0) {
-        while (i < lim && *reinterpret_cast<volatile int*>(&x_flag) == 0) {
+        while (i < lim && atomicAdd(&x_flag, 0) == 0) {  // (a timing hint only: an atomic poll)
           if (P.pace_ns > 0) {
             issue_slot(i, i);
             ++i;
@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(kDecBlock, kDecCtasPerSm) gemv_dec_kernel(cons
       xv[r] = active && v < nvec ? __ldg(xr + v) : make_uint4(0u, 0u, 0u, 0u);
     }
     // activation loads issued: the producer warp issues the rest of the ring
-    if (tid == 0) *reinterpret_cast<volatile int*>(&x_flag) = 1;
+    if (tid == 0) atomicExch(&x_flag, 1);
     // min / max in the order-preserving integer image of fp32 (exact for fp16
     // inputs): one REDUX per warp
     auto ord = [](float f) {
