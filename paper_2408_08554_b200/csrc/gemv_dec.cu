@@ -231,7 +231,10 @@ __global__ void __launch_bounds__(kDecBlock, kDecCtasPerSm) gemv_dec_kernel(cons
       for (int idx = tid; idx < ntail * MT; idx += kDecThreads) act[act_frag_index(k4 + idx / MT, idx % MT, MT)] = 0u;
     }
   }
-  __syncthreads();  // barrier initialisation and the zeroed state visible
+  // barrier initialisation and the zeroed state visible to the consumers; the
+  // producer warp only ARRIVES (it does not wait for the consumers' set-up)
+  if (prod) asm volatile("bar.arrive 0, %0;" ::"n"(kDecBlock) : "memory");
+  else asm volatile("bar.sync 0, %0;" ::"n"(kDecBlock) : "memory");
   if (prod) {
     // The weights are input-independent.  Fused path: while the consumers
     // await the activations (the previous kernel may still be running), one
