@@ -139,6 +139,7 @@ __global__ void __launch_bounds__(kDecBlock, kDecCtasPerSm) gemv_dec_kernel(cons
   constexpr bool RAW = (QT & (QT - 1)) == 0;  // q in {1, 2, 4, 8}: raw masked fields
   constexpr int NF = RAW ? 8 / QT : 1;         // fields (scales) per byte lane
   constexpr int NA = NF >= 2 ? NF : 2;         // accumulators per set (>= 2 independent chains)
+  constexpr int FSH = RAW && NF >= 2 ? QT * (NF - 1) : 0;  // folded row-tile sums hold 2^FSH * the sum
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ int r_lo[NW], r_hi[NW];
   __shared__ double s_sa[MT];
@@ -457,13 +458,15 @@ __global__ void __launch_bounds__(kDecBlock, kDecCtasPerSm) gemv_dec_kernel(cons
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       const int row = g + 8 * (r >> 1), tok = 2 * tig + (r & 1);
-      if (tok < tok_n) atomicAdd(&accs[(lrt * 16 + row) * MT + tok], tot[r]);
+      if (tok < tok_n) atomicAdd(&accs[(lrt * 16 + row) * MT + tok], tot[r] >> FSH);
       tot[r] = 0u;
     }
   };
   // fold a unit's accumulator set into the row-tile sums.  Field f holds
-  // 2^(QT f) * its partial sum exactly (every per-unit sum is < 2^31; the
-  // row-tile sum < 2^32 for K <= 65536); the fields are divided out exactly.
+  // 2^(QT f) * its partial sum S_f exactly; ((acc_0 << QT) + acc_1) << QT ... =
+  // 2^FSH * sum_f S_f (one shift-add per field, LEA); the per-warp row-tile sums
+  // stay below 2^32 (<= 16 units of <= 2^FSH * 255 * 255 * 256 each for K <=
+  // 65536) and 2^FSH is divided out exactly before the shared atomic.
   auto fold = [&](int (&acc)[NA][4], int r_t) {
     if (r_t != tot_rt) {
       flush_tot();
@@ -471,11 +474,11 @@ __global__ void __launch_bounds__(kDecBlock, kDecCtasPerSm) gemv_dec_kernel(cons
     }
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
-      uint32_t v = 0;
+      uint32_t v = static_cast<uint32_t>(acc[0][r]);
+      acc[0][r] = 0;
 #pragma unroll
-      for (int f = 0; f < NA; ++f) {
-        const int sh = RAW && NF >= 2 ? QT * f : 0;
-        v += static_cast<uint32_t>(acc[f][r]) >> sh;
+      for (int f = 1; f < NA; ++f) {
+        v = (FSH ? (v << QT) : v) + static_cast<uint32_t>(acc[f][r]);
         acc[f][r] = 0;
       }
       tot[r] += v;
