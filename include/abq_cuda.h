@@ -307,7 +307,8 @@ int abq_get_gemm_schedule(void);
  * the defaults are the measured best): "dec_pre_kb" (decode GEMV weight-ring
  * KB issued before the activations are awaited, default 64), "dec_ring_kb"
  * (ring cap, 0 = whole CTA share), "dec_pdl" (0/1), "tc_dbg" (prefill GEMM
- * experiment switches, tools/trace_gemm.py), "reset".  Returns ABQ_ERR_VALUE
+ * experiment switches, tools/trace_gemm.py), "tc_tt" (prefill token-tile cap),
+ * "dec_pace_ns" (decode producer-warp slot spacing), "reset".  Returns ABQ_ERR_VALUE
  * for an unknown key. */
 int abq_set_tuning(const char* key, long long value);
 

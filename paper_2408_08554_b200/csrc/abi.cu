@@ -431,6 +431,7 @@ int abq_set_tuning(const char* key, long long value) {
   else if (k == "dec_pdl") t.pdl = value != 0;
   else if (k == "dec_pace_ns" && value >= 0) t.pace_ns = static_cast<int>(value);
   else if (k == "tc_dbg") t.tc_dbg = static_cast<int>(value);
+  else if (k == "tc_tt" && value >= 0) t.tc_tt = static_cast<int>(value);
   else if (k == "reset") t = DecTuning{};
   else return fail(ABQ_ERR_VALUE, "abq_set_tuning: unknown key or bad value '%s'=%lld", key, value);
   return ABQ_OK;

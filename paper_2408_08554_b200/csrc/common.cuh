@@ -25,6 +25,7 @@ struct DecTuning {
   int pdl = 1;       // decode GEMV: programmatic dependent launch
   int pace_ns = 0;   // decode GEMV: producer-warp slot spacing while awaiting activations (0 = auto)
   int tc_dbg = 0;    // prefill GEMM: experiment switches (tools/trace_gemm.py), 0 in production
+  int tc_tt = 0;     // prefill GEMM: token-tile cap for the serving path (0 = by M)
 };
 DecTuning& dec_tuning();
 

@@ -888,6 +888,7 @@ int run_gemm_tc(const uint32_t* wtc, unsigned q, size_t n, size_t k, const uint8
   P.e = e;
   P.trace = trace_buffer();
   P.dbg = dec_tuning().tc_dbg;
+  if (plan.token_tile == 0 && dec_tuning().tc_tt > 0) plan.token_tile = dec_tuning().tc_tt;
   // a TileConfig's schedule (abi.cu plan_of) wins, then an explicit
   // abq_set_gemm_schedule; else the default
   const int sched = plan.schedule != ABQ_GEMM_AUTO ? plan.schedule : gemm_schedule();
