@@ -281,6 +281,22 @@ int abq_silu_mul_quant(const void* gate, const void* up, size_t m, size_t k, con
  * GEMV launch, no ReQuant phases on its critical path. */
 int abq_linear_qact(const abq_qact* act, const abq_weights* w, void* y, int out_kind, void* stream);
 
+/* ---- end-to-end serving with host buffers ----------------------------------
+ * abq_stage_in: device dst <- pinned host src (read over PCIe by a kernel
+ * through the UVA address; 16-B aligned), PDL-chained: the loads are issued as
+ * soon as the kernel starts (overlapping the previous kernel), the stores after
+ * griddepcontrol.wait, so a following engine linear starts streaming its
+ * weights early and only its activation read waits for the copy.  The engine
+ * linears accept pinned host memory as their output y (the epilogue writes the
+ * result over PCIe): one H2D kernel + one linear per step, no copy nodes. */
+int abq_stage_in(void* dst, const void* src_host, size_t bytes, void* stream);
+/* abq_stage_in(x_stage <- x_host) + abq_linear(x_stage -> y_host) in one call
+ * (x_host / y_host pinned host memory, x_stage an m*k device buffer): the
+ * end-to-end serving step on host buffers. */
+int abq_linear_host(const void* x_host, int x_dtype, size_t m, size_t k, void* x_stage,
+                    const abq_quant_spec* act_spec, const abq_weights* w, void* y_host, int out_kind,
+                    void* workspace, size_t workspace_bytes, int64_t* err_index, void* stream);
+
 /* ---- kernel selection (decode GEMV variants) -------------- */
 typedef enum {
   ABQ_GEMV_AUTO = 0,

@@ -98,6 +98,9 @@ _SIGNATURES = {
     "abq_qact_codes_bytes": (_S, [_S, _S]),
     "abq_rmsnorm_quant": (_I, [_P, _P, C.c_float, _S, _S, C.POINTER(QuantSpecC), _P, C.POINTER(QActC), _P, _P]),
     "abq_silu_mul_quant": (_I, [_P, _P, _S, _S, C.POINTER(QuantSpecC), _P, C.POINTER(QActC), _P, _P]),
+    "abq_stage_in": (_I, [_P, _P, _S, _P]),
+    "abq_linear_host": (_I, [_P, _I, _S, _S, _P, C.POINTER(QuantSpecC), C.POINTER(WeightsC), _P, _I, _P, _S,
+                             _P, _P]),
     "abq_linear_qact": (_I, [C.POINTER(QActC), C.POINTER(WeightsC), _P, _I, _P]),
     "abq_set_gemv_variant": (_I, [_I]),
     "abq_get_gemv_variant": (_I, []),

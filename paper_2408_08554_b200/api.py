@@ -76,6 +76,12 @@ def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
     return t.data_ptr()
 
 
+def _out_ptr(t: torch.Tensor) -> int:
+    """device tensor, or pinned host tensor (its UVA address: the engine
+    writes it over PCIe)"""
+    return t.data_ptr() if (t.device.type == "cpu" and t.is_pinned()) else _ptr(t)
+
+
 def _stream() -> int:
     return torch.cuda.current_stream().cuda_stream
 
@@ -921,11 +927,13 @@ class Linear:
         else:
             if out.dtype not in _OUT:
                 raise ValueError(f"Linear: unsupported output dtype {out.dtype}")
-            if tuple(out.shape) != (m, n) or not out.is_contiguous() or out.device != x.device:
-                raise ShapeError(f"Linear: out must be a contiguous ({m}, {n}) tensor on {x.device}")
+            # (pinned host memory is accepted too: the epilogue writes it over PCIe)
+            if tuple(out.shape) != (m, n) or not out.is_contiguous() or \
+                    (out.device != x.device and not (out.device.type == "cpu" and out.is_pinned())):
+                raise ShapeError(f"Linear: out must be a contiguous ({m}, {n}) tensor on {x.device} or pinned host")
         # x.shape[1] (not self.k): the C-ABI rejects an inner-dimension mismatch
         _check(L.lib().abq_linear(_ptr(x), _dtype_code(x), m, x.shape[1], C.byref(self._sc),
-                                  C.byref(self._wc), _ptr(out), _OUT[out.dtype], _ptr(self.ws),
+                                  C.byref(self._wc), _out_ptr(out), _OUT[out.dtype], _ptr(self.ws),
                                   self.ws_bytes, None if check else _ptr(self.err), _stream()))
         if not check:
             self._last_k = x.shape[1]
@@ -950,6 +958,41 @@ class Linear:
         if v != -1:
             k = getattr(self, "_last_k", self.k)
             raise ValueError(f"quantize: non-finite element at ({v // k},{v % k})")
+
+
+class HostLinear:
+    """End-to-end serving call on host buffers, without copy nodes: step()
+    stages the pinned host activations into HBM with a kernel (abq_stage_in:
+    PCIe loads issued at once, stores after the previous kernel completes) and
+    runs the engine linear with its epilogue writing y straight into pinned
+    host memory.  Both launches are programmatic-dependent, so consecutive
+    steps overlap like a chain of layers (the next step's weights stream while
+    the previous step finishes).  The caller synchronises before reading y_host."""
+
+    def __init__(self, lin: "Linear", m: int, x_dtype=torch.float16, out_dtype=torch.float16):
+        self.lin = lin
+        k, n = lin.k, lin.w.planes.rows
+        self.x_host = torch.empty((m, k), dtype=x_dtype, pin_memory=True)
+        self.y_host = torch.empty((m, n), dtype=out_dtype, pin_memory=True)
+        self.x_dev = torch.empty((m, k), dtype=x_dtype, device=_dev())
+        self.h2d_bytes = self.x_host.numel() * self.x_host.element_size()
+        self.d2h_bytes = self.y_host.numel() * self.y_host.element_size()
+        if self.y_host.dtype not in _OUT:
+            raise ValueError(f"HostLinear: unsupported output dtype {out_dtype}")
+        # one C call per step (abq_linear_host) with its arguments bound once:
+        # the step is otherwise host-bound on Python / ctypes overhead
+        self._fn = L.lib().abq_linear_host
+        self._stream = _stream()
+        self._args = (self.x_host.data_ptr(), _dtype_code(self.x_dev), m, k, _ptr(self.x_dev), C.byref(lin._sc),
+                      C.byref(lin._wc), self.y_host.data_ptr(), _OUT[self.y_host.dtype], _ptr(lin.ws), lin.ws_bytes,
+                      _ptr(lin.err), self._stream)
+
+    def step(self) -> torch.Tensor:
+        """one step on the stream current at construction; raises on error"""
+        st = self._fn(*self._args)
+        if st:
+            _check(st)
+        return self.y_host
 
 
 class GraphedLinear:

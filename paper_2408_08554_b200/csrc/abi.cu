@@ -91,6 +91,7 @@ int run_gemv_dec_qact(const uint32_t* frag, unsigned q, size_t n, size_t k, size
                       const double* s_a, const int32_t* z_a, const long long* rowsum, const QuantParams& qp,
                       const EpiParams& e, cudaStream_t st);
 size_t qact_codes_bytes(size_t m, size_t k);
+int run_stage_in(void* dst, const void* src, size_t bytes, cudaStream_t st);
 bool qact_supported(size_t m, size_t k);
 int run_rmsnorm_quant(const __half* x, const __half* gain, float eps, size_t m, size_t k, const QuantParams& qp,
                       __half* y_out, uint32_t* codes, double* s_a, int32_t* z_a, long long* rowsum,
@@ -198,6 +199,8 @@ static QuantParams params_of(const abq_quant_spec& s) {
 }
 
 static int check_device() {
+  static thread_local bool ok = false;  // a device, once seen, stays
+  if (ok) return ABQ_OK;
   int n = 0;
   cudaError_t e = cudaGetDeviceCount(&n);
   if (e != cudaSuccess || n == 0) {
@@ -205,6 +208,7 @@ static int check_device() {
     return fail(ABQ_ERR_CUDA, "abq: no CUDA device available (%s); the engine has no CPU path",
                 cudaGetErrorString(e));
   }
+  ok = true;
   return ABQ_OK;
 }
 
@@ -394,6 +398,13 @@ int abq_silu_mul_quant(const void* gate, const void* up, size_t m, size_t k, con
                               static_cast<__half*>(y_out), out->codes, out->scales, out->zero_points,
                               reinterpret_cast<long long*>(out->rowsums), err, s);
   });
+}
+
+int abq_stage_in(void* dst, const void* src_host, size_t bytes, void* stream) {
+  if (!dst || !src_host) return fail(ABQ_ERR_VALUE, "stage_in: null buffer");
+  int st = check_device();
+  if (st) return st;
+  return run_stage_in(dst, src_host, bytes, as_stream(stream));
 }
 
 int abq_linear_qact(const abq_qact* act, const abq_weights* w, void* y, int out_kind, void* stream) {
@@ -834,6 +845,18 @@ int abq_linear(const void* x, int x_dtype, size_t m, size_t k, const abq_quant_s
   if (b != ~0ull)
     return fail(ABQ_ERR_VALUE, "quantize: non-finite element at (%llu,%llu)", b / k, b % k);
   return ABQ_OK;
+}
+
+int abq_linear_host(const void* x_host, int x_dtype, size_t m, size_t k, void* x_stage,
+                    const abq_quant_spec* act_spec, const abq_weights* w, void* y_host, int out_kind,
+                    void* workspace, size_t workspace_bytes, int64_t* err_index, void* stream) {
+  if (!x_host || !x_stage || !y_host) return fail(ABQ_ERR_VALUE, "linear_host: null buffer");
+  const size_t esize = x_dtype == ABQ_F16 ? 2 : x_dtype == ABQ_F32 ? 4 : 8;
+  int st = check_device();
+  if (st) return st;
+  if ((st = run_stage_in(x_stage, x_host, m * k * esize, as_stream(stream)))) return st;
+  return abq_linear(x_stage, x_dtype, m, k, act_spec, w, y_host, out_kind, workspace, workspace_bytes, err_index,
+                    stream);
 }
 
 }  // extern "C"

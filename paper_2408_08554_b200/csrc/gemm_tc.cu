@@ -823,8 +823,15 @@ template <int Q, int TT>
 static int launch_tc(const TcParams& P, bool pdl, cudaStream_t st) {
   using Sh = TcShape<Q, TT>;
   auto kern = gemm_tc_kernel<Q, TT>;
-  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Sh::kSmem);
-  if (err != cudaSuccess) return fail(ABQ_ERR_CUDA, "gemm_tc: smem attribute: %s", cudaGetErrorString(err));
+  static bool attr_set[64] = {false};  // once per instantiation and device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || !attr_set[dev]) {
+    const cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Sh::kSmem);
+    if (err != cudaSuccess) return fail(ABQ_ERR_CUDA, "gemm_tc: smem attribute: %s", cudaGetErrorString(err));
+    if (dev >= 0 && dev < 64) attr_set[dev] = true;
+  }
+  cudaError_t err = cudaSuccess;
   TcParams L = P;
   const int gy = (P.m + TT - 1) / TT;
   int gx = P.rowtiles;

@@ -642,9 +642,19 @@ static int launch_dec2(const DecParams& P, int grid, size_t smem, bool pdl, cuda
               : P.xr <= 1 ? gemv_dec_kernel<QT, MT, 1>
               : P.xr <= 2 ? gemv_dec_kernel<QT, MT, 2> : gemv_dec_kernel<QT, MT, 4>;
   if (smem > 220 * 1024) return fail(ABQ_ERR_VALUE, "gemv_dec: shared memory plan too large (%zu B)", smem);
-  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  if (err == cudaSuccess)
-    err = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  // the attributes are set once per instantiation and device (and raised when
+  // a larger plan needs it): they are host API calls on every launch otherwise
+  static size_t set_smem[4][64] = {};  // [kernel variant][device]
+  const int var = !P.x16 ? 0 : P.xr <= 1 ? 1 : P.xr <= 2 ? 2 : 3;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaError_t err = cudaSuccess;
+  if (dev < 0 || dev >= 64 || smem > set_smem[var][dev]) {
+    err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (err == cudaSuccess)
+      err = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    if (err == cudaSuccess && dev >= 0 && dev < 64) set_smem[var][dev] = smem;
+  }
   if (err != cudaSuccess) return fail(ABQ_ERR_CUDA, "gemv_dec: smem attribute: %s", cudaGetErrorString(err));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);

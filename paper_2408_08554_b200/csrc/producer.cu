@@ -17,6 +17,8 @@
 // One CTA per token, kProdThreads threads, the row kept in registers.
 #include <math_constants.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "gemv_frag.cuh"
 #include "quant_dev.cuh"
@@ -207,6 +209,35 @@ __global__ void __launch_bounds__(kProdThreads) silu_mul_quant_kernel(
   requant_row_f16(v, nvec, k, tok, mt, kpad, qp, codes, s_a, z_a, rowsum, err, sm);
 }
 
+// ---- stage-in of host activations (end-to-end serving path) --------------------
+// dst (device) <- src (pinned host memory, read over PCIe through its UVA
+// address): the loads are issued first, then griddepcontrol.wait (the previous
+// kernel in the stream may still read dst), then the stores.  PDL: launched
+// early, the PCIe read latency overlaps the previous kernel's tail.
+__global__ void __launch_bounds__(256) stage_in_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src,
+                                                       size_t n16, unsigned char* __restrict__ dst_tail,
+                                                       const unsigned char* __restrict__ src_tail, int tail) {
+  asm volatile("griddepcontrol.launch_dependents;");
+  constexpr int R = 4;
+  const size_t base = static_cast<size_t>(blockIdx.x) * 256 * R + threadIdx.x;
+  uint4 v[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const size_t i = base + static_cast<size_t>(r) * 256;
+    if (i < n16) v[r] = src[i];
+  }
+  unsigned char t = 0;
+  const bool has_tail = blockIdx.x == 0 && static_cast<int>(threadIdx.x) < tail;
+  if (has_tail) t = src_tail[threadIdx.x];
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const size_t i = base + static_cast<size_t>(r) * 256;
+    if (i < n16) dst[i] = v[r];
+  }
+  if (has_tail) dst_tail[threadIdx.x] = t;
+}
+
 // ---- host ---------------------------------------------------------------------
 size_t qact_codes_bytes(size_t m, size_t k) {
   const size_t mt = static_cast<size_t>(qact_mt(m));
@@ -230,6 +261,21 @@ static int launch_pdl(const void* fn, dim3 grid, dim3 block, void** args, cudaSt
   if (err != cudaSuccess) return fail(ABQ_ERR_CUDA, "producer launch: %s", cudaGetErrorString(err));
   ABQ_LAUNCHED();
   return ABQ_OK;
+}
+
+int run_stage_in(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  if (bytes == 0) return ABQ_OK;
+  if ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15)
+    return fail(ABQ_ERR_VALUE, "stage_in: 16-byte aligned buffers required");
+  size_t n16 = bytes / 16;
+  int tail = static_cast<int>(bytes - n16 * 16);
+  uint4* d = static_cast<uint4*>(dst);
+  const uint4* s = static_cast<const uint4*>(src);
+  unsigned char* dt = static_cast<unsigned char*>(dst) + n16 * 16;
+  const unsigned char* stl = static_cast<const unsigned char*>(src) + n16 * 16;
+  const unsigned grid = static_cast<unsigned>(std::max<size_t>(1, (n16 + 1023) / 1024));
+  void* args[] = {&d, &s, &n16, &dt, &stl, &tail};
+  return launch_pdl(reinterpret_cast<const void*>(stage_in_kernel), dim3(grid), dim3(256), args, st);
 }
 
 int run_rmsnorm_quant(const __half* x, const __half* gain, float eps, size_t m, size_t k, const QuantParams& qp,

@@ -206,3 +206,26 @@ def test_serving_linear_random_shapes_vs_oracle(abq, orc):
         ac, sa, za = orc.quantize(x.astype(np.float64), ab, 0, 2)
         want = exact_linear(ac, sa, za, wc, sb, zb)
         assert np.array_equal(y, want), (m, n, k, wb, ab)
+
+
+@pytest.mark.parametrize("m,n,k,wb,ab", [(1, 11008, 4096, 4, 4), (3, 1000, 4100, 2, 8), (16, 512, 2048, 4, 4)])
+def test_host_linear_end_to_end(abq, orc, m, n, k, wb, ab):
+    """HostLinear.step(): pinned host activations staged by a kernel over PCIe
+    (abq_stage_in, incl. a byte tail), the linear's epilogue writing y into
+    pinned host memory; several calls back to back (PDL-chained) each equal
+    the oracle."""
+    rng = np.random.default_rng(m + n + k)
+    hosts, wants = [], []
+    for rep in range(3):
+        x, wc, sb, zb = _case(rng, m, n, k, wb, ab)
+        w = abq.PackedWeights.from_planes(abq.bitpack(wc, wb), sb, zb)
+        h = abq.HostLinear(abq.Linear(w, abq.QuantSpec(bits=ab, granularity=abq.api.PER_TOKEN), max_m=m), m)
+        h.x_host.copy_(torch.from_numpy(x))
+        ac, sa, za = orc.quantize(x.astype(np.float64), ab, 0, 2)
+        hosts.append(h)
+        wants.append(orc.quantized_linear(ac, ab, sa, za, wc, wb, sb, zb).astype(np.float16))
+    for h in hosts:
+        h.step()
+    torch.cuda.synchronize()
+    for h, want in zip(hosts, wants):
+        assert np.array_equal(h.y_host.numpy(), want)
