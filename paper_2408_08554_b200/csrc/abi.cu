@@ -441,6 +441,7 @@ int abq_set_tuning(const char* key, long long value) {
   else if (k == "dec_ring_kb" && value >= 0) t.ring_kb = static_cast<int>(value);
   else if (k == "dec_pdl") t.pdl = value != 0;
   else if (k == "dec_pace_ns" && value >= 0) t.pace_ns = static_cast<int>(value);
+  else if (k == "dec_grid_balanced") t.grid_balanced = value != 0;
   else if (k == "tc_dbg") t.tc_dbg = static_cast<int>(value);
   else if (k == "tc_tt" && value >= 0) t.tc_tt = static_cast<int>(value);
   else if (k == "reset") t = DecTuning{};

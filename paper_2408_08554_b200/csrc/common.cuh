@@ -24,6 +24,7 @@ struct DecTuning {
   int ring_kb = 0;   // decode GEMV: ring size cap in KB (0 = the CTA's whole share when it fits)
   int pdl = 1;       // decode GEMV: programmatic dependent launch
   int pace_ns = 0;   // decode GEMV: producer-warp slot spacing while awaiting activations (0 = auto)
+  int grid_balanced = 0;  // decode GEMV: fewer CTAs, all with the same row-tile count
   int tc_dbg = 0;    // prefill GEMM: experiment switches (tools/trace_gemm.py), 0 in production
   int tc_tt = 0;     // prefill GEMM: token-tile cap for the serving path (0 = by M)
 };

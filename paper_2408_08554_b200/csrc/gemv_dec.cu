@@ -805,7 +805,13 @@ static int launch_dec(DecParams& P, size_t m, bool fused, bool qact, cudaStream_
   const size_t n = static_cast<size_t>(P.n), k = static_cast<size_t>(P.k);
   const int mt = dec_mt(m);
   const int kpad = P.kblocks * kKBlock;
-  const int grid = std::min(num_sms(), P.rowtiles);
+  // grid: one CTA per SM; with dec_grid_balanced, only as many CTAs as give
+  // every CTA the same (maximal) number of row-tiles (no light CTAs)
+  int grid = std::min(num_sms(), P.rowtiles);
+  if (dec_tuning().grid_balanced) {
+    const int per = (P.rowtiles + grid - 1) / grid;
+    grid = (P.rowtiles + per - 1) / per;
+  }
   const int nl = dec_nlrt_max(P.rowtiles, grid);
   P.slots = dec_slots(q, n, k, mt, grid);
   const size_t slot_bytes = static_cast<size_t>(kDecUPS) * q * 512;
