@@ -675,7 +675,7 @@ inline Mat quantized_linear(const QuantizedTensor& act, const QuantizedTensor& w
     detail::check(abq_weights_prepack_tc(dwp.get(), q, n, k, dlay.get(), nullptr));
   abq_weights w{dwp.get(), q, n, k, dsb.get(), dzb.get(), dcb.get(),
                 wt.spec.granularity == Granularity::PerTensor, decode ? dlay.get() : nullptr,
-                decode ? nullptr : dlay.get()};
+                decode ? nullptr : dlay.get(), nullptr};
   Mat out(m, n);
   detail::DeviceBuffer<double> dy(out.data.size());
   detail::check(abq_linear_planes(&a, &w, dy.get(), ABQ_OUT_F64, nullptr));
@@ -720,7 +720,8 @@ class Weights {
   }
   abq_weights view() const {
     return abq_weights{planes_.get(), q_, n_, k_, scales_.get(), zps_.get(), colsums_.get(),
-                       per_tensor_ ? 1 : 0, frag_.size() ? frag_.get() : nullptr, tc_.size() ? tc_.get() : nullptr};
+                       per_tensor_ ? 1 : 0, frag_.size() ? frag_.get() : nullptr, tc_.size() ? tc_.get() : nullptr,
+                       nullptr};
   }
   std::size_t resident_bytes() const {
     return planes_.size() * 8 + frag_.size() * 4 + tc_.size() * 4;
@@ -816,6 +817,10 @@ class Linear {
     const abq_qact v = act.view();
     detail::check(abq_linear_qact(&v, &w_, y, out_kind, stream));
   }
+  /// successor-layer hint (abq_weights.next): the linear run next on the same
+  /// stream; this layer's decode GEMV prefetches the start of its weights into
+  /// L2 in its tail.  `next` must outlive this Linear (nullptr clears).
+  void prefetch_next(const Linear* next) { w_.next = next ? &next->w_ : nullptr; }
 
  private:
   abq_weights w_;

@@ -80,7 +80,7 @@ typedef struct {
  * re-packs weights on every quantized_linear call, gemm.hpp:274-278).
  * planes: ABQP [q][n][words_per_row]; scales/zero_points: n entries
  * (per-channel) or 1 (per-tensor); colsums[n] = code_rowsums(wt.codes). */
-typedef struct {
+typedef struct abq_weights_s {
   const uint64_t* planes;
   unsigned q;
   size_t n, k;
@@ -94,6 +94,13 @@ typedef struct {
   /* optional tcgen05-GEMM copy of the planes (abq_weights_prepack_tc) used
    * for M >= 9 tokens; NULL = no prefill tensor-core path */
   const uint32_t* tc;
+  /* optional successor-layer hint: the weights the caller runs NEXT on this
+   * stream (a decode step's layer order is static).  In the decode GEMV's
+   * tail, once a CTA's own weights have landed, it prefetches the first
+   * KB of its share of next->frag into L2 (HBM otherwise idles while the
+   * grid finishes and the next launch's CTAs start); NULL = no hint.  Results
+   * never depend on it. */
+  const struct abq_weights_s* next;
 } abq_weights;
 
 /* Activation-side metadata produced by abq_quant_pack_act (per-token or

@@ -46,7 +46,8 @@ class QActC(C.Structure):
 class WeightsC(C.Structure):
     _fields_ = [("planes", C.c_void_p), ("q", C.c_uint), ("n", C.c_size_t), ("k", C.c_size_t),
                 ("scales", C.c_void_p), ("zero_points", C.c_void_p), ("colsums", C.c_void_p),
-                ("per_tensor", C.c_int), ("frag", C.c_void_p), ("tc", C.c_void_p)]
+                ("per_tensor", C.c_int), ("frag", C.c_void_p), ("tc", C.c_void_p),
+                ("next", C.c_void_p)]
 
 
 class ActC(C.Structure):

@@ -951,6 +951,17 @@ class Linear:
         _check(L.lib().abq_linear_qact(C.byref(a.c()), C.byref(self._wc), _ptr(out), _OUT[out.dtype], _stream()))
         return out
 
+    def prefetch_next(self, nxt: Optional["Linear"]) -> "Linear":
+        """Successor-layer hint (abq_weights.next): `nxt` is the linear the
+        caller runs next on the same stream (a decode step's layer order is
+        static).  In this layer's decode GEMV tail every CTA, once its own
+        weights have landed, prefetches the first KB of its share of nxt's
+        weights into L2, so HBM keeps streaming while this grid finishes and
+        the next launch's CTAs start.  Results never depend on it; None clears."""
+        self._next = nxt
+        self._wc.next = C.addressof(nxt._wc) if nxt is not None else None
+        return self
+
     def raise_if_nonfinite(self) -> None:
         """Synchronise and raise abq.ValueError if the last check=False call
         saw a non-finite activation (the report is reset by every call)."""

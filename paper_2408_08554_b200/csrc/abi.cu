@@ -89,7 +89,7 @@ bool imma_supported(size_t m, size_t k);
 bool dec_supported(unsigned q, size_t n, size_t k, size_t m);
 int run_gemv_dec_qact(const uint32_t* frag, unsigned q, size_t n, size_t k, size_t m, const uint32_t* codes,
                       const double* s_a, const int32_t* z_a, const long long* rowsum, const QuantParams& qp,
-                      const EpiParams& e, cudaStream_t st);
+                      const EpiParams& e, cudaStream_t st, const DecNext* nx);
 size_t qact_codes_bytes(size_t m, size_t k);
 int run_stage_in(void* dst, const void* src, size_t bytes, cudaStream_t st);
 bool qact_supported(size_t m, size_t k);
@@ -106,7 +106,15 @@ int run_gemv_imma_planes(const uint32_t* frag, unsigned q, size_t n, size_t k, s
                          const uint64_t* a_planes, unsigned p, const EpiParams& e, cudaStream_t st);
 int run_gemv_dec(const uint32_t* frag, unsigned q, size_t n, size_t k, size_t m, const void* x, int x_dtype,
                  const QuantParams& qp, const EpiParams& e, void* ws, unsigned long long* bad_out,
-                 cudaStream_t st);
+                 cudaStream_t st, const DecNext* nx);
+
+// successor-layer hint of a weights block (abq_weights.next), for the decode GEMV
+static const DecNext* next_of(const abq_weights* w, DecNext* buf) {
+  const abq_weights* n = w->next;
+  if (!n || !n->frag || n->q < 1 || n->q > 8 || n->n == 0 || n->k == 0) return nullptr;
+  *buf = DecNext{n->frag, n->q, n->n, n->k};
+  return buf;
+}
 
 int run_gemm_bmma(const uint64_t* a, unsigned p, size_t m, const uint64_t* w, unsigned q, size_t n, size_t k,
                   int32_t* out, cudaStream_t st);
@@ -429,8 +437,10 @@ int abq_linear_qact(const abq_qact* act, const abq_weights* w, void* y, int out_
   e.k = static_cast<long long>(act->k);
   QuantParams qp{};
   qp.bits = act->bits;
+  DecNext nb;
   return run_gemv_dec_qact(w->frag, w->q, w->n, act->k, act->m, act->codes, act->scales, act->zero_points,
-                           reinterpret_cast<const long long*>(act->rowsums), qp, e, as_stream(stream));
+                           reinterpret_cast<const long long*>(act->rowsums), qp, e, as_stream(stream),
+                           next_of(w, &nb));
 }
 
 int abq_set_tuning(const char* key, long long value) {
@@ -444,6 +454,9 @@ int abq_set_tuning(const char* key, long long value) {
   else if (k == "dec_grid_balanced") t.grid_balanced = value != 0;
   else if (k == "tc_dbg") t.tc_dbg = static_cast<int>(value);
   else if (k == "tc_tt" && value >= 0) t.tc_tt = static_cast<int>(value);
+  else if (k == "dec_next_kb" && value >= 0) t.next_kb = static_cast<int>(value);
+  else if (k == "dec_next_min_kb" && value >= 0) t.next_min_kb = static_cast<int>(value);
+  else if (k == "dec_l2_plain") t.l2_plain = value != 0;
   else if (k == "reset") t = DecTuning{};
   else return fail(ABQ_ERR_VALUE, "abq_set_tuning: unknown key or bad value '%s'=%lld", key, value);
   return ABQ_OK;
@@ -796,7 +809,8 @@ int abq_linear(const void* x, int x_dtype, size_t m, size_t k, const abq_quant_s
     e.colsum_b = w->colsums;
     e.k = static_cast<long long>(k);
     const QuantParams qp = params_of(*act_spec);
-    st = run_gemv_dec(w->frag, w->q, w->n, k, m, x, x_dtype, qp, e, ws_imma, bad, s);
+    DecNext nb;
+    st = run_gemv_dec(w->frag, w->q, w->n, k, m, x, x_dtype, qp, e, ws_imma, bad, s, next_of(w, &nb));
     if (st) return st;
   } else if (use_tc(w, m, k, !fits_int32_host(p, w->q, k))) {
     // ReQuant straight to u8 codes (K1), then the tcgen05 GEMM with the fused epilogue

@@ -69,6 +69,12 @@ struct DecParams {
   int pace_ns;   // producer warp: spacing of the ring slots issued while the activations are awaited
   int slots;     // TMA ring slots of kDecUPS units
   int preslots;  // ring slots issued before the activations are awaited
+  // successor layer (abq_weights.next): its decode-layout weights, partition
+  // (same row-tile split as its own launch) and the bytes per CTA prefetched
+  // into L2 once this CTA's stream has landed
+  const unsigned char* nx;
+  int nx_rowtiles, nx_kblocks, nx_unit, nx_grid, nx_bytes;
+  int l2_plain;  // weight TMA without the L2 evict-first hint (sweeps)
   unsigned long long* trace;  // ABQ_TRACE build only: [grid][64] stamps
 };
 
@@ -205,8 +211,12 @@ __global__ void __launch_bounds__(kDecBlock, kDecCtasPerSm) gemv_dec_kernel(cons
     const int n_units = min(UPS, nu - i * UPS);
     const uint32_t bytes = static_cast<uint32_t>(n_units * unit_bytes);
     mbar_expect_tx(&full[sl], bytes);
-    tma_bulk_g2s_hint(ring + static_cast<size_t>(sl) * slot_bytes, wsrc + static_cast<size_t>(i) * slot_bytes, bytes,
-                      &full[sl], pol);
+    if (P.l2_plain)
+      tma_bulk_g2s(ring + static_cast<size_t>(sl) * slot_bytes, wsrc + static_cast<size_t>(i) * slot_bytes, bytes,
+                   &full[sl]);
+    else
+      tma_bulk_g2s_hint(ring + static_cast<size_t>(sl) * slot_bytes, wsrc + static_cast<size_t>(i) * slot_bytes,
+                        bytes, &full[sl], pol);
   };
   // ---- 1. ring: the producer warp's lane s initialises barrier s; the
   // slots are issued after the set-up barrier (below)
@@ -259,6 +269,30 @@ __global__ void __launch_bounds__(kDecBlock, kDecCtasPerSm) gemv_dec_kernel(cons
     }
 #pragma unroll 1
     for (int j = i + lane; j < lim; j += 32) issue_slot(j, j);  // the rest, one slot per lane
+#ifdef ABQ_TRACE
+    if (P.trace && lane == 0) P.trace[64 * blockIdx.x + 15] = gtimer();
+#endif
+    // Successor prefetch: once this CTA's whole share has landed (ring not
+    // refilled: the last slot's barrier completes exactly once), the SM's HBM
+    // stream is done while the grid still finishes, the next launch's CTAs
+    // start and their first loads see HBM latency.  The first nx_bytes of the
+    // share the next layer's CTA with this index will stream are requested
+    // into L2 now (same split as that launch: rt_first / nlrt below).
+    if (P.nx && lane == 0 && nsl > 0 && nsl <= S && static_cast<int>(blockIdx.x) < P.nx_grid) {
+      mbar_wait_parity(&full[nsl - 1], 0);
+      const int gn = P.nx_grid, base = P.nx_rowtiles / gn, hv = P.nx_rowtiles - base * gn;
+      const int b = blockIdx.x;
+      const int rf = b < hv ? b * (base + 1) : hv + b * base;
+      const int nl = base + (b < hv ? 1 : 0);
+      const size_t share = static_cast<size_t>(nl) * P.nx_kblocks * P.nx_unit;
+      const size_t bytes = min(share, static_cast<size_t>(P.nx_bytes));
+      const unsigned char* src = P.nx + static_cast<size_t>(rf) * P.nx_kblocks * P.nx_unit;
+#pragma unroll 1
+      for (size_t off = 0; off < bytes; off += 16384)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + off),
+                     "r"(static_cast<uint32_t>(bytes - off < 16384 ? bytes - off : 16384))
+                     : "memory");
+    }
     return;
   }
   DEC_STAMP(1, clock64());
@@ -266,6 +300,7 @@ __global__ void __launch_bounds__(kDecBlock, kDecCtasPerSm) gemv_dec_kernel(cons
   // ---- 2. the activations, which the previous kernel may still be producing
   asm volatile("griddepcontrol.wait;" ::: "memory");
   DEC_STAMP(2, clock64());
+  DEC_STAMP(12, gtimer());
   if constexpr (FUSED) {
     // Fused ReQuant, per token, fp16 rows (K % 8 == 0, K <= 32 * TPT: the host
     // routes longer rows through act_quant_kernel).  GT warps per token; each
@@ -408,6 +443,7 @@ __global__ void __launch_bounds__(kDecBlock, kDecCtasPerSm) gemv_dec_kernel(cons
   }
   cta_sync();
   DEC_STAMP(5, clock64());
+  DEC_STAMP(13, gtimer());
 
   // ---- 3. main loop.  Local unit l = warp + NW j lives in ring slot index
   // l / UPS = grp + NG j (group grp = warp / UPS takes the slots = grp mod NG),
@@ -532,10 +568,18 @@ __global__ void __launch_bounds__(kDecBlock, kDecCtasPerSm) gemv_dec_kernel(cons
     uint4 w[QT];
     int rtA = -1, rtB = -1;
     DEC_STAMP(16, clock64());
+#ifdef ABQ_TRACE
+    unsigned long long last_data = 0;
+#define DEC_LAST_DATA() do { if (P.trace && tid == 0) last_data = gtimer(); } while (0)
+#else
+#define DEC_LAST_DATA() do { } while (0)
+#endif
     for (int j = 0; j < nw; j += 2) {
       // unit j -> set A (fold set B = unit j - 1 behind its IMMAs)
       mbar_wait_parity(&full[fs], fph);
+      DEC_LAST_DATA();
       if (j == 0) DEC_STAMP(17, clock64());
+      if (j == 0) DEC_STAMP(22, gtimer());
       lds_unit(fs, w);
       const int slA = fs, iA = fi, kbA = fkb;
       rtA = frt;
@@ -547,6 +591,7 @@ __global__ void __launch_bounds__(kDecBlock, kDecCtasPerSm) gemv_dec_kernel(cons
       if (j + 1 >= nw) break;
       // unit j + 1 -> set B (fold set A behind its IMMAs)
       mbar_wait_parity(&full[fs], fph);
+      DEC_LAST_DATA();
       lds_unit(fs, w);
       const int slB = fs, iB = fi, kbB = fkb;
       rtB = frt;
@@ -559,6 +604,10 @@ __global__ void __launch_bounds__(kDecBlock, kDecCtasPerSm) gemv_dec_kernel(cons
       rtA = -1;
     }
     DEC_STAMP(19, clock64());
+    DEC_STAMP(14, gtimer());
+#ifdef ABQ_TRACE
+    if (P.trace && tid == 0) trace[21] = last_data;
+#endif
     if (rtA >= 0) fold(accA, rtA);
     else if (nw > 0 && (nw & 1) == 0) fold(accB, rtB);
     flush_tot();
@@ -726,13 +775,13 @@ bool dec_supported(unsigned q, size_t n, size_t k, size_t m) {
 // GEMV (one launch); anything else goes through act_quant_kernel first, with
 // this kernel as its PDL secondary.  Every launch is itself PDL-enabled so
 // consecutive layers overlap.
-static int launch_dec(DecParams& P, size_t m, bool fused, bool qact, cudaStream_t st);
+static int launch_dec(DecParams& P, size_t m, bool fused, bool qact, cudaStream_t st, const DecNext* nx);
 
 // Consumer of a producer-fused ReQuant (producer.cu): codes already in the
 // B-fragment layout of dec_mt(m) tokens, with s_a / z_a / code row sums.
 int run_gemv_dec_qact(const uint32_t* frag, unsigned q, size_t n, size_t k, size_t m, const uint32_t* codes,
                       const double* s_a, const int32_t* z_a, const long long* rowsum, const QuantParams& qp,
-                      const EpiParams& e, cudaStream_t st) {
+                      const EpiParams& e, cudaStream_t st, const DecNext* nx) {
   if (m == 0 || n == 0) return ABQ_OK;
   if (!dec_supported(q, n, k, m)) return fail(ABQ_ERR_VALUE, "gemv_dec: layer shape not supported");
   DecParams P{};
@@ -750,12 +799,12 @@ int run_gemv_dec_qact(const uint32_t* frag, unsigned q, size_t n, size_t k, size
   P.s_a = s_a;
   P.z_a = z_a;
   P.rowsum = rowsum;
-  return launch_dec(P, m, false, true, st);
+  return launch_dec(P, m, false, true, st, nx);
 }
 
 int run_gemv_dec(const uint32_t* frag, unsigned q, size_t n, size_t k, size_t m, const void* x, int x_dtype,
                  const QuantParams& qp, const EpiParams& e, void* ws, unsigned long long* bad_out,
-                 cudaStream_t st) {
+                 cudaStream_t st, const DecNext* nx) {
   if (m == 0 || n == 0) return ABQ_OK;
   if (!dec_supported(q, n, k, m)) return fail(ABQ_ERR_VALUE, "gemv_dec: layer shape not supported");
   DecParams P{};
@@ -797,20 +846,37 @@ int run_gemv_dec(const uint32_t* frag, unsigned q, size_t n, size_t k, size_t m,
     P.z_a = z_a;
     P.rowsum = rowsum;
   }
-  return launch_dec(P, m, fused, false, st);
+  return launch_dec(P, m, fused, false, st, nx);
 }
 
-static int launch_dec(DecParams& P, size_t m, bool fused, bool qact, cudaStream_t st) {
+// grid: one CTA per SM; with dec_grid_balanced, only as many CTAs as give
+// every CTA the same (maximal) number of row-tiles (no light CTAs)
+static int dec_grid(int rowtiles) {
+  int grid = std::min(num_sms(), rowtiles);
+  if (dec_tuning().grid_balanced) {
+    const int per = (rowtiles + grid - 1) / grid;
+    grid = (rowtiles + per - 1) / per;
+  }
+  return grid;
+}
+
+static int launch_dec(DecParams& P, size_t m, bool fused, bool qact, cudaStream_t st, const DecNext* nx) {
   const unsigned q = static_cast<unsigned>(P.q);
   const size_t n = static_cast<size_t>(P.n), k = static_cast<size_t>(P.k);
   const int mt = dec_mt(m);
   const int kpad = P.kblocks * kKBlock;
-  // grid: one CTA per SM; with dec_grid_balanced, only as many CTAs as give
-  // every CTA the same (maximal) number of row-tiles (no light CTAs)
-  int grid = std::min(num_sms(), P.rowtiles);
-  if (dec_tuning().grid_balanced) {
-    const int per = (P.rowtiles + grid - 1) / grid;
-    grid = (P.rowtiles + per - 1) / per;
+  const int grid = dec_grid(P.rowtiles);
+  P.l2_plain = dec_tuning().l2_plain;
+  // successor prefetch only behind a long stream (measured: +5 % at W4 up_proj,
+  // 152 KB per CTA; -1..-5 % for shares <= ~76 KB, profiles/r02_dec_next_sweep.txt)
+  const size_t share = static_cast<size_t>(dec_nlrt_max(P.rowtiles, grid)) * P.kblocks * q * 512;
+  if (nx && nx->frag && dec_tuning().next_kb > 0 && share >= static_cast<size_t>(dec_tuning().next_min_kb) * 1024) {
+    P.nx = reinterpret_cast<const unsigned char*>(nx->frag);
+    P.nx_rowtiles = static_cast<int>((nx->n + kRowTile - 1) / kRowTile);
+    P.nx_kblocks = static_cast<int>((nx->k + kKBlock - 1) / kKBlock);
+    P.nx_unit = static_cast<int>(nx->q) * 512;
+    P.nx_grid = dec_grid(P.nx_rowtiles);
+    P.nx_bytes = dec_tuning().next_kb * 1024;
   }
   const int nl = dec_nlrt_max(P.rowtiles, grid);
   P.slots = dec_slots(q, n, k, mt, grid);

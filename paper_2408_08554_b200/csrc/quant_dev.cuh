@@ -200,30 +200,98 @@ __device__ __forceinline__ unsigned quant_code_f32(float v, double step, float i
   return static_cast<unsigned>(c < 0 ? 0 : (c > top ? top : c));
 }
 
+// Exact code of an fp16 value x whose fp32 quotient estimate q = RN32(x RN32(1/step))
+// lies in the tie band, without the FP64 division: |q| is within the band
+// (< 1/4 for |q| < 2^19) of h = floor(|q|) + 1/2, so round(RN64(|x|/step)) is
+// floor(|q|) + 1 iff RN64(|x|/step) >= h.  With r = RN(|x| - h step) (one FMA,
+// sign exact): r >= 0 => |x|/step >= h.  Else D = h step - |x| > 0 and
+// RN64(|x|/step) = h iff |x|/step is above the midpoint of h and its double
+// predecessor h - u, i.e. D < T = (u/2) step (T exact: u is a power of two):
+// RN(D) < T => yes, RN(D) > T => no; RN(D) == T (or |q| >= 2^19) is left to
+// the division (*ok = false).  code = clamp(sign(x) * mag + z, 0, top), as
+// quant_code (quantizer.hpp:205-209: round half away from zero, then + z).
+__device__ __forceinline__ int quant_code_tie(float xf, float q, double step, int z, int top, bool* ok) {
+  const float qa = fabsf(q);
+  if (!(qa < 524288.0f)) {
+    *ok = false;
+    return 0;
+  }
+  const double n = floor(static_cast<double>(qa)), h = n + 0.5;
+  const double r = __fma_rn(-h, step, fabs(static_cast<double>(xf)));
+  int mag = static_cast<int>(n) + 1;
+  if (r < 0.0) {
+    const double u = h - __longlong_as_double(__double_as_longlong(h) - 1);
+    const double T = __dmul_rn(__dmul_rn(u, 0.5), step), d = -r;
+    if (d > T) mag -= 1;
+    else if (!(d < T)) {
+      *ok = false;
+      return 0;
+    }
+  }
+  const int c = (xf < 0.0f ? -mag : mag) + z;
+  return c < 0 ? 0 : (c > top ? top : c);
+}
+
+// In-band elements (mask bit e of band) of a vector replaced by their exact
+// codes (quant_code_tie inline; the FP64 division out of line only where that
+// cannot decide).  Rare: about one element per 4096-wide token at 8-bit codes.
+__device__ __forceinline__ uint3 quant_codes8_ties(const uint4& xv, double step, float inv32, int z, int top,
+                                                   uint32_t band, uint32_t w0, uint32_t w1);
+
 // Eight fp16 activations (one 16-byte vector) -> eight u8 codes (two words,
-// element e in byte e%4 of word e/4), all on the fp32 pipe; the exact FP64
-// path (quant_code) runs out of line, for the whole vector, only when one of
-// the eight is inside the tie band of quant_code_f32.  Returns the code sum.
-// (returns {word 0, word 1, code sum}; by value: a pointer argument would put
-// the words in local memory, and a local-memory miss behind the weight stream
-// costs a full memory round trip)
-static __device__ __noinline__ uint3 quant_codes8_exact(uint4 xv, double step, int z, int top) {
+// element e in byte e%4 of word e/4), all on the fp32 pipe.  Elements inside
+// the tie band of quant_code_f32 (mask bit e) are then replaced by their exact
+// FP64 codes out of line, one FP64 division per flagged element: the band is
+// ~2^-21 |q| wide, so at 8-bit codes about one element per 4096-wide token
+// falls in it, and recomputing the whole vector cost that warp ~8 divisions on
+// the critical path of every CTA.  Returns {word 0, word 1, code sum}, by value
+// (a pointer argument would put the words in local memory).
+static __device__ __noinline__ uint3 quant_codes8_patch(uint4 xv, double step, int z, int top, uint32_t band,
+                                                        uint32_t w0, uint32_t w1) {
   const __half* hv = reinterpret_cast<const __half*>(&xv);
-  uint3 r = make_uint3(0u, 0u, 0u);
+#pragma unroll 1
   for (int e = 0; e < 8; ++e) {
+    if (!((band >> e) & 1u)) continue;
     const unsigned c = quant_code(static_cast<double>(__half2float(hv[e])), step, static_cast<double>(z),
                                   static_cast<double>(top));
-    r.z += c;
-    if (e < 4) r.x |= c << (8 * e);
-    else r.y |= c << (8 * (e - 4));
+    const uint32_t sh = 8u * static_cast<uint32_t>(e & 3), m = ~(0xFFu << sh);
+    if (e < 4) w0 = (w0 & m) | (c << sh);
+    else w1 = (w1 & m) | (c << sh);
   }
-  return r;
+  uint32_t sum = 0;
+#pragma unroll
+  for (int b = 0; b < 4; ++b) sum += ((w0 >> (8 * b)) & 0xFFu) + ((w1 >> (8 * b)) & 0xFFu);
+  return make_uint3(w0, w1, sum);
+}
+__device__ __forceinline__ uint3 quant_codes8_ties(const uint4& xv, double step, float inv32, int z, int top,
+                                                   uint32_t band, uint32_t w0, uint32_t w1) {
+  uint32_t slow = 0;
+#pragma unroll 1
+  for (uint32_t b = band; b; b &= b - 1u) {
+    const int e = __ffs(static_cast<int>(b)) - 1;
+    const uint32_t wd = (e >> 1) == 0 ? xv.x : (e >> 1) == 1 ? xv.y : (e >> 1) == 2 ? xv.z : xv.w;
+    const float xf = __half2float(__ushort_as_half(static_cast<unsigned short>(wd >> (16 * (e & 1)))));
+    bool ok = true;
+    const uint32_t c = static_cast<uint32_t>(quant_code_tie(xf, __fmul_rn(xf, inv32), step, z, top, &ok));
+    if (!ok) {
+      slow |= 1u << e;
+      continue;
+    }
+    const uint32_t sh = 8u * static_cast<uint32_t>(e & 3), m = ~(0xFFu << sh);
+    if (e < 4) w0 = (w0 & m) | (c << sh);
+    else w1 = (w1 & m) | (c << sh);
+  }
+  if (slow) return quant_codes8_patch(xv, step, z, top, slow, w0, w1);
+  uint32_t sum = 0;
+#pragma unroll
+  for (int b = 0; b < 4; ++b) sum += ((w0 >> (8 * b)) & 0xFFu) + ((w1 >> (8 * b)) & 0xFFu);
+  return make_uint3(w0, w1, sum);
 }
 __device__ __forceinline__ int quant_codes8_f16(const uint4& xv, double step, float inv32, int z, int top,
                                                 uint32_t* w0, uint32_t* w1) {
   const __half2* h2 = reinterpret_cast<const __half2*>(&xv);
   int c[8];
-  bool ok = true;
+  uint32_t band = 0;
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
     const float2 f = __half22float2(h2[e]);
@@ -234,34 +302,23 @@ __device__ __forceinline__ int quant_codes8_f16(const uint4& xv, double step, fl
       const float t = __fadd_rn(q, 12582912.0f);
       const float r = __fsub_rn(t, 12582912.0f);
       const float d = __fsub_rn(0.5f, fabsf(__fsub_rn(q, r)));
-      ok = ok && fabsf(q) < 4194304.0f && d > fmaxf(fabsf(q), 1.0f) * 4.76837158203125e-07f;
+      const bool in = fabsf(q) < 4194304.0f && d > fmaxf(fabsf(q), 1.0f) * 4.76837158203125e-07f;
+      band |= (in ? 0u : 1u) << (2 * e + h);
       const int ci = (__float_as_int(t) - 0x4B400000) + z;
       c[2 * e + h] = ci < 0 ? 0 : (ci > top ? top : ci);
     }
-  }
-  if (!ok) {
-    const uint3 r = quant_codes8_exact(xv, step, z, top);
-    *w0 = r.x;
-    *w1 = r.y;
-    return static_cast<int>(r.z);
   }
   *w0 = static_cast<uint32_t>(c[0]) | (static_cast<uint32_t>(c[1]) << 8) | (static_cast<uint32_t>(c[2]) << 16) |
         (static_cast<uint32_t>(c[3]) << 24);
   *w1 = static_cast<uint32_t>(c[4]) | (static_cast<uint32_t>(c[5]) << 8) | (static_cast<uint32_t>(c[6]) << 16) |
         (static_cast<uint32_t>(c[7]) << 24);
+  if (band) {
+    const uint3 r = quant_codes8_ties(xv, step, inv32, z, top, band, *w0, *w1);
+    *w0 = r.x;
+    *w1 = r.y;
+    return static_cast<int>(r.z);
+  }
   return c[0] + c[1] + c[2] + c[3] + c[4] + c[5] + c[6] + c[7];
-}
-
-// The exact step is only needed on the tie path: LazyStep carries what it is
-// computed from (group_params, out of line) instead of the step itself.
-struct LazyStep {
-  const QuantParams* qp;
-  float lo, hi;
-};
-static __device__ __noinline__ uint3 quant_codes8_exact_lazy(uint4 xv, QuantParams qp, float lo, float hi, int z,
-                                                             int top) {
-  const StepZ r = group_params_ool(qp, lo, hi);
-  return quant_codes8_exact(xv, r.step, z, top);
 }
 
 // Asymmetric per-token zero point and reciprocal step for the CODES, on the
@@ -301,12 +358,11 @@ __device__ __forceinline__ float band_threshold(float lo, float hi, float inv32)
   const float qmax = __fmul_ru(fmaxf(fabsf(lo), fabsf(hi)), __fmul_ru(inv32, 1.0000010f));  // >= every |q|
   return qmax < 4194304.0f ? 0.5f - fmaxf(qmax, 1.0f) * 4.76837158203125e-07f : -1.0f;  // -1: all exact
 }
-template <typename StepT>
-__device__ __forceinline__ int quant_codes8_f16_band(const uint4& xv, StepT step, float inv32, float thr, int z,
+__device__ __forceinline__ int quant_codes8_f16_band(const uint4& xv, double step, float inv32, float thr, int z,
                                                      int top, uint32_t* w0, uint32_t* w1) {
   const __half2* h2 = reinterpret_cast<const __half2*>(&xv);
   int c[8];
-  bool ok = true;
+  uint32_t band = 0;
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
     const float2 f = __half22float2(h2[e]);
@@ -314,23 +370,21 @@ __device__ __forceinline__ int quant_codes8_f16_band(const uint4& xv, StepT step
     for (int h = 0; h < 2; ++h) {
       const float q = __fmul_rn(h ? f.y : f.x, inv32);
       const float t = __fadd_rn(q, 12582912.0f);  // 1.5 * 2^23: rint(q) in the low mantissa bits
-      ok = ok && fabsf(__fsub_rn(q, __fsub_rn(t, 12582912.0f))) < thr;
+      band |= (fabsf(__fsub_rn(q, __fsub_rn(t, 12582912.0f))) < thr ? 0u : 1u) << (2 * e + h);
       const int ci = (__float_as_int(t) - 0x4B400000) + z;
       c[2 * e + h] = ci < 0 ? 0 : (ci > top ? top : ci);
     }
-  }
-  if (!ok) {
-    uint3 r;
-    if constexpr (sizeof(StepT) == sizeof(double)) r = quant_codes8_exact(xv, step, z, top);
-    else r = quant_codes8_exact_lazy(xv, *step.qp, step.lo, step.hi, z, top);
-    *w0 = r.x;
-    *w1 = r.y;
-    return static_cast<int>(r.z);
   }
   *w0 = static_cast<uint32_t>(c[0]) | (static_cast<uint32_t>(c[1]) << 8) | (static_cast<uint32_t>(c[2]) << 16) |
         (static_cast<uint32_t>(c[3]) << 24);
   *w1 = static_cast<uint32_t>(c[4]) | (static_cast<uint32_t>(c[5]) << 8) | (static_cast<uint32_t>(c[6]) << 16) |
         (static_cast<uint32_t>(c[7]) << 24);
+  if (band) {  // rare: exact codes of the flagged elements only
+    const uint3 r = quant_codes8_ties(xv, step, inv32, z, top, band, *w0, *w1);
+    *w0 = r.x;
+    *w1 = r.y;
+    return static_cast<int>(r.z);
+  }
   return c[0] + c[1] + c[2] + c[3] + c[4] + c[5] + c[6] + c[7];
 }
 

@@ -229,3 +229,43 @@ def test_host_linear_end_to_end(abq, orc, m, n, k, wb, ab):
     torch.cuda.synchronize()
     for h, want in zip(hosts, wants):
         assert np.array_equal(h.y_host.numpy(), want)
+
+
+def test_prefetch_next_hint_is_transparent(abq, orc):
+    """abq_weights.next (Linear.prefetch_next): a cycle of decode layers of
+    different shapes and bit widths, each hinting its successor (the tail L2
+    prefetch runs for every CTA), replayed twice -- outputs bit-identical to the
+    oracle and to the unhinted run; also on producer-quantized activations."""
+    rng = np.random.default_rng(44)
+    shapes = [(1, 4096, 4096, 4, 4), (2, 11008, 4096, 2, 8), (1, 4096, 11008, 2, 8), (3, 700, 1500, 3, 6),
+              (1, 12288, 4096, 8, 8)]
+    lins, cases = [], []
+    for m, n, k, wb, ab in shapes:
+        x, wc, sb, zb = _case(rng, m, n, k, wb, ab)
+        w = abq.PackedWeights.from_planes(abq.bitpack(wc, wb), sb, zb)
+        lins.append(abq.Linear(w, abq.QuantSpec(bits=ab, granularity=abq.api.PER_TOKEN), max_m=m))
+        ac, sa, za = orc.quantize(x.astype(np.float64), ab, 0, 2)
+        cases.append((torch.from_numpy(x).cuda(), orc.quantized_linear(ac, ab, sa, za, wc, wb, sb, zb)))
+    plain = [lin(x, out_dtype=torch.float64).cpu().numpy() for lin, (x, _) in zip(lins, cases)]
+    for i, lin in enumerate(lins):
+        lin.prefetch_next(lins[(i + 1) % len(lins)])
+    outs = [torch.empty((x.shape[0], lin.w.planes.rows), dtype=torch.float64, device="cuda")
+            for lin, (x, _) in zip(lins, cases)]
+    for _ in range(2):
+        for lin, (x, _), y in zip(lins, cases, outs):
+            lin(x, out=y)
+    torch.cuda.synchronize()
+    for i, ((_, want), y) in enumerate(zip(cases, outs)):
+        assert np.array_equal(y.cpu().numpy(), want), shapes[i]
+        assert np.array_equal(plain[i], want), shapes[i]
+    # producer-quantized activations (abq_linear_qact) with the hint set
+    spec = abq.QuantSpec(bits=4, granularity=abq.api.PER_TOKEN)
+    xq = torch.from_numpy((rng.standard_normal((1, 4096))).astype(np.float16)).cuda()
+    g = torch.ones(4096, dtype=torch.float16, device="cuda")
+    qa = abq.QAct(1, 4096, spec)
+    h = torch.empty((1, 4096), dtype=torch.float16, device="cuda")
+    abq.rmsnorm_quant(xq, g, 1e-6, spec, out=qa, y_out=h)
+    y_q = lins[0](qa, out_dtype=torch.float64).cpu().numpy()
+    lins[0].prefetch_next(None)
+    y_f = lins[0](h, out_dtype=torch.float64).cpu().numpy()
+    assert np.array_equal(y_q, y_f)
