@@ -59,6 +59,18 @@ for _m in (4, 8, 16, 128):
         WORKLOADS[f"cfg2_w{_w}a{_w}_m{_m}"] = (
             _m, 11008, 4096, _w, _w, f"cfg2 W{_w}A{_w} M={_m} K=4096 N=11008 (LLaMA-7B up_proj)")
 
+# cfg3: the mixed-precision sweep (W2A4 / W3A8 / W4A8 / W6A6) over every
+# LLaMA-7B linear shape (fused q/k/v, o, fused gate/up, down) at M = 1 and 128;
+# `--workload cfg3_sweep` times them all (one JSON line, a row per workload)
+CFG3_PAIRS = [(2, 4), (3, 8), (4, 8), (6, 6)]
+CFG3_SHAPES = [("qkv", 12288, 4096), ("o", 4096, 4096), ("gate_up", 22016, 4096), ("down", 4096, 11008)]
+CFG3 = []
+for _wb, _ab in CFG3_PAIRS:
+    for _nm, _n, _k in CFG3_SHAPES:
+        for _m in (1, 128):
+            CFG3.append(f"cfg3_w{_wb}a{_ab}_{_nm}_m{_m}")
+            WORKLOADS[CFG3[-1]] = (_m, _n, _k, _wb, _ab, f"cfg3 W{_wb}A{_ab} M={_m} LLaMA-7B {_nm} (N={_n} K={_k})")
+
 # layer workloads (strong scaling): name -> (m, w_bits, a_bits, [(proj, n, k)], unit, description)
 LAYERS = {
     "cfg4_w2a8_13b_decode": (
@@ -617,10 +629,56 @@ def run_layer(args, world, rank, local):
             "run": {"rotation_copies": copies, "shard_bytes_per_rank": shard_bytes}}))
 
 
+def cpu_row(m, n, k, wb, ab, n_sample=256):
+    """The reference step on 1 host thread for one sweep row: the full layer at
+    M = 1, a sample of n_sample output channels at M > 1 (the work is linear in
+    N; the time is scaled to the layer)."""
+    from oracle.oracle import RefOracle
+    if not RefOracle.available():
+        return None
+    f, ns = reference_step_fn(m, n, k, wb, ab, 1, n_sample=None if m == 1 else n_sample)
+    f()
+    reps, t0 = 0, time.perf_counter()
+    while reps < 2 or time.perf_counter() - t0 < 0.3:
+        f()
+        reps += 1
+    us = (time.perf_counter() - t0) / reps * 1e6 * n / ns
+    return {"step_us": round(us, 1), "GBps": round(packed_bytes(n, k, wb) / us / 1e3, 3),
+            "TOPS": round(2 * m * n * k / us / 1e6, 4), "cores": 1, "kind": "reference",
+            "sample": "full layer" if ns == n else f"{ns} of {n} output channels, scaled"}
+
+
+def run_cfg3(args, world, abq, torch, local):
+    """cfg3 sweep (BASELINE configs[2]): every mixed-precision pair on every
+    LLaMA-7B linear shape at M = 1 and 128, each row with its roofline, the
+    cuBLAS fp16 GEMM of the same shape at M = 128 and the reference CPU step."""
+    peaks, peak_kind = measured_peaks()
+    l2 = torch.cuda.get_device_properties(local).L2_cache_size
+    steps = min(args.steps, 200)
+    rows = {}
+    for name in CFG3:
+        row = measure_part(abq, torch, name, world, steps, args.warmup, l2, peaks, peak_kind)
+        if not args.no_cpu:
+            m, n, k, wb, ab, _ = WORKLOADS[name]
+            row["cpu_reference"] = cpu_row(m, n, k, wb, ab)
+        rows[name] = row
+    fr = [r["roofline"]["frac"] for r in rows.values()]
+    sp = [r["speedup_vs_cublas_fp16"] for r in rows.values() if "speedup_vs_cublas_fp16" in r]
+    print(json.dumps({"metric": METRIC, "workload": "cfg3_sweep", "n_gpus": world, "steps": steps,
+                      "warmup": args.warmup, "data": "synthetic",
+                      "l2": "rotating packed-weight copies (> 4x L2 per rotation)",
+                      "summary": {"rows": len(rows), "roofline_frac_min": min(fr), "roofline_frac_max": max(fr),
+                                  "m128_speedup_vs_cublas_fp16_min": min(sp) if sp else None,
+                                  "m128_speedup_vs_cublas_fp16_max": max(sp) if sp else None},
+                      "rows": rows}))
+
+
 def run_ours(args, world, rank, local):
     import torch
 
     import paper_2408_08554_b200 as abq
+    if args.workload == "cfg3_sweep":
+        return run_cfg3(args, world, abq, torch, local)
     if args.workload in LAYERS:
         return run_layer(args, world, rank, local)
     if args.workload in CHAINS:  # tool mode: the chain part alone
@@ -797,7 +855,8 @@ def main():
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=50)
     ap.add_argument("--impl", default="abq", choices=["abq", "reference"])
-    ap.add_argument("--workload", default="cfg2_w4a4_m1", choices=sorted(list(WORKLOADS) + list(LAYERS) + list(CHAINS)))
+    ap.add_argument("--workload", default="cfg2_w4a4_m1",
+                    choices=sorted(list(WORKLOADS) + list(LAYERS) + list(CHAINS)) + ["cfg3_sweep"])
     ap.add_argument("--no-check", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parts", action="store_true", help="headline workload only")

@@ -457,6 +457,7 @@ int abq_set_tuning(const char* key, long long value) {
   else if (k == "dec_next_kb" && value >= 0) t.next_kb = static_cast<int>(value);
   else if (k == "dec_next_min_kb" && value >= 0) t.next_min_kb = static_cast<int>(value);
   else if (k == "dec_l2_plain") t.l2_plain = value != 0;
+  else if (k == "dec_dbg_nostream") t.dbg_nostream = value != 0;
   else if (k == "reset") t = DecTuning{};
   else return fail(ABQ_ERR_VALUE, "abq_set_tuning: unknown key or bad value '%s'=%lld", key, value);
   return ABQ_OK;

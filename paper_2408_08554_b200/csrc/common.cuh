@@ -30,6 +30,7 @@ struct DecTuning {
   int next_kb = 64;  // decode GEMV: KB per CTA of the successor layer prefetched into L2 in the tail (0 = off)
   int next_min_kb = 128;  // ... only when this layer's per-CTA weight share is at least this long
   int l2_plain = 0;  // decode GEMV: weight TMA without the L2 evict-first hint
+  int dbg_nostream = 0;  // decode GEMV, TRACE build only: no weight stream (timing experiment, results invalid)
 };
 DecTuning& dec_tuning();
 

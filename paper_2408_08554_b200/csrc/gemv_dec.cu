@@ -75,6 +75,7 @@ struct DecParams {
   const unsigned char* nx;
   int nx_rowtiles, nx_kblocks, nx_unit, nx_grid, nx_bytes;
   int l2_plain;  // weight TMA without the L2 evict-first hint (sweeps)
+  int dbg_nostream;  // TRACE build timing experiment: ring barriers arrive without data
   unsigned long long* trace;  // ABQ_TRACE build only: [grid][64] stamps
 };
 
@@ -210,6 +211,12 @@ __global__ void __launch_bounds__(kDecBlock, kDecCtasPerSm) gemv_dec_kernel(cons
   auto issue_slot = [&](int i, int sl) {  // thread-level: TMA of slot index i into ring slot sl
     const int n_units = min(UPS, nu - i * UPS);
     const uint32_t bytes = static_cast<uint32_t>(n_units * unit_bytes);
+#ifdef ABQ_TRACE
+    if (P.dbg_nostream) {  // timing experiment only: no weight bytes (results invalid)
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&full[sl])) : "memory");
+      return;
+    }
+#endif
     mbar_expect_tx(&full[sl], bytes);
     if (P.l2_plain)
       tma_bulk_g2s(ring + static_cast<size_t>(sl) * slot_bytes, wsrc + static_cast<size_t>(i) * slot_bytes, bytes,
@@ -270,7 +277,15 @@ __global__ void __launch_bounds__(kDecBlock, kDecCtasPerSm) gemv_dec_kernel(cons
 #pragma unroll 1
     for (int j = i + lane; j < lim; j += 32) issue_slot(j, j);  // the rest, one slot per lane
 #ifdef ABQ_TRACE
-    if (P.trace && lane == 0) P.trace[64 * blockIdx.x + 15] = gtimer();
+    if (P.trace && lane == 0) {
+      P.trace[64 * blockIdx.x + 15] = gtimer();
+      if (nsl > 0 && nsl <= S) {  // arrival of the first and the last ring slot
+        mbar_wait_parity(&full[0], 0);
+        P.trace[64 * blockIdx.x + 41] = gtimer();
+        mbar_wait_parity(&full[nsl - 1], 0);
+        P.trace[64 * blockIdx.x + 42] = gtimer();
+      }
+    }
 #endif
     // Successor prefetch: once this CTA's whole share has landed (ring not
     // refilled: the last slot's barrier completes exactly once), the SM's HBM
@@ -867,6 +882,7 @@ static int launch_dec(DecParams& P, size_t m, bool fused, bool qact, cudaStream_
   const int kpad = P.kblocks * kKBlock;
   const int grid = dec_grid(P.rowtiles);
   P.l2_plain = dec_tuning().l2_plain;
+  P.dbg_nostream = dec_tuning().dbg_nostream;
   // successor prefetch only behind a long stream (measured: +5 % at W4 up_proj,
   // 152 KB per CTA; -1..-5 % for shares <= ~76 KB, profiles/r02_dec_next_sweep.txt)
   const size_t share = static_cast<size_t>(dec_nlrt_max(P.rowtiles, grid)) * P.kblocks * q * 512;

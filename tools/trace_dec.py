@@ -29,6 +29,10 @@ x = torch.from_numpy(x_np).cuda()
 y = torch.empty((m, n), dtype=torch.float16, device="cuda")
 bufs = [torch.zeros(64 * 4096, dtype=torch.int64, device="cuda") for _ in range(L)]
 lib = abq._lib.lib()
+for kv in os.environ.get("ABQ_TUNE", "").split(","):
+    if kv:
+        key, val = kv.split("=")
+        lib.abq_set_tuning(key.encode(), int(val))
 s = torch.cuda.Stream()
 with torch.cuda.stream(s):
     for i in range(L):

@@ -31,6 +31,10 @@ x = torch.from_numpy(x_np).cuda()
 y = torch.empty((m, n), dtype=torch.float16, device="cuda")
 bufs = [torch.zeros(64 * 4096, dtype=torch.int64, device="cuda") for _ in range(L)]
 lib = abq._lib.lib()
+for kv in os.environ.get("ABQ_TUNE", "").split(","):
+    if kv:
+        key, val = kv.split("=")
+        lib.abq_set_tuning(key.encode(), int(val))
 s = torch.cuda.Stream()
 with torch.cuda.stream(s):
     for i in range(L):
@@ -55,8 +59,8 @@ G = len(rows[0])
 rowtiles = (n + 15) // 16
 heavy = np.arange(G) < rowtiles % G
 print(f"{name} ({desc}): {L} launches, {G} CTAs ({heavy.sum()} heavy)")
-cols = (("start", 8), ("prodissued", 15), ("waitret", 12), ("firstdata", 22), ("codes", 13), ("lastdata", 21),
-        ("mainend", 14), ("end", 9))
+cols = (("start", 8), ("prodissued", 15), ("slot0", 41), ("waitret", 12), ("firstdata", 22), ("codes", 13),
+        ("lastdata", 21), ("lastslot", 42), ("mainend", 14), ("end", 9))
 prev_end = None
 steps = []
 for i, t in enumerate(rows):
