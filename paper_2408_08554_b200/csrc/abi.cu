@@ -454,6 +454,7 @@ int abq_set_tuning(const char* key, long long value) {
   else if (k == "dec_grid_balanced") t.grid_balanced = value != 0;
   else if (k == "tc_dbg") t.tc_dbg = static_cast<int>(value);
   else if (k == "tc_tt" && value >= 0) t.tc_tt = static_cast<int>(value);
+  else if (k == "tc_pre" && value >= 0) t.tc_pre = static_cast<int>(value);
   else if (k == "dec_next_kb" && value >= 0) t.next_kb = static_cast<int>(value);
   else if (k == "dec_next_min_kb" && value >= 0) t.next_min_kb = static_cast<int>(value);
   else if (k == "dec_l2_plain") t.l2_plain = value != 0;

@@ -212,7 +212,7 @@ __device__ __forceinline__ void tc_epilogue(const EpiParams& E, uint32_t taddr, 
                                             int n, const double* t_sa, const unsigned* t_za, const unsigned* t_kz,
                                             const unsigned* t_ra, __half* stage, int lch, const double* c_sb,
                                             const int* c_zb, const int* c_cs, bool k32, const uint32_t* part,
-                                            int npart) {
+                                            int npart, int dbg) {
   constexpr bool kRaw = MODE == EPI_ACC_I32 || MODE == EPI_ACC_I64;
   const bool chan_ok = ch < n;
   // per-channel values, staged in shared memory during the k-loop (loaded here
@@ -242,6 +242,16 @@ __device__ __forceinline__ void tc_epilogue(const EpiParams& E, uint32_t taddr, 
           : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
           : "r"(taddr + static_cast<uint32_t>(c0)));
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    if (dbg & 128) {  // timing experiment (results invalid): the accumulator loads dropped
+#pragma unroll
+      for (int i = 0; i < CW; ++i) v[i] = static_cast<uint32_t>(i);
+    }
+    if (dbg & 64) {  // timing experiment (results invalid): no correction / dequant math
+      if (chan_ok && MODE == EPI_F16)
+#pragma unroll
+        for (int i = 0; i < CW; ++i) stage[(c0 + i) * kTcM + lch] = __ushort_as_half(static_cast<unsigned short>(v[i]));
+      continue;
+    }
     // stream-K: the k-ranges of this tile other CTAs accumulated (exact
     // modulo 2^32 like the accumulator itself)
     for (int c = 0; c < npart; ++c)
@@ -349,6 +359,7 @@ struct TcParams {
   unsigned long long* bad_word;  // ReQuant status (~index, 0 = none), published to bad_out
   unsigned long long* bad_out;
   unsigned long long* trace;  // optional [grid][64] clock64 / globaltimer stamps (profiling)
+  int pre_w;                  // weight stages requested before griddepcontrol.wait (the rest behind the activations)
   int dbg;                    // experiments (abq_set_tuning "tc_dbg"): 2 MMA skips the A wait, 4 no UMMA,
                               // 8 no activation TMA, 16 no weight TMA, 32 no widening (results invalid)
   // stream-K (one token tile, grid < rowtiles x kblocks units): CTA b owns the
@@ -525,13 +536,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_con
         bulk_g2s(b_of(s), asrc + static_cast<size_t>(kk) * P.groups * 1024, Sh::kB, &abar[s]);
       };
       const int pre = nU < S ? nU : S;
-      for (int kb = 0; kb < pre; ++kb) issue_w(kb);
+      const int pre_w = P.pre_w > 0 && P.pre_w < pre ? P.pre_w : pre;
+      for (int kb = 0; kb < pre_w; ++kb) issue_w(kb);
       {  // the rest of this CTA's weights: L2 bulk prefetch, so the ring's later
          // weight copies hit L2 instead of waiting on HBM latency
         uint64_t pol;
         asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
         const size_t total = static_cast<size_t>(nU) * WB;
-        for (size_t off = static_cast<size_t>(pre) * WB; off < total; off += 32768)
+        for (size_t off = static_cast<size_t>(pre_w) * WB; off < total; off += 32768)
           asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(wsrc + off),
                        "r"(static_cast<uint32_t>(total - off < 32768 ? total - off : 32768)), "l"(pol)
                        : "memory");
@@ -544,7 +556,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_con
         *P.bad_out = w ? ~w : ~0ull;
         *P.bad_word = 0ull;
       }
-      for (int kb = 0; kb < pre; ++kb) issue_a(kb);
+      // the activation tiles first (they queue behind whatever this SM has
+      // requested), then the weight stages not requested yet
+      for (int kb = 0; kb < pre; ++kb) {
+        issue_a(kb);
+        if (kb + pre_w < pre) issue_w(kb + pre_w);
+      }
       for (int kb = S; kb < nU; ++kb) {
         mbar_wait(&ebar[kb % S], ((kb / S) - 1) & 1);  // MMA of kb - S done with the stage
         if (trace && kb < S + 16) trace[48 + kb - S] = clock64();
@@ -746,12 +763,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_con
     const uint32_t taddr = tlane + (fin_seg == 1 ? static_cast<uint32_t>(TT) : 0u);
     const bool k32 = P.k <= 32768;
     switch (P.e.mode) {
-      case EPI_ACC_I32: tc_epilogue<EPI_ACC_I32, TT>(P.e, taddr, half, tok0, P.m, ch, P.n, t_sa, t_za, t_kz, t_ra, stage, lch, c_sb, c_zb, c_cs, k32, part, npart); break;
-      case EPI_ACC_I64: tc_epilogue<EPI_ACC_I64, TT>(P.e, taddr, half, tok0, P.m, ch, P.n, t_sa, t_za, t_kz, t_ra, stage, lch, c_sb, c_zb, c_cs, k32, part, npart); break;
-      case EPI_F64: tc_epilogue<EPI_F64, TT>(P.e, taddr, half, tok0, P.m, ch, P.n, t_sa, t_za, t_kz, t_ra, stage, lch, c_sb, c_zb, c_cs, k32, part, npart); break;
-      case EPI_F16: tc_epilogue<EPI_F16, TT>(P.e, taddr, half, tok0, P.m, ch, P.n, t_sa, t_za, t_kz, t_ra, stage, lch, c_sb, c_zb, c_cs, k32, part, npart); break;
-      case EPI_F32: tc_epilogue<EPI_F32, TT>(P.e, taddr, half, tok0, P.m, ch, P.n, t_sa, t_za, t_kz, t_ra, stage, lch, c_sb, c_zb, c_cs, k32, part, npart); break;
-      default: tc_epilogue<EPI_CORR_I64, TT>(P.e, taddr, half, tok0, P.m, ch, P.n, t_sa, t_za, t_kz, t_ra, stage, lch, c_sb, c_zb, c_cs, k32, part, npart); break;
+      case EPI_ACC_I32: tc_epilogue<EPI_ACC_I32, TT>(P.e, taddr, half, tok0, P.m, ch, P.n, t_sa, t_za, t_kz, t_ra, stage, lch, c_sb, c_zb, c_cs, k32, part, npart, P.dbg); break;
+      case EPI_ACC_I64: tc_epilogue<EPI_ACC_I64, TT>(P.e, taddr, half, tok0, P.m, ch, P.n, t_sa, t_za, t_kz, t_ra, stage, lch, c_sb, c_zb, c_cs, k32, part, npart, P.dbg); break;
+      case EPI_F64: tc_epilogue<EPI_F64, TT>(P.e, taddr, half, tok0, P.m, ch, P.n, t_sa, t_za, t_kz, t_ra, stage, lch, c_sb, c_zb, c_cs, k32, part, npart, P.dbg); break;
+      case EPI_F16: tc_epilogue<EPI_F16, TT>(P.e, taddr, half, tok0, P.m, ch, P.n, t_sa, t_za, t_kz, t_ra, stage, lch, c_sb, c_zb, c_cs, k32, part, npart, P.dbg); break;
+      case EPI_F32: tc_epilogue<EPI_F32, TT>(P.e, taddr, half, tok0, P.m, ch, P.n, t_sa, t_za, t_kz, t_ra, stage, lch, c_sb, c_zb, c_cs, k32, part, npart, P.dbg); break;
+      default: tc_epilogue<EPI_CORR_I64, TT>(P.e, taddr, half, tok0, P.m, ch, P.n, t_sa, t_za, t_kz, t_ra, stage, lch, c_sb, c_zb, c_cs, k32, part, npart, P.dbg); break;
     }
     if (trace && tid == 0) trace[6] = clock64();
     if (P.e.mode == EPI_F16) {
@@ -895,6 +912,7 @@ int run_gemm_tc(const uint32_t* wtc, unsigned q, size_t n, size_t k, const uint8
   P.e = e;
   P.trace = trace_buffer();
   P.dbg = dec_tuning().tc_dbg;
+  P.pre_w = dec_tuning().tc_pre;
   if (plan.token_tile == 0 && dec_tuning().tc_tt > 0) plan.token_tile = dec_tuning().tc_tt;
   // a TileConfig's schedule (abi.cu plan_of) wins, then an explicit
   // abq_set_gemm_schedule; else the default

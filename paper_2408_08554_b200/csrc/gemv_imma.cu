@@ -112,7 +112,11 @@ static __device__ __noinline__ void act_report_nonfinite(const __half* row, int 
 
 // ROW: write the tcgen05 GEMM's tiled u8 operand (tc_act_offset, `row_ld` =
 // token groups) instead of the GEMV's B-fragment order.
-template <typename T, bool ROW>
+// VR: 16-byte fp16 vectors per thread of the register-resident fast path
+// (4: K <= 8192; 8: K <= 16384, e.g. LLaMA-7B/13B down_proj K = 11008 / 13824;
+// 16: K <= 32768, LLaMA-70B down_proj K = 28672), which otherwise took the
+// generic per-element FP64 path: ~12 us per launch at K = 11008, M = 128.
+template <typename T, bool ROW, int VR>
 __global__ void __launch_bounds__(kActThreads) act_quant_kernel(const T* __restrict__ x, int m, int k, int mt,
                                                                 QuantParams qp, uint32_t* __restrict__ act_frag,
                                                                 int row_ld, double* __restrict__ s_a,
@@ -136,14 +140,14 @@ __global__ void __launch_bounds__(kActThreads) act_quant_kernel(const T* __restr
   const int kzero = ROW ? (k + 127) / 128 * 128 : kpad;
   const T* row = x + static_cast<size_t>(tok) * k;
   if constexpr (sizeof(T) == 2) {
-    // fp16 rows, per token, K % 8 == 0, K <= 8 * 4 * kActThreads: the row is read
+    // fp16 rows, per token, K % 8 == 0, K <= 8 * VR * kActThreads: the row is read
     // once with 16-byte loads and kept in registers (min/max in fp32 is exact
     // for fp16 inputs); codes and sums as in the generic path below.
-    if (!qp.per_tensor && (k & 7) == 0 && k <= 8 * 4 * kActThreads) {
+    if (!qp.per_tensor && (k & 7) == 0 && k <= 8 * VR * kActThreads) {
       const int nvec = k >> 3;
-      uint4 v[4];
+      uint4 v[VR];
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
+      for (int r = 0; r < VR; ++r) {
         const int idx = tid + r * kActThreads;
         v[r] = idx < nvec ? __ldg(reinterpret_cast<const uint4*>(row) + idx) : make_uint4(0u, 0u, 0u, 0u);
       }
@@ -160,7 +164,7 @@ __global__ void __launch_bounds__(kActThreads) act_quant_kernel(const T* __restr
       int lo = 0x7FFFFFFF, hi = static_cast<int>(0x80000000u);
       uint32_t bad = 0;
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
+      for (int r = 0; r < VR; ++r) {
         if (tid + r * kActThreads >= nvec) break;
         bad |= f16x8_nonfinite(v[r]);
         const __half2* h2 = reinterpret_cast<const __half2*>(&v[r]);
@@ -199,7 +203,7 @@ __global__ void __launch_bounds__(kActThreads) act_quant_kernel(const T* __restr
       const int topi = static_cast<int>(qp.levels - 1);
       int rsum = 0;
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
+      for (int r = 0; r < VR; ++r) {
         const int idx = tid + r * kActThreads;
         if (idx >= nvec) break;
         uint32_t w0, w1;
@@ -955,19 +959,27 @@ int run_act_quant(const void* x, int x_dtype, size_t m, size_t k, int mt, const 
                   unsigned long long* bad_word, cudaStream_t st) {
   const dim3 grid(static_cast<unsigned>(m)), block(kActThreads);
   const int im = static_cast<int>(m), ik = static_cast<int>(k);
-#define ABQ_ACTQ(T, ROWL)                                                                                  \
-  act_quant_kernel<T, ROWL><<<grid, block, 0, st>>>(static_cast<const T*>(x), im, ik, mt, qp, out, row_ld, s_a, \
-                                                   z_a, rowsum, bad_word)
+#define ABQ_ACTQ(T, ROWL, VR)                                                                                  \
+  act_quant_kernel<T, ROWL, VR><<<grid, block, 0, st>>>(static_cast<const T*>(x), im, ik, mt, qp, out, row_ld, s_a, \
+                                                       z_a, rowsum, bad_word)
   const bool row = row_ld > 0;
+  // vectors per thread of the fp16 fast path: 4 (K <= 8192), 8 (<= 16384), 16 (<= 32768)
+  const int vr = k <= static_cast<size_t>(8 * 4 * kActThreads) ? 4 : k <= static_cast<size_t>(8 * 8 * kActThreads) ? 8 : 16;
   switch (x_dtype) {
     case ABQ_F16:
-      if (row) ABQ_ACTQ(__half, true); else ABQ_ACTQ(__half, false);
+      if (vr == 16) {
+        if (row) ABQ_ACTQ(__half, true, 16); else ABQ_ACTQ(__half, false, 16);
+      } else if (vr == 8) {
+        if (row) ABQ_ACTQ(__half, true, 8); else ABQ_ACTQ(__half, false, 8);
+      } else {
+        if (row) ABQ_ACTQ(__half, true, 4); else ABQ_ACTQ(__half, false, 4);
+      }
       break;
     case ABQ_F32:
-      if (row) ABQ_ACTQ(float, true); else ABQ_ACTQ(float, false);
+      if (row) ABQ_ACTQ(float, true, 4); else ABQ_ACTQ(float, false, 4);
       break;
     default:
-      if (row) ABQ_ACTQ(double, true); else ABQ_ACTQ(double, false);
+      if (row) ABQ_ACTQ(double, true, 4); else ABQ_ACTQ(double, false, 4);
       break;
   }
 #undef ABQ_ACTQ

@@ -24,6 +24,10 @@ for _ in range(3):
     lins[0](x, out=y, check=False)
 torch.cuda.synchronize()
 lib = abq._lib.lib()
+for kv in os.environ.get("ABQ_TUNE", "").split(","):
+    if kv:
+        key, val = kv.split("=")
+        lib.abq_set_tuning(key.encode(), int(val))
 if len(sys.argv) > 3:
     abq.api.set_gemm_schedule(sys.argv[3])
     for _ in range(3):
