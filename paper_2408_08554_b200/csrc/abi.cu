@@ -126,9 +126,9 @@ int run_gemm_tc(const uint32_t* wtc, unsigned q, size_t n, size_t k, const uint8
                 const EpiParams& e, cudaStream_t st, unsigned long long* bad_word = nullptr,
                 unsigned long long* bad_out = nullptr, bool pdl = false, unsigned* sk_flags = nullptr,
                 uint32_t* sk_part = nullptr, EnginePlan plan = EnginePlan{0, 0});
-size_t tc_sk_flag_bytes(size_t n);
+size_t tc_sk_flag_bytes(size_t n, size_t k);
 int& gemm_schedule();
-size_t tc_sk_part_bytes(size_t m, size_t n);
+size_t tc_sk_part_bytes(size_t m, size_t n, size_t k);
 int run_tile_codes(const uint8_t* src, size_t m, size_t k, uint8_t* dst, cudaStream_t st);
 int run_act_quant(const void* x, int x_dtype, size_t m, size_t k, int mt, const QuantParams& qp,
                   uint32_t* out, int row_ld, double* s_a, int32_t* z_a, long long* rowsum,
@@ -258,9 +258,9 @@ static int gemm_tc_from_planes(const uint64_t* a, unsigned p, size_t m, const ui
   unsigned* flags = nullptr;
   uint32_t* part = nullptr;
   if (!st && plan.schedule == ABQ_GEMM_STREAM_K) {
-    cudaError_t err = cudaMallocAsync(reinterpret_cast<void**>(&flags), tc_sk_flag_bytes(n), s);
-    if (err == cudaSuccess) err = cudaMemsetAsync(flags, 0, tc_sk_flag_bytes(n), s);
-    if (err == cudaSuccess) err = cudaMallocAsync(reinterpret_cast<void**>(&part), tc_sk_part_bytes(m, n), s);
+    cudaError_t err = cudaMallocAsync(reinterpret_cast<void**>(&flags), tc_sk_flag_bytes(n, k), s);
+    if (err == cudaSuccess) err = cudaMemsetAsync(flags, 0, tc_sk_flag_bytes(n, k), s);
+    if (err == cudaSuccess) err = cudaMallocAsync(reinterpret_cast<void**>(&part), tc_sk_part_bytes(m, n, k), s);
     if (err != cudaSuccess) st = fail(ABQ_ERR_CUDA, "gemm_tc: stream-K scratch: %s", cudaGetErrorString(err));
   }
   if (!st) st = run_gemm_tc(wtc, q, n, k, tiled, m, e, s, nullptr, nullptr, false, flags, part, plan);
@@ -455,6 +455,7 @@ int abq_set_tuning(const char* key, long long value) {
   else if (k == "tc_dbg") t.tc_dbg = static_cast<int>(value);
   else if (k == "tc_tt" && value >= 0) t.tc_tt = static_cast<int>(value);
   else if (k == "tc_pre" && value >= 0) t.tc_pre = static_cast<int>(value);
+  else if (k == "tc_sk_ctas" && value >= 2 && value <= 64) t.tc_sk_ctas = static_cast<int>(value);
   else if (k == "dec_next_kb" && value >= 0) t.next_kb = static_cast<int>(value);
   else if (k == "dec_next_min_kb" && value >= 0) t.next_min_kb = static_cast<int>(value);
   else if (k == "dec_l2_plain") t.l2_plain = value != 0;
@@ -750,10 +751,10 @@ size_t abq_linear_workspace_bytes(size_t m, size_t n, size_t k, unsigned act_pla
   // [gacc + gcnt for the stream-K decode GEMV][stream-K GEMM flags][ReQuant report word, 256 B][act planes][s_a][z_a]
   // [rowsum_a][range 256 B][tiled u8 act codes for the tcgen05 GEMM][row-major u8 codes m x k]
   // [stream-K GEMM partial tiles]; everything before the act planes depends on n, k only
-  return align256(imma_ws_bytes(n, k)) + align256(tc_sk_flag_bytes(n)) + 256 +
+  return align256(imma_ws_bytes(n, k)) + align256(tc_sk_flag_bytes(n, k)) + 256 +
          align256(size_t(act_planes) * m * wpr_of(k) * 8) + align256(m * 8) + align256(m * 4) +
          align256(m * 8) + 256 + align256(tc_act_bytes(m, k)) + align256(m * k) +
-         align256(tc_sk_part_bytes(std::min<size_t>(m, 256), n));
+         align256(tc_sk_part_bytes(std::min<size_t>(m, 256), n, k));
   // (the stream-K partial tiles are sized for min(m, 256) tokens: the GEMM only
   // runs stream-K up to 256 tokens, and the total must not shrink as m grows,
   // so a workspace sized for max_m serves every m <= max_m)
@@ -777,7 +778,7 @@ int abq_linear(const void* x, int x_dtype, size_t m, size_t k, const abq_quant_s
   void* ws_imma = ws;
   ws += align256(imma_ws_bytes(w->n, k));
   unsigned* sk_flags = reinterpret_cast<unsigned*>(ws);
-  ws += align256(tc_sk_flag_bytes(w->n));
+  ws += align256(tc_sk_flag_bytes(w->n, k));
   // zero between calls; at an offset independent of m (the regions after it
   // move with m and hold data of earlier calls)
   unsigned long long* bad_word = reinterpret_cast<unsigned long long*>(ws);

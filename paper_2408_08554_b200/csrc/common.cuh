@@ -28,6 +28,7 @@ struct DecTuning {
   int tc_dbg = 0;    // prefill GEMM: experiment switches (tools/trace_gemm.py), 0 in production
   int tc_tt = 0;     // prefill GEMM: token-tile cap for the serving path (0 = by M)
   int tc_pre = 0;    // prefill GEMM: weight stages requested before the PDL wait (0 = the whole ring)
+  int tc_sk_ctas = 2;  // prefill GEMM stream-K: CTAs per row-tile (grid = min(SMs, this x row-tiles))
   int next_kb = 64;  // decode GEMV: KB per CTA of the successor layer prefetched into L2 in the tail (0 = off)
   int next_min_kb = 128;  // ... only when this layer's per-CTA weight share is at least this long
   int l2_plain = 0;  // decode GEMV: weight TMA without the L2 evict-first hint

@@ -368,8 +368,9 @@ struct TcParams {
   // (at most 2) publish partial accumulators + a flag.  Flags are zero
   // between launches (the finisher resets them).
   int sk;
-  unsigned* sk_flags;  // [rowtiles][2]
-  uint32_t* sk_part;   // [rowtiles][2][TT][128]
+  unsigned* sk_flags;  // [rowtiles][sk_slots]
+  uint32_t* sk_part;   // [rowtiles][sk_slots][TT][128]
+  int sk_slots;        // CTAs that can share one tile (tc_sk_slots)
 };
 
 // stream-K workspace: flags (zero-filled once by the caller, at an offset that
@@ -380,14 +381,33 @@ int& gemm_schedule() {
   return s;
 }
 
-size_t tc_sk_flag_bytes(size_t n) { return (n + kTcM - 1) / kTcM * 2 * 4; }
+// Stream-K grid: G = min(SMs, c x rowtiles, T) CTAs for T = rowtiles x kblocks
+// units, c = tc_sk_ctas (abq_set_tuning "tc_sk_ctas", default 2).  G >= rowtiles
+// keeps every CTA's range <= kblocks: <= 2 segments, the first finishing a
+// tile, the last contributing to one.  A tile is shared by at most
+// ceil(kblocks / floor(T / G)) + 1 CTAs: its slots in the flag and
+// partial-tile arrays.  Measured (profiles/r02_gemm_n4096.txt): every SM
+// (c = 5 at N = 4096) halves the k-loop but the finisher then sums 4-5
+// partial tiles from L2 on its tail (o_proj M=128 17.7 -> 21.7 us), so c = 2.
+constexpr size_t kSkMaxRowtiles = 160;
+int tc_sk_grid(long long rowtiles, long long kblocks) {
+  const long long c = std::max(2, dec_tuning().tc_sk_ctas);
+  return static_cast<int>(std::min<long long>(std::min<long long>(num_sms(), c * rowtiles), rowtiles * kblocks));
+}
+int tc_sk_slots(size_t n, size_t k) {
+  const long long rt = static_cast<long long>((n + kTcM - 1) / kTcM), kb = static_cast<long long>((k + kTcK - 1) / kTcK);
+  const long long T = rt * kb, G = tc_sk_grid(rt, kb);
+  if (G <= 0) return 2;
+  const long long per = std::max<long long>(1, T / G);
+  return static_cast<int>(std::max<long long>(2, (kb + per - 1) / per + 1));
+}
+size_t tc_sk_flag_bytes(size_t n, size_t k) { return (n + kTcM - 1) / kTcM * tc_sk_slots(n, k) * 4; }
 // stream-K only runs with fewer row-tiles than SMs; layers wider than this
 // never need partial tiles (keeps the per-layer workspace small)
-constexpr size_t kSkMaxRowtiles = 160;
-size_t tc_sk_part_bytes(size_t m, size_t n) {
+size_t tc_sk_part_bytes(size_t m, size_t n, size_t k) {
   if (m == 0 || m > 256 || (n + kTcM - 1) / kTcM > kSkMaxRowtiles) return 0;
   const size_t tt = m <= 16 ? 16 : m <= 32 ? 32 : m <= 64 ? 64 : m <= 128 ? 128 : 256;
-  return (n + kTcM - 1) / kTcM * 2 * tt * kTcM * 4;
+  return (n + kTcM - 1) / kTcM * tc_sk_slots(n, k) * tt * kTcM * 4;
 }
 
 // Shared memory: an input ring of kS stages -- the packed weights of a
@@ -727,26 +747,26 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_con
     if (con_seg >= 0) {
       const int tcon = t0 + con_seg, slot = static_cast<int>(blockIdx.x) - cta_of(static_cast<long long>(tcon) * nkb);
       tc_store_partial<TT>(tlane + (con_seg ? static_cast<uint32_t>(TT) : 0u), half, lch,
-                           P.sk_part + (static_cast<size_t>(tcon) * 2 + slot) * TT * kTcM);
+                           P.sk_part + (static_cast<size_t>(tcon) * P.sk_slots + slot) * TT * kTcM);
       __syncthreads();
       if (tid == 0) {
         __threadfence();
-        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(P.sk_flags + tcon * 2 + slot), "r"(1u) : "memory");
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(P.sk_flags + tcon * P.sk_slots + slot), "r"(1u) : "memory");
         if (trace) trace[10] = clock64();
       }
     }
     if (rt >= 0) {
       npart = static_cast<int>(blockIdx.x) - cta_of(static_cast<long long>(rt) * nkb);
-      part = P.sk_part + static_cast<size_t>(rt) * 2 * TT * kTcM;
+      part = P.sk_part + static_cast<size_t>(rt) * P.sk_slots * TT * kTcM;
       if (tid == 0) {
         for (int c = 0; c < npart; ++c) {
           unsigned f = 0;
           for (;;) {
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(P.sk_flags + rt * 2 + c) : "memory");
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(P.sk_flags + rt * P.sk_slots + c) : "memory");
             if (f) break;
             __nanosleep(64);
           }
-          P.sk_flags[rt * 2 + c] = 0u;  // consumed: zero for the next launch
+          P.sk_flags[rt * P.sk_slots + c] = 0u;  // consumed: zero for the next launch
         }
         if (trace) {
           trace[11] = clock64();
@@ -852,13 +872,16 @@ static int launch_tc(const TcParams& P, bool pdl, cudaStream_t st) {
   TcParams L = P;
   const int gy = (P.m + TT - 1) / TT;
   int gx = P.rowtiles;
-  // stream-K when one token tile leaves SMs idle: G = min(SMs, 2 x row-tiles)
-  // CTAs share the (row-tile, k-block) units; G <= 2 rowtiles keeps every
-  // range >= kblocks / 2 (<= 2 contributors per tile), G > rowtiles keeps it
-  // <= kblocks (<= 2 segments per CTA)
+  // stream-K when one token tile leaves SMs idle: G = min(SMs, units) CTAs
+  // (tc_sk_grid) share the (row-tile, k-block) units, tc_sk_slots CTAs per tile
+  // at most.  Finishers spin on their contributors, so every CTA must become
+  // resident: G <= SMs with one CTA per SM, and this kernel never triggers its
+  // dependents early (no griddepcontrol.launch_dependents: a dependent grid
+  // waiting on this one cannot hold an SM a contributor needs).
   if (L.sk && gy == 1 && P.kblocks >= 2 && P.rowtiles < num_sms() &&
       static_cast<size_t>(P.rowtiles) <= kSkMaxRowtiles) {
-    gx = std::min(num_sms(), 2 * P.rowtiles);
+    gx = tc_sk_grid(P.rowtiles, P.kblocks);
+    L.sk_slots = tc_sk_slots(static_cast<size_t>(P.n), static_cast<size_t>(P.k));
   } else {
     L.sk = 0;
   }
