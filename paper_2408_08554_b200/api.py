@@ -1006,6 +1006,33 @@ class HostLinear:
         return self.y_host
 
 
+class GraphedHostLinear:
+    """HostLinear's step captured as a CUDA graph: one replay per step runs the
+    stage-in kernel (pinned x read over PCIe into HBM) and the engine linear
+    whose epilogue writes y into pinned host memory -- no copy nodes, and no
+    per-step host launch cost beyond one graph launch.  step() replays it; the
+    caller synchronises before reading y_host."""
+
+    def __init__(self, lin: "Linear", m: int, x_dtype=torch.float16, out_dtype=torch.float16):
+        # the HostLinear is bound to the stream current at construction: build,
+        # warm up and capture it on one side stream
+        self._s = torch.cuda.Stream()
+        self._s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(self._s):
+            self.host = HostLinear(lin, m, x_dtype, out_dtype)
+            self.host.step()
+        self._s.synchronize()
+        self.x_host, self.y_host = self.host.x_host, self.host.y_host
+        self.h2d_bytes, self.d2h_bytes = self.host.h2d_bytes, self.host.d2h_bytes
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, stream=self._s):
+            self.host.step()
+
+    def step(self) -> torch.Tensor:
+        self.graph.replay()
+        return self.y_host
+
+
 class GraphedLinear:
     """Serving entry point: one decode/prefill step of a Linear captured as a
     CUDA graph together with its host I/O -- H2D of the activations from a

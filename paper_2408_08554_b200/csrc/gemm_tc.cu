@@ -904,6 +904,14 @@ static int launch_tc(const TcParams& P, bool pdl, cudaStream_t st) {
 
 template <int Q>
 static int launch_tt(const TcParams& P, bool pdl, cudaStream_t st, int tt_cap) {
+  // Narrow layers with short K (LLaMA-7B o_proj N = K = 4096 at M = 128): 32-token
+  // tiles fill one wave of SMs (32 row-tiles x 4 token tiles) where one
+  // 128-token tile per row-tile leaves 116 SMs idle or hands partial tiles
+  // around (stream-K): 17.0 -> 15.5 us (profiles/r02_gemm_tt_sweep.txt).  Longer
+  // K (down_proj) and wide N lose with it (each CTA widens the whole weight tile).
+  if (tt_cap <= 0 && P.m > 32 && P.kblocks <= 32 &&
+      static_cast<long long>(P.rowtiles) * ((P.m + 31) / 32) <= num_sms())
+    tt_cap = 32;
   const int cap = tt_cap > 0 ? std::max(16, tt_cap) : 256;  // TileConfig BM cap (abi.cu plan_of)
   if (P.m <= 16 || cap <= 16) return launch_tc<Q, 16>(P, pdl, st);
   if (P.m <= 32 || cap <= 32) return launch_tc<Q, 32>(P, pdl, st);

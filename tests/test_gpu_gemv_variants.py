@@ -231,6 +231,25 @@ def test_host_linear_end_to_end(abq, orc, m, n, k, wb, ab):
         assert np.array_equal(h.y_host.numpy(), want)
 
 
+@pytest.mark.parametrize("m,n,k,wb,ab", [(1, 11008, 4096, 4, 4), (16, 512, 2048, 4, 4)])
+def test_graphed_host_linear_end_to_end(abq, orc, m, n, k, wb, ab):
+    """GraphedHostLinear.step(): HostLinear's step replayed from a CUDA graph;
+    new host activations written between replays are picked up (the graph
+    reads the pinned buffer), each result equals the oracle."""
+    rng = np.random.default_rng(7 * m + n)
+    x, wc, sb, zb = _case(rng, m, n, k, wb, ab)
+    w = abq.PackedWeights.from_planes(abq.bitpack(wc, wb), sb, zb)
+    g = abq.GraphedHostLinear(abq.Linear(w, abq.QuantSpec(bits=ab, granularity=abq.api.PER_TOKEN), max_m=m), m)
+    for rep in range(3):
+        x = (rng.standard_normal((m, k)) * (rep + 1)).astype(np.float16)
+        g.x_host.copy_(torch.from_numpy(x))
+        g.step()
+        torch.cuda.synchronize()
+        ac, sa, za = orc.quantize(x.astype(np.float64), ab, 0, 2)
+        want = orc.quantized_linear(ac, ab, sa, za, wc, wb, sb, zb).astype(np.float16)
+        assert np.array_equal(g.y_host.numpy(), want), rep
+
+
 def test_prefetch_next_hint_is_transparent(abq, orc):
     """abq_weights.next (Linear.prefetch_next): a cycle of decode layers of
     different shapes and bit widths, each hinting its successor (the tail L2

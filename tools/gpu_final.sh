@@ -16,3 +16,4 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemv
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemm_tc -s 5 -c 1 -f -o $O/${TAG}_gemm \
   python bench.py --workload cfg2_w4a4_m128 --steps 10 --warmup 3 --no-cpu --no-check --no-parts > $O/${TAG}_ncu_gemm.log 2>&1
 echo done
+timeout 1200 python bench.py --workload cfg3_sweep --steps 200 --warmup 10 > $O/${TAG}_cfg3_sweep.json 2> $O/${TAG}_cfg3_sweep.err
