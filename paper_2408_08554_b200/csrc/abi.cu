@@ -458,6 +458,7 @@ int abq_set_tuning(const char* key, long long value) {
   else if (k == "tc_sk_ctas" && value >= 2 && value <= 64) t.tc_sk_ctas = static_cast<int>(value);
   else if (k == "dec_next_kb" && value >= 0) t.next_kb = static_cast<int>(value);
   else if (k == "dec_next_min_kb" && value >= 0) t.next_min_kb = static_cast<int>(value);
+  else if (k == "dec_next_at" && value >= 1 && value <= 100) t.next_at = static_cast<int>(value);
   else if (k == "dec_l2_plain") t.l2_plain = value != 0;
   else if (k == "dec_dbg_nostream") t.dbg_nostream = value != 0;
   else if (k == "reset") t = DecTuning{};

@@ -31,6 +31,7 @@ struct DecTuning {
   int tc_sk_ctas = 2;  // prefill GEMM stream-K: CTAs per row-tile (grid = min(SMs, this x row-tiles))
   int next_kb = 64;  // decode GEMV: KB per CTA of the successor layer prefetched into L2 in the tail (0 = off)
   int next_min_kb = 128;  // ... only when this layer's per-CTA weight share is at least this long
+  int next_at = 100;      // ... issued once this percentage of the CTA's share has landed
   int l2_plain = 0;  // decode GEMV: weight TMA without the L2 evict-first hint
   int dbg_nostream = 0;  // decode GEMV, TRACE build only: no weight stream (timing experiment, results invalid)
 };

@@ -73,7 +73,7 @@ struct DecParams {
   // (same row-tile split as its own launch) and the bytes per CTA prefetched
   // into L2 once this CTA's stream has landed
   const unsigned char* nx;
-  int nx_rowtiles, nx_kblocks, nx_unit, nx_grid, nx_bytes;
+  int nx_rowtiles, nx_kblocks, nx_unit, nx_grid, nx_bytes, nx_at;
   int l2_plain;  // weight TMA without the L2 evict-first hint (sweeps)
   int dbg_nostream;  // TRACE build timing experiment: ring barriers arrive without data
   unsigned long long* trace;  // ABQ_TRACE build only: [grid][64] stamps
@@ -294,7 +294,7 @@ __global__ void __launch_bounds__(kDecBlock, kDecCtasPerSm) gemv_dec_kernel(cons
     // share the next layer's CTA with this index will stream are requested
     // into L2 now (same split as that launch: rt_first / nlrt below).
     if (P.nx && lane == 0 && nsl > 0 && nsl <= S && static_cast<int>(blockIdx.x) < P.nx_grid) {
-      mbar_wait_parity(&full[nsl - 1], 0);
+      mbar_wait_parity(&full[max(0, (nsl * P.nx_at + 99) / 100 - 1)], 0);  // nx_at % of the share landed
       const int gn = P.nx_grid, base = P.nx_rowtiles / gn, hv = P.nx_rowtiles - base * gn;
       const int b = blockIdx.x;
       const int rf = b < hv ? b * (base + 1) : hv + b * base;
@@ -893,6 +893,7 @@ static int launch_dec(DecParams& P, size_t m, bool fused, bool qact, cudaStream_
     P.nx_unit = static_cast<int>(nx->q) * 512;
     P.nx_grid = dec_grid(P.nx_rowtiles);
     P.nx_bytes = dec_tuning().next_kb * 1024;
+    P.nx_at = std::min(100, std::max(1, dec_tuning().next_at));
   }
   const int nl = dec_nlrt_max(P.rowtiles, grid);
   P.slots = dec_slots(q, n, k, mt, grid);
